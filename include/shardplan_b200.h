@@ -1,0 +1,273 @@
+/*
+ * shardplan_b200.h — C-ABI of the B200-native embedding hot path that
+ * DreamShard (arXiv 2210.02023) places and costs.
+ *
+ * The reference (`shardplan`, header-only C++20 under
+ * /root/reference/proj/include/shardplan/) fakes GPU execution with a
+ * closed-form cost oracle. This library executes the same four stages for
+ * real on B200 GPUs and returns them in the reference's own shape:
+ *
+ *   fwd_comp  sum-pooled EmbeddingBag forward         (oracle.hpp:163-174)
+ *   fwd_comm  all-to-all of pooled vectors             (oracle.hpp:178-185)
+ *   bwd_comm  all-to-all of pooled-vector gradients    (oracle.hpp:178-185)
+ *   bwd_comp  sort/segment sparse row-wise SGD         (oracle.hpp:149)
+ *
+ * composed exactly as CostOracle::evaluate_placement composes them
+ * (oracle.hpp:222-227): overall = max fwd + fwd stage + bwd stage + max bwd.
+ *
+ * It also exports the batched on-GPU evaluator of DreamShard's cost network
+ * (costnet.hpp) and policy network (policy.hpp) used by Alg. 2 `infer`
+ * (harness.hpp:332-356) and by estimated-MDP rollouts.
+ *
+ * Conventions:
+ *  - plain pointers and sizes only; HOST pointers unless a name says _dev;
+ *  - every function returns an int status: 0 = ok, else ErrorKind + 1
+ *    (error.hpp:11-22), plus SP_ERR_CUDA / SP_ERR_NCCL for device failures;
+ *    the message is available from sp_last_error();
+ *  - handles are opaque and owned by the caller; calls on one handle are not
+ *    thread-safe, several handles may coexist (mdp.hpp:28-34 providers are
+ *    single-threaded per environment).
+ */
+#ifndef SHARDPLAN_B200_H_
+#define SHARDPLAN_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SP_ABI_VERSION 1
+#define SP_NUM_BINS 17      /* table.hpp:26 kNumBins */
+#define SP_NUM_FEATURES 21  /* table.hpp:28 kNumFeatures */
+#define SP_NCCL_ID_BYTES 128
+
+/* Status codes: ErrorKind (error.hpp:11-22) + 1. */
+enum sp_status {
+  SP_OK = 0,
+  SP_ERR_INFEASIBLE = 1,
+  SP_ERR_MEMORY_VIOLATION = 2,
+  SP_ERR_MALFORMED_BATCH = 3,
+  SP_ERR_BAD_SPEC = 4,
+  SP_ERR_UNKNOWN_TABLE = 5,
+  SP_ERR_TOO_LARGE = 6,
+  SP_ERR_ILLEGAL_ACTION = 7,
+  SP_ERR_SHAPE_MISMATCH = 8,
+  SP_ERR_NO_LEGAL_ACTION = 9,
+  SP_ERR_BAD_INPUT = 10,
+  SP_ERR_CUDA = 11,
+  SP_ERR_NCCL = 12
+};
+
+/* One embedding table; field-for-field shardplan::TableDesc
+ * (table.hpp:45-52). `table_size_gb` uses the caller's bytes_per_param
+ * (table.hpp:55-63); this library stores fp32 rows (4 B/param). */
+typedef struct sp_table_spec {
+  int32_t id;
+  int32_t dim;
+  int64_t hash_size;
+  double pooling_factor;
+  double table_size_gb;
+  double dist[SP_NUM_BINS];
+} sp_table_spec;
+
+/* shardplan::CostBreakdown (oracle.hpp:105-116) without the trace events
+ * (they are a pure function of these numbers, oracle.hpp:229-238). The
+ * three per-device arrays are caller-owned and hold num_devices entries. */
+typedef struct sp_breakdown {
+  double* fwd_ms;
+  double* bwd_ms;
+  double* comm_ms; /* per-device all-to-all time (max of fwd/bwd exchange) */
+  double fwd_comm_stage_ms;
+  double bwd_comm_stage_ms;
+  double overall_ms;
+} sp_breakdown;
+
+typedef struct sp_ctx sp_ctx;       /* one rank's shard of a placement */
+typedef struct sp_evaluator sp_evaluator; /* cost/policy nets on one GPU */
+
+/* ------------------------------------------------------------------ */
+/* Library                                                              */
+
+int sp_abi_version(void);
+/* Message of the last failure on this thread (any handle). */
+const char* sp_last_error(void);
+/* Number of kernels this library has launched on this thread's handles
+ * since load (CUB/NCCL internal launches excluded). */
+uint64_t sp_kernel_launches(void);
+/* Page-locked host buffers for the LookupBatch upload (cudaHostAlloc). */
+int sp_host_alloc(uint64_t bytes, void** out);
+void sp_host_free(void* p);
+
+/* ------------------------------------------------------------------ */
+/* Embedding shard context — replaces CostOracle::evaluate_placement
+ * (oracle.hpp:187-240) with a measured iteration.                      */
+
+/* NCCL unique id for a multi-rank context; rank 0 calls it and the caller
+ * broadcasts the bytes (e.g. with torch.distributed). */
+int sp_nccl_unique_id(uint8_t out_id[SP_NCCL_ID_BYTES]);
+
+/* Creates rank `rank`'s shard of `placement` (length num_tables, entries in
+ * [0, num_devices), oracle.hpp:75-76).
+ *  - world_size == num_devices: one process per GPU, all-to-all over NCCL
+ *    (nccl_id from sp_nccl_unique_id, NULL when num_devices == 1);
+ *  - world_size == 1 < num_devices: emulation — all num_devices virtual
+ *    devices live on this GPU and run back to back; their per-device
+ *    compute is measured for real, the exchange is a device-local copy of
+ *    the same layout (reported, not NVLink).
+ * batch_size must be divisible by num_devices. Validates the
+ * placement like evaluate_placement (oracle.hpp:190-204) against
+ * mem_cap_gb (<= 0 disables the cap). */
+int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
+                  int32_t num_devices, const int32_t* placement,
+                  int32_t batch_size, double mem_cap_gb, float lr,
+                  int32_t rank, int32_t world_size, const uint8_t* nccl_id,
+                  int32_t cuda_device, sp_ctx** out);
+void sp_ctx_destroy(sp_ctx* ctx);
+
+/* cudaStream_t the context launches on (as void*). */
+int sp_ctx_stream(sp_ctx* ctx, void** stream);
+/* Bytes of device memory held by the context. */
+int sp_ctx_device_bytes(sp_ctx* ctx, uint64_t* bytes);
+/* Local (this rank's) table ids in ascending order; returns the count via
+ * n_out; `ids` may be NULL to query the count. */
+int sp_ctx_local_tables(sp_ctx* ctx, int32_t* ids, int32_t* n_out);
+
+/* Table weights. Deterministic init w = 0.5 + 0.5*u(seed, table, row, col)
+ * (SURVEY §8d), or explicit fp32 rows [hash_size, dim] row-major. */
+int sp_init_tables(sp_ctx* ctx, uint64_t seed);
+int sp_set_table(sp_ctx* ctx, int32_t table_id, const float* rows);
+int sp_get_table(sp_ctx* ctx, int32_t table_id, float* rows);
+
+/* Lookup batch in the reference layout, shardplan::LookupBatch
+ * (table.hpp:158-165): offsets[num_tables*B + 1], indices[offsets.back()],
+ * ordered by (table_id, batch_offset). Host pointers. The local tables'
+ * segments are copied to the device and narrowed to 32-bit; validated like
+ * validate_batch (table.hpp:167-184) plus 0 <= index < hash_size. */
+int sp_upload_batch(sp_ctx* ctx, const int64_t* offsets, int64_t offsets_len,
+                    const int64_t* indices, int64_t indices_len);
+/* Same batch, generated on the device by the SURVEY §8d generator. */
+int sp_synth_batch(sp_ctx* ctx, uint64_t seed);
+/* Number of local lookup indices of the current batch. */
+int sp_batch_nnz(sp_ctx* ctx, int64_t* nnz);
+
+/* Stage entry points (asynchronous on the context stream). */
+int sp_forward(sp_ctx* ctx);
+int sp_a2a_forward(sp_ctx* ctx);
+int sp_a2a_backward(sp_ctx* ctx);
+int sp_backward_sgd(sp_ctx* ctx);
+
+/* Gradient of this rank's pooled outputs, [B/num_devices, W_total] fp32
+ * (W_total = sum of all dims, columns in global table-id order). With
+ * emulation (world_size 1) the rank owns the whole batch [B, W_total]. */
+int sp_set_grad(sp_ctx* ctx, const float* grad);
+int sp_synth_grad(sp_ctx* ctx, uint64_t seed);
+/* Pooled outputs after sp_a2a_forward, same layout as the gradient. */
+int sp_get_pooled(sp_ctx* ctx, float* pooled);
+/* Pooled outputs of (virtual) device `dev` before the exchange,
+ * [B, W_dev] (W_dev = sum of dev's dims, its tables in ascending id order).
+ * In NCCL mode dev must be this rank. */
+int sp_get_local_pooled(sp_ctx* ctx, int32_t dev, float* pooled);
+
+/* Backward internals for bit-exact checks: runs the key
+ * build, the stable radix sort and the segment-head selection of (virtual)
+ * device `dev` (this rank in NCCL mode) on the current batch and returns
+ * the sorted keys (local row base + row, tables in ascending id order), the
+ * bag payload, and the run heads (first position of each run). Pass NULL
+ * arrays to query the sizes. */
+int sp_get_sorted(sp_ctx* ctx, int32_t dev, uint32_t* keys, uint32_t* bags,
+                  int64_t* n_keys, uint32_t* seg_heads, int64_t* n_unique);
+
+/* One full measured iteration: fwd -> fwd a2a -> bwd a2a -> bwd SGD with
+ * per-stage CUDA events; fills `out` like evaluate_placement
+ * (oracle.hpp:206-227). Synchronizes the stream. In NCCL mode the per-device
+ * arrays hold every rank's numbers (gathered), identical on all ranks. */
+int sp_run_iteration(sp_ctx* ctx, sp_breakdown* out);
+/* Enqueue one iteration without events or host sync (for timing loops and
+ * CUDA-graph capture). */
+int sp_enqueue_iteration(sp_ctx* ctx);
+/* Capture sp_enqueue_iteration into a CUDA graph and replay it `iters`
+ * times; 0 iters only builds the graph. Reports kernel nodes per graph. */
+int sp_graph_replay(sp_ctx* ctx, int32_t iters, int32_t* kernels_per_iter);
+
+/* Algorithmic bytes of one launch of each stage on this rank:
+ * [0]=fwd (K1) [1]=a2a send per direction [2]=bwd floor (K4, sort
+ * excluded) [3]=sort traffic estimate. */
+int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]);
+
+/* ------------------------------------------------------------------ */
+/* Ingest — ingest_lookup_batch (table.hpp:188-232) on the GPU.         */
+
+/* Per table: pooling_factor = total/B, dist[17] = access-count histogram
+ * normalised by total; table_size_gb from bytes_per_param. Bit-exact with
+ * the reference. Host LookupBatch in, TableDesc-shaped specs out. */
+int sp_ingest_lookup_batch(const int64_t* offsets, int64_t offsets_len,
+                           const int64_t* indices, int64_t indices_len,
+                           int32_t num_tables, int32_t batch_size,
+                           const int32_t* dims, const int64_t* hash_sizes,
+                           int32_t bytes_per_param, int32_t cuda_device,
+                           sp_table_spec* out_tables);
+
+/* ------------------------------------------------------------------ */
+/* Batched cost/policy evaluator (costnet.hpp, policy.hpp).             */
+
+/* Parameters in the reference's flat Mlp layout [W0 (out x in row-major),
+ * b0, W1, b1, ...] (nn.hpp:21-53), fp64 exactly as the DSHD checkpoint
+ * stores them (checkpoint.hpp:135-142). Sizes are fixed by the reference:
+ * cost.table 21-128-32, cost heads 32-64-1 (x4: fwd, bwd, comm, overall),
+ * policy.table 21-128-32, policy.cost 3-64-32, policy.head 64-1. */
+typedef struct sp_nets {
+  const double* cost_table;   /* 6944  */
+  const double* cost_fwd;     /* 2177  */
+  const double* cost_bwd;     /* 2177  */
+  const double* cost_comm;    /* 2177  */
+  const double* cost_overall; /* 2177  */
+  const double* pol_table;    /* 6944  */
+  const double* pol_cost;     /* 2336  */
+  const double* pol_head;     /* 65    */
+  const double* feature_mean; /* 21 */
+  const double* feature_std;  /* 21 */
+  const double* feature_mask; /* 21, 0/1 */
+  int32_t reduction_tables;   /* 0 sum, 1 mean, 2 max (costnet.hpp:31) */
+  int32_t reduction_devices;
+} sp_nets;
+
+/* Binds the nets and one placement task (tables, D, mem cap) to a GPU:
+ * builds the normalised feature rows (table.hpp:89-104 with the
+ * checkpoint's stats), the cached table representations of both nets
+ * (costnet.hpp:456-464, policy.hpp:121-131) and the predicted visit order
+ * (harness.hpp:131-137). */
+int sp_evaluator_create(const sp_nets* nets, const sp_table_spec* tables,
+                        int32_t num_tables, int32_t num_devices,
+                        double mem_cap_gb, int32_t cuda_device,
+                        sp_evaluator** out);
+void sp_evaluator_destroy(sp_evaluator* ev);
+/* The visit order predicted_order() yields (length num_tables). */
+int sp_evaluator_order(sp_evaluator* ev, int32_t* order);
+
+/* EstimatedCostProvider::overall (costnet.hpp:479-496) for n_cand complete
+ * placements [n_cand, num_tables]: the RAW overall prediction, plus
+ * optionally the clamped per-device q [n_cand, D, 3] (costnet.hpp:466-477).
+ * fp32 on the GPU. */
+int sp_eval_batch(sp_evaluator* ev, const int32_t* placements, int32_t n_cand,
+                  float* overall, float* q);
+
+/* n_cand rollouts of the policy on the estimated MDP (PlacementEnv over
+ * EstimatedCostProvider, mdp.hpp:140-159) in the predicted order.
+ * mode 0 = greedy (infer, harness.hpp:340-346), mode 1 = sampled with one
+ * uniform per step from uniforms[n_cand, num_tables] (policy.hpp:156-169).
+ * Outputs placements [n_cand, num_tables], predicted overall (raw,
+ * costnet.hpp:479-496) per candidate, and a status per candidate
+ * (0 ok, SP_ERR_INFEASIBLE when some table fits nowhere).
+ * precision 0: fp32 with an fp64 re-run of every candidate whose decision
+ * margin fell under 1e-4 relative; 1: fp64 throughout; 2: fp32 only. */
+int sp_rollout_batch(sp_evaluator* ev, int32_t mode, const double* uniforms,
+                     int32_t n_cand, int32_t precision, int32_t* placements,
+                     double* predicted, int32_t* status, int32_t* n_refined);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SHARDPLAN_B200_H_ */

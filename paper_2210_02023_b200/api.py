@@ -1,0 +1,643 @@
+"""Host-side mirror of the reference's interface for the embedding hot path.
+
+The reference (`shardplan`, C++ headers under proj/include/shardplan) fakes
+GPU execution with CostOracle. This module keeps its names, argument meaning
+and error behaviour, and routes every computation through the CUDA library
+(`_shardplan_b200.so`, C-ABI in include/shardplan_b200.h):
+
+  TableDesc, table_memory_gb ............ table.hpp:45-63
+  LookupBatch, validate_batch ........... table.hpp:158-184
+  ingest_lookup_batch ................... table.hpp:188-232   (GPU, K5)
+  PlacementTask, Placement, CostBreakdown oracle.hpp:68-116
+  EmbeddingShard.run_iteration .......... oracle.hpp:187-240  (GPU K1-K4)
+  CostProvider / MeasuredCostProvider ... mdp.hpp:28-54
+  Checkpoint / load_checkpoint .......... checkpoint.hpp:26-217
+  Evaluator, infer ...................... costnet.hpp:454-515, policy.hpp:87-184,
+                                          harness.hpp:112-137, 332-356 (GPU K6/K7)
+
+There is no CPU fallback: a missing library raises ImportError.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import struct
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from ._lib import SpBreakdown, SpNets, SpTableSpec, ShardplanError, check, lib
+
+NUM_BINS = 17
+NUM_FEATURES = 21
+DEFAULT_BATCH_SIZE = 65536
+DEFAULT_BYTES_PER_PARAM = 2
+
+__all__ = [
+    "TableDesc", "table_memory_gb", "LookupBatch", "validate_batch", "PlacementTask",
+    "CostBreakdown", "TraceEvent", "EmbeddingShard", "CostProvider",
+    "MeasuredCostProvider", "ingest_lookup_batch", "compute_feature_stats", "Checkpoint",
+    "load_checkpoint", "Evaluator", "infer", "ShardplanError", "nccl_unique_id",
+    "hot_mass", "HostBuffer",
+]
+
+
+# ---------------------------------------------------------------------------
+# table.hpp
+
+@dataclass
+class TableDesc:
+    """shardplan::TableDesc (table.hpp:45-52)."""
+
+    id: int = 0
+    dim: int = 1
+    hash_size: int = 1
+    pooling_factor: float = 0.0
+    table_size_gb: float = 0.0
+    dist: List[float] = field(default_factory=lambda: [0.0] * NUM_BINS)
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "TableDesc":
+        return cls(int(d["id"]), int(d["dim"]), int(d["hash_size"]),
+                   float(d["pooling_factor"]), float(d["table_size_gb"]),
+                   [float(x) for x in d["dist"]])
+
+    def to_dict(self) -> dict:
+        return {"id": self.id, "dim": self.dim, "hash_size": self.hash_size,
+                "pooling_factor": self.pooling_factor, "table_size_gb": self.table_size_gb,
+                "dist": list(self.dist)}
+
+
+def table_memory_gb(hash_size: int, dim: int, bytes_per_param: int = DEFAULT_BYTES_PER_PARAM):
+    """table.hpp:55-63: rows * columns * bytes per parameter / 2^30."""
+    return float(hash_size) * dim * bytes_per_param / (1024.0 * 1024.0 * 1024.0)
+
+
+def hot_mass(t: TableDesc) -> float:
+    """oracle.hpp:119-123: access mass in bins whose lower edge is >= 8."""
+    h = 0.0
+    for b in range(4, NUM_BINS):
+        h += t.dist[b]
+    return h
+
+
+def _specs(tables: Sequence[TableDesc]):
+    arr = (SpTableSpec * max(len(tables), 1))()
+    for i, t in enumerate(tables):
+        arr[i].id = t.id
+        arr[i].dim = t.dim
+        arr[i].hash_size = t.hash_size
+        arr[i].pooling_factor = t.pooling_factor
+        arr[i].table_size_gb = t.table_size_gb
+        for b in range(NUM_BINS):
+            arr[i].dist[b] = t.dist[b]
+    return arr
+
+
+def _ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+@dataclass
+class LookupBatch:
+    """shardplan::LookupBatch (table.hpp:158-165): CSR ordered by
+    (table_id, batch_offset); lookup k of table t reads
+    indices[offsets[t*B + k] : offsets[t*B + k + 1]]."""
+
+    indices: np.ndarray
+    offsets: np.ndarray
+    num_tables: int
+    batch_size: int
+
+    def __post_init__(self):
+        self.indices = np.ascontiguousarray(self.indices, dtype=np.int64)
+        self.offsets = np.ascontiguousarray(self.offsets, dtype=np.int64)
+
+
+def validate_batch(b: LookupBatch) -> None:
+    """table.hpp:167-184; raises ShardplanError(malformed_batch)."""
+    if b.num_tables < 0 or b.batch_size <= 0:
+        raise ShardplanError(3, "non-positive table or batch count")
+    want = b.num_tables * b.batch_size + 1
+    if len(b.offsets) != want:
+        raise ShardplanError(3, f"offsets length {len(b.offsets)}, expected {want}")
+    if b.offsets[0] != 0:
+        raise ShardplanError(3, "offsets must start at 0")
+    d = np.diff(b.offsets)
+    if len(d) and d.min() < 0:
+        raise ShardplanError(3, f"offsets decrease at position {int(np.argmax(d < 0)) + 1}")
+    if int(b.offsets[-1]) != len(b.indices):
+        raise ShardplanError(3, "last offset != indices length")
+
+
+def compute_feature_stats(tables: Sequence[TableDesc]):
+    """table.hpp:108-131: per-feature (mean, std) of ln(1+x)."""
+    if not tables:
+        return np.zeros(NUM_FEATURES), np.ones(NUM_FEATURES)
+    raw = np.array([[t.dim, t.hash_size, t.pooling_factor, t.table_size_gb] + list(t.dist)
+                    for t in tables], dtype=np.float64)
+    y = np.log1p(raw)
+    n = float(len(tables))
+    s = np.zeros(NUM_FEATURES)
+    s2 = np.zeros(NUM_FEATURES)
+    for row in y:  # same accumulation order as the reference
+        s += row
+        s2 += row * row
+    mean = s / n
+    var = np.maximum(0.0, s2 / n - mean * mean)
+    return mean, np.sqrt(var)
+
+
+def ingest_lookup_batch(b: LookupBatch, dims: Sequence[int], hash_sizes: Sequence[int],
+                        bytes_per_param: int = DEFAULT_BYTES_PER_PARAM, device: int = 0):
+    """ingest_lookup_batch (table.hpp:188-232) on the GPU (K5).
+
+    Returns (tables, feature_mean, feature_std) — the TablePool content."""
+    dims_a = np.ascontiguousarray(dims, dtype=np.int32)
+    hs_a = np.ascontiguousarray(hash_sizes, dtype=np.int64)
+    out = (SpTableSpec * max(b.num_tables, 1))()
+    check(lib().sp_ingest_lookup_batch(_ptr(b.offsets), len(b.offsets), _ptr(b.indices),
+                                       len(b.indices), b.num_tables, b.batch_size,
+                                       _ptr(dims_a), _ptr(hs_a), bytes_per_param, device, out))
+    tables = [TableDesc(s.id, s.dim, s.hash_size, s.pooling_factor, s.table_size_gb,
+                        list(s.dist)) for s in out][:b.num_tables]
+    mean, std = compute_feature_stats(tables)
+    return tables, mean, std
+
+
+# ---------------------------------------------------------------------------
+# oracle.hpp types
+
+@dataclass
+class PlacementTask:
+    """shardplan::PlacementTask (oracle.hpp:68-73)."""
+
+    tables: List[TableDesc]
+    num_devices: int = 1
+    mem_cap_gb: float = 0.0
+    batch_size: int = DEFAULT_BATCH_SIZE
+
+
+@dataclass
+class TraceEvent:
+    device: int
+    phase: str
+    start_ms: float
+    dur_ms: float
+
+
+@dataclass
+class CostBreakdown:
+    """shardplan::CostBreakdown (oracle.hpp:105-116), measured on B200."""
+
+    fwd_ms: List[float]
+    bwd_ms: List[float]
+    comm_ms: List[float]
+    fwd_comm_stage_ms: float
+    bwd_comm_stage_ms: float
+    overall_ms: float
+
+    @property
+    def events(self) -> List[TraceEvent]:
+        """Synchronised stage bars, laid out as oracle.hpp:229-238."""
+        t1 = max(self.fwd_ms)
+        t2 = t1 + self.fwd_comm_stage_ms
+        t3 = t2 + self.bwd_comm_stage_ms
+        ev = []
+        for d in range(len(self.fwd_ms)):
+            ev.append(TraceEvent(d, "fwd_comp", 0.0, self.fwd_ms[d]))
+            ev.append(TraceEvent(d, "fwd_comm", t1, self.comm_ms[d]))
+            ev.append(TraceEvent(d, "bwd_comm", t2, self.comm_ms[d]))
+            ev.append(TraceEvent(d, "bwd_comp", t3, self.bwd_ms[d]))
+        return ev
+
+    def to_json(self) -> dict:
+        return {"devices": len(self.fwd_ms), "overall_ms": self.overall_ms,
+                "fwd_ms": list(self.fwd_ms), "bwd_ms": list(self.bwd_ms),
+                "comm_ms": list(self.comm_ms), "fwd_comm_stage_ms": self.fwd_comm_stage_ms,
+                "bwd_comm_stage_ms": self.bwd_comm_stage_ms,
+                "events": [e.__dict__ for e in self.events]}
+
+
+def nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    check(lib().sp_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class HostBuffer:
+    """Page-locked host array (sp_host_alloc) for the e2e upload path."""
+
+    def __init__(self, n: int, dtype=np.int64):
+        self._p = ctypes.c_void_p()
+        self.dtype = np.dtype(dtype)
+        check(lib().sp_host_alloc(max(n, 1) * self.dtype.itemsize, ctypes.byref(self._p)))
+        buf = (ctypes.c_char * (max(n, 1) * self.dtype.itemsize)).from_address(self._p.value)
+        self.array = np.frombuffer(buf, dtype=self.dtype)[:n]
+
+    def __del__(self):
+        if getattr(self, "_p", None) and self._p.value:
+            lib().sp_host_free(self._p)
+            self._p = ctypes.c_void_p()
+
+
+# ---------------------------------------------------------------------------
+# The measured execution of a placement (replaces CostOracle).
+
+class EmbeddingShard:
+    """One rank's shard of a placement on one B200 (sp_ctx).
+
+    world_size == num_devices: one process per GPU, exchanges over NCCL.
+    world_size == 1 < num_devices: emulation, all virtual devices on this GPU
+    (compute measured per device; exchange is a device-local copy)."""
+
+    def __init__(self, task: PlacementTask, placement: Sequence[int], lr: float = 0.01,
+                 rank: int = 0, world_size: int = 1, nccl_id: Optional[bytes] = None,
+                 device: int = 0):
+        self.task = task
+        self.placement = np.ascontiguousarray(placement, dtype=np.int32)
+        if len(self.placement) != len(task.tables):
+            raise ShardplanError(10, "placement length != table count")
+        self.D = task.num_devices
+        self.B = task.batch_size
+        self.rank = rank
+        self.world = world_size
+        self.dims = np.array([t.dim for t in task.tables], dtype=np.int64)
+        self.W_total = int(self.dims.sum())
+        self._specs = _specs(task.tables)
+        h = ctypes.c_void_p()
+        idb = None
+        if nccl_id is not None:
+            idb = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
+        check(lib().sp_ctx_create(self._specs, len(task.tables), self.D, _ptr(self.placement),
+                                  self.B, float(task.mem_cap_gb), float(lr), rank, world_size,
+                                  idb, device, ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().sp_ctx_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        self.close()
+
+    # -- properties
+    @property
+    def stream(self) -> int:
+        s = ctypes.c_void_p()
+        check(lib().sp_ctx_stream(self._h, ctypes.byref(s)))
+        return s.value or 0
+
+    @property
+    def device_bytes(self) -> int:
+        b = ctypes.c_uint64()
+        check(lib().sp_ctx_device_bytes(self._h, ctypes.byref(b)))
+        return b.value
+
+    def local_tables(self) -> List[int]:
+        n = ctypes.c_int32()
+        check(lib().sp_ctx_local_tables(self._h, None, ctypes.byref(n)))
+        ids = np.zeros(n.value, dtype=np.int32)
+        check(lib().sp_ctx_local_tables(self._h, _ptr(ids), ctypes.byref(n)))
+        return ids.tolist()
+
+    def rows_per_rank(self) -> int:
+        return self.B if self.world == 1 else self.B // self.D
+
+    # -- tables
+    def init_tables(self, seed: int):
+        check(lib().sp_init_tables(self._h, seed))
+
+    def set_table(self, table_id: int, rows: np.ndarray):
+        t = self.task.tables[table_id]
+        rows = np.ascontiguousarray(rows, dtype=np.float32).reshape(t.hash_size, t.dim)
+        check(lib().sp_set_table(self._h, table_id, _ptr(rows)))
+
+    def get_table(self, table_id: int) -> np.ndarray:
+        t = self.task.tables[table_id]
+        out = np.empty((t.hash_size, t.dim), dtype=np.float32)
+        check(lib().sp_get_table(self._h, table_id, _ptr(out)))
+        return out
+
+    # -- batch
+    def upload_batch(self, b: LookupBatch):
+        if b.num_tables != len(self.task.tables) or b.batch_size != self.B:
+            raise ShardplanError(8, "batch shape does not match the task")
+        check(lib().sp_upload_batch(self._h, _ptr(b.offsets), len(b.offsets), _ptr(b.indices),
+                                    len(b.indices)))
+
+    def upload_batch_ptr(self, offsets_ptr: int, offsets_len: int, indices_ptr: int,
+                         indices_len: int):
+        check(lib().sp_upload_batch(self._h, ctypes.c_void_p(offsets_ptr), offsets_len,
+                                    ctypes.c_void_p(indices_ptr), indices_len))
+
+    def synth_batch(self, seed: int):
+        check(lib().sp_synth_batch(self._h, seed))
+
+    @property
+    def nnz(self) -> int:
+        n = ctypes.c_int64()
+        check(lib().sp_batch_nnz(self._h, ctypes.byref(n)))
+        return n.value
+
+    # -- stages
+    def forward(self):
+        check(lib().sp_forward(self._h))
+
+    def a2a_forward(self):
+        check(lib().sp_a2a_forward(self._h))
+
+    def a2a_backward(self):
+        check(lib().sp_a2a_backward(self._h))
+
+    def backward_sgd(self):
+        check(lib().sp_backward_sgd(self._h))
+
+    def set_grad(self, grad: np.ndarray):
+        g = np.ascontiguousarray(grad, dtype=np.float32).reshape(self.rows_per_rank(),
+                                                                  self.W_total)
+        check(lib().sp_set_grad(self._h, _ptr(g)))
+
+    def synth_grad(self, seed: int):
+        check(lib().sp_synth_grad(self._h, seed))
+
+    def pooled(self) -> np.ndarray:
+        out = np.empty((self.rows_per_rank(), self.W_total), dtype=np.float32)
+        check(lib().sp_get_pooled(self._h, _ptr(out)))
+        return out
+
+    def local_pooled(self, dev: int) -> np.ndarray:
+        w = int(self.dims[self.placement == dev].sum())
+        out = np.empty((self.B, w), dtype=np.float32)
+        check(lib().sp_get_local_pooled(self._h, dev, _ptr(out)))
+        return out
+
+    def sorted(self, dev: int):
+        """(keys, bags, run heads) of device dev's backward sort."""
+        n = ctypes.c_int64()
+        nu = ctypes.c_int64()
+        check(lib().sp_get_sorted(self._h, dev, None, None, ctypes.byref(n), None,
+                                  ctypes.byref(nu)))
+        keys = np.empty(n.value, dtype=np.uint32)
+        bags = np.empty(n.value, dtype=np.uint32)
+        heads = np.empty(max(n.value, 1), dtype=np.uint32)
+        check(lib().sp_get_sorted(self._h, dev, _ptr(keys), _ptr(bags), ctypes.byref(n),
+                                  _ptr(heads), ctypes.byref(nu)))
+        return keys, bags, heads[:nu.value]
+
+    def run_iteration(self) -> CostBreakdown:
+        D = self.D
+        f = (ctypes.c_double * D)()
+        b = (ctypes.c_double * D)()
+        c = (ctypes.c_double * D)()
+        bd = SpBreakdown(f, b, c, 0.0, 0.0, 0.0)
+        check(lib().sp_run_iteration(self._h, ctypes.byref(bd)))
+        return CostBreakdown(list(f), list(b), list(c), bd.fwd_comm_stage_ms,
+                             bd.bwd_comm_stage_ms, bd.overall_ms)
+
+    def enqueue_iteration(self):
+        check(lib().sp_enqueue_iteration(self._h))
+
+    def graph_replay(self, iters: int) -> int:
+        k = ctypes.c_int32()
+        check(lib().sp_graph_replay(self._h, iters, ctypes.byref(k)))
+        return k.value
+
+    def algorithmic_bytes(self) -> dict:
+        out = (ctypes.c_double * 4)()
+        check(lib().sp_ctx_algorithmic_bytes(self._h, out))
+        return {"fwd": out[0], "a2a": out[1], "bwd": out[2], "sort": out[3]}
+
+
+# ---------------------------------------------------------------------------
+# mdp.hpp plugin boundary
+
+class CostProvider:
+    """shardplan::CostProvider (mdp.hpp:28-34)."""
+
+    def cost_features(self, assignment: Sequence[Sequence[int]]):  # pragma: no cover
+        raise NotImplementedError
+
+    def overall(self, placement: Sequence[int]) -> float:  # pragma: no cover
+        raise NotImplementedError
+
+
+class MeasuredCostProvider(CostProvider):
+    """CostProvider whose numbers are measured on this B200 instead of the
+    synthetic oracle (the drop-in for OracleCostProvider, mdp.hpp:37-54).
+
+    Every query builds an emulated shard of the (partial) assignment on this
+    GPU — all D virtual devices, real K1/K4 kernels on the synthetic batch of
+    the task — and returns median stage times over `iters` iterations after
+    `warmup`. cost_features returns per device (fwd_ms, bwd_ms, comm_ms);
+    a device with no tables reports (0, 0, 0) like oracle.hpp:242-269."""
+
+    def __init__(self, task: PlacementTask, seed: int = 2210, iters: int = 5, warmup: int = 2,
+                 device: int = 0):
+        self.task = task
+        self.seed = seed
+        self.iters = iters
+        self.warmup = warmup
+        self.device = device
+        self.calls = 0
+
+    def _measure(self, placement: np.ndarray, subset: np.ndarray) -> CostBreakdown:
+        tables = [self.task.tables[i] for i in subset]
+        sub_task = PlacementTask(tables, self.task.num_devices, self.task.mem_cap_gb,
+                                 self.task.batch_size)
+        shard = EmbeddingShard(sub_task, placement[subset], device=self.device)
+        try:
+            shard.init_tables(self.seed)
+            shard.synth_batch(self.seed)
+            shard.synth_grad(self.seed)
+            runs = []
+            for i in range(self.warmup + self.iters):
+                bd = shard.run_iteration()
+                if i >= self.warmup:
+                    runs.append(bd)
+        finally:
+            shard.close()
+        k = int(np.argsort([r.overall_ms for r in runs])[len(runs) // 2])
+        return runs[k]
+
+    def cost_features(self, assignment):
+        self.calls += 1
+        D = self.task.num_devices
+        if len(assignment) != D:
+            raise ShardplanError(10, "assignment has wrong device count")
+        placement = np.full(len(self.task.tables), -1, dtype=np.int32)
+        for d, ids in enumerate(assignment):
+            for i in ids:
+                if i < 0 or i >= len(self.task.tables):
+                    raise ShardplanError(5, f"table id {i}")
+                placement[i] = d
+        subset = np.nonzero(placement >= 0)[0]
+        if len(subset) == 0:
+            return [(0.0, 0.0, 0.0)] * D
+        bd = self._measure(placement, subset)
+        return [(bd.fwd_ms[d], bd.bwd_ms[d], bd.comm_ms[d]) if len(assignment[d]) else
+                (0.0, 0.0, 0.0) for d in range(D)]
+
+    def overall(self, placement):
+        self.calls += 1
+        p = np.ascontiguousarray(placement, dtype=np.int32)
+        return self._measure(p, np.arange(len(p))).overall_ms
+
+
+# ---------------------------------------------------------------------------
+# checkpoint.hpp (DSHD) and the GPU evaluator
+
+REDUCTIONS = {"sum": 0, "mean": 1, "max": 2}
+
+
+@dataclass
+class Checkpoint:
+    """shardplan::Checkpoint (checkpoint.hpp:28-33), parameters in the flat
+    Mlp layout (nn.hpp:21-53)."""
+
+    sections: dict
+
+    @property
+    def feature_mean(self):
+        return self.sections["feature_mean"]
+
+    @property
+    def feature_std(self):
+        return self.sections["feature_std"]
+
+    @property
+    def feature_mask(self):
+        return self.sections["feature_mask"]
+
+    @property
+    def reductions(self):
+        r = self.sections["reductions"]
+        return int(r[0]), int(r[1])
+
+
+_SECTION_SIZES = {
+    "cost.table_mlp": 6944, "cost.head_fwd": 2177, "cost.head_bwd": 2177,
+    "cost.head_comm": 2177, "cost.head_overall": 2177, "policy.table_mlp": 6944,
+    "policy.cost_mlp": 2336, "policy.head": 65, "feature_mean": 21, "feature_std": 21,
+    "feature_mask": 21, "reductions": 2, "config": 24,
+}
+
+
+def load_checkpoint(path: str) -> Checkpoint:
+    """DSHD reader (checkpoint.hpp:149-217): magic, u32 version, u32 count,
+    then (u32 name_len, name, u64 n, f64[n]) sections, little-endian."""
+    with open(path, "rb") as f:
+        data = f.read()
+    if data[:4] != b"DSHD":
+        raise ShardplanError(10, f"{path}: not a checkpoint file")
+    version, count = struct.unpack_from("<II", data, 4)
+    if version != 1:
+        raise ShardplanError(10, f"unsupported checkpoint version {version}")
+    off = 12
+    sections = {}
+    for _ in range(count):
+        (nl,) = struct.unpack_from("<I", data, off)
+        off += 4
+        name = data[off:off + nl].decode()
+        off += nl
+        (n,) = struct.unpack_from("<Q", data, off)
+        off += 8
+        if off + 8 * n > len(data):
+            raise ShardplanError(10, "truncated checkpoint")
+        sections[name] = np.frombuffer(data, dtype="<f8", count=n, offset=off).copy()
+        off += 8 * n
+    for name, size in _SECTION_SIZES.items():
+        if name not in sections:
+            raise ShardplanError(10, f"checkpoint missing section {name}")
+        if len(sections[name]) != size:
+            raise ShardplanError(10, f"section {name} has wrong length")
+    return Checkpoint(sections)
+
+
+class Evaluator:
+    """Cost network + policy network of a checkpoint bound to one placement
+    task on one GPU (sp_evaluator)."""
+
+    def __init__(self, ckpt: Checkpoint, task: PlacementTask, device: int = 0):
+        s = ckpt.sections
+        self._keep = {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in s.items()}
+        k = self._keep
+        dp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))  # noqa: E731
+        rt, rd = ckpt.reductions
+        self._nets = SpNets(dp(k["cost.table_mlp"]), dp(k["cost.head_fwd"]),
+                            dp(k["cost.head_bwd"]), dp(k["cost.head_comm"]),
+                            dp(k["cost.head_overall"]), dp(k["policy.table_mlp"]),
+                            dp(k["policy.cost_mlp"]), dp(k["policy.head"]),
+                            dp(k["feature_mean"]), dp(k["feature_std"]), dp(k["feature_mask"]),
+                            rt, rd)
+        self.task = task
+        self.M = len(task.tables)
+        self.D = task.num_devices
+        self._specs = _specs(task.tables)
+        h = ctypes.c_void_p()
+        check(lib().sp_evaluator_create(ctypes.byref(self._nets), self._specs, self.M, self.D,
+                                        float(task.mem_cap_gb), device, ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().sp_evaluator_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        self.close()
+
+    def order(self) -> np.ndarray:
+        """predicted_order (harness.hpp:131-137)."""
+        o = np.zeros(self.M, dtype=np.int32)
+        check(lib().sp_evaluator_order(self._h, _ptr(o)))
+        return o
+
+    def eval_batch(self, placements: np.ndarray):
+        """EstimatedCostProvider::overall for each row (raw) + clamped q."""
+        p = np.ascontiguousarray(placements, dtype=np.int32).reshape(-1, self.M)
+        n = p.shape[0]
+        overall = np.zeros(n, dtype=np.float32)
+        q = np.zeros((n, self.D, 3), dtype=np.float32)
+        check(lib().sp_eval_batch(self._h, _ptr(p), n, _ptr(overall), _ptr(q)))
+        return overall, q
+
+    def rollout(self, n: int, mode: str = "greedy", uniforms: Optional[np.ndarray] = None,
+                precision: str = "guarded"):
+        """n estimated-MDP rollouts (greedy = Alg. 2 infer; sample = policy
+        sampling with one uniform per step). Returns (placements [n, M],
+        predicted overall [n], status [n], n_refined)."""
+        m = {"greedy": 0, "sample": 1}[mode]
+        prec = {"guarded": 0, "fp64": 1, "fp32": 2}[precision]
+        if m == 1:
+            if uniforms is None:
+                raise ShardplanError(10, "sampled rollouts need uniforms [n, M]")
+            u = np.ascontiguousarray(uniforms, dtype=np.float64).reshape(n, self.M)
+            up = _ptr(u)
+        else:
+            u = None
+            up = None
+        pl = np.zeros((n, self.M), dtype=np.int32)
+        pred = np.zeros(n, dtype=np.float64)
+        st = np.zeros(n, dtype=np.int32)
+        nref = ctypes.c_int32()
+        check(lib().sp_rollout_batch(self._h, m, up, n, prec, _ptr(pl), _ptr(pred), _ptr(st),
+                                     ctypes.byref(nref)))
+        return pl, pred, st, nref.value
+
+
+def infer(ckpt: Checkpoint, task: PlacementTask, device: int = 0):
+    """harness.hpp:332-356 infer() on the GPU: (placement, predicted_ms).
+
+    Infeasibility is a hard error, as in the reference."""
+    ev = Evaluator(ckpt, task, device)
+    try:
+        pl, pred, st, _ = ev.rollout(1, "greedy")
+    finally:
+        ev.close()
+    if st[0] != 0:
+        raise ShardplanError(int(st[0]), "no device can hold the next table")
+    return pl[0], max(0.0, float(pred[0]))

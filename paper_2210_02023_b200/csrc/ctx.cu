@@ -1,0 +1,1074 @@
+// ctx.cu — sp_ctx: one rank's shard of a table->device placement and the
+// measured four-stage iteration that replaces the reference's synthetic
+// CostOracle::evaluate_placement (oracle.hpp:187-240).
+//
+// HBM layout per GPU (all fp32 / int32, 16-byte aligned):
+//   weight slab   every local table's rows back to back, [rows_t, dim_t]
+//   CSR           per (virtual) device: offsets[T_v*B+1], indices[nnz_v]
+//   pooled_v      [B, W_v] batch-major, so the rows bound for peer j are the
+//                 contiguous slice [j*B/D, (j+1)*B/D) (no packing, §8e)
+//   recv / gin    per destination rank: [src i][B/D][W_i] grouped by source
+//   grad_v        [B, W_v], the bwd exchange lands each peer's slice in place
+//   sort scratch  keys/bags double buffers, run heads, CUB temp (shared by
+//                 the virtual devices, stream-ordered)
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "nccl_loader.h"
+#include "synth.cuh"
+#include "tbe.h"
+
+namespace sp {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+}  // namespace
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+template <class T>
+T* dalloc(size_t n, std::vector<void*>& owned, uint64_t& bytes) {
+  if (n == 0) n = 1;
+  void* p = nullptr;
+  SP_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  owned.push_back(p);
+  bytes += n * sizeof(T);
+  return static_cast<T*>(p);
+}
+
+struct VDev {
+  int vid = 0;
+  std::vector<int> tables;  // global ids, ascending
+  std::vector<TableMeta> meta_canon, meta_grid;
+  std::vector<uint32_t> rb_end;
+  std::vector<int32_t> colmap;  // local col -> global col
+  int64_t W = 0, rows_total = 0, fwd_blocks = 0;
+  int end_bit = 1;
+  TableMeta* d_meta_grid = nullptr;
+  TableMeta* d_meta_canon = nullptr;
+  uint32_t* d_rb_end = nullptr;
+  int32_t* d_colmap = nullptr;
+  int32_t* d_off = nullptr;
+  int32_t* d_idx = nullptr;
+  int64_t nnz = 0, idx_cap = 0;
+  std::vector<int64_t> table_nnz;
+  float* d_pooled = nullptr;
+  float* d_grad = nullptr;
+  double fwd_bytes = 0, bwd_bytes = 0;
+  cudaEvent_t ev[8] = {};
+};
+
+}  // namespace sp
+
+struct sp_ctx {
+  int M = 0, D = 1, world = 1, rank = 0, B = 0, device = 0;
+  float lr = 0.01f;
+  double cap = 0.0;
+  std::vector<sp_table_spec> tables;
+  std::vector<int> placement;
+  std::vector<int64_t> gcol;   // global column of each table
+  std::vector<int64_t> dev_W;  // W per device
+  std::vector<int64_t> cumW;   // prefix over devices
+  int64_t W_total = 0;
+  std::vector<sp::VDev> vdevs;
+  std::vector<int64_t> woff;   // per global table (-1 if not local)
+  float* d_w = nullptr;
+  float* d_recv = nullptr;     // rows_per_dst * W_total per destination
+  float* d_gin = nullptr;
+  int n_dst = 1;               // destinations held here (D in emulation)
+  uint32_t *d_ka = nullptr, *d_kb = nullptr, *d_ba = nullptr, *d_bb = nullptr;
+  uint32_t* d_seg = nullptr;
+  int32_t* d_nseg = nullptr;
+  int32_t* d_flag = nullptr;
+  int64_t sort_cap = 0;
+  void* d_temp = nullptr;
+  size_t temp_bytes = 0;
+  int64_t* d_stage64 = nullptr;
+  int64_t stage_cap = 0;
+  int sgd_grid = 0;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  double* d_bd = nullptr;      // breakdown gather buffer
+  int32_t* d_barrier = nullptr;
+  cudaEvent_t ev_a2a[4] = {};
+  cudaGraphExec_t graph_exec = nullptr;
+  int graph_kernels = 0;
+  std::vector<void*> owned;
+  std::vector<void*> sort_owned;
+  uint64_t dev_bytes = 0;
+  bool has_batch = false;
+
+  ~sp_ctx() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    for (auto& v : vdevs)
+      for (auto& e : v.ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : ev_a2a)
+      if (e) cudaEventDestroy(e);
+    for (void* p : sort_owned) cudaFree(p);
+    for (void* p : owned) cudaFree(p);
+    if (comm) sp::nccl().CommDestroy(comm);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace sp {
+namespace {
+
+int64_t rows_per_dst(const sp_ctx* c) { return c->B / c->D; }
+
+// Frees and re-allocates the sort scratch for n positions.
+void ensure_sort_capacity(sp_ctx* c, int64_t n) {
+  if (n <= c->sort_cap && c->d_temp) return;
+  SP_CUDA(cudaStreamSynchronize(c->stream));
+  for (void* p : c->sort_owned) cudaFree(p);
+  c->sort_owned.clear();
+  const int64_t cap = std::max<int64_t>(n, 1);
+  uint64_t dummy = 0;
+  c->d_ka = dalloc<uint32_t>(cap, c->sort_owned, dummy);
+  c->d_kb = dalloc<uint32_t>(cap, c->sort_owned, dummy);
+  c->d_ba = dalloc<uint32_t>(cap, c->sort_owned, dummy);
+  c->d_bb = dalloc<uint32_t>(cap, c->sort_owned, dummy);
+  c->d_seg = dalloc<uint32_t>(cap + 1, c->sort_owned, dummy);
+  int max_bit = 1;
+  for (auto& v : c->vdevs) max_bit = std::max(max_bit, v.end_bit);
+  size_t t1 = sort_pairs(nullptr, 0, c->d_ka, c->d_kb, c->d_ba, c->d_bb, cap,
+                         max_bit, c->stream);
+  size_t t2 = select_heads(nullptr, 0, c->d_kb, cap, c->d_seg, c->d_nseg,
+                           c->stream);
+  size_t t3 = exclusive_scan_i32(nullptr, 0, nullptr, nullptr,
+                                 static_cast<int64_t>(c->B) * 256 + 1, c->stream);
+  c->temp_bytes = std::max({t1, t2, t3, static_cast<size_t>(256)});
+  c->d_temp = dalloc<uint8_t>(c->temp_bytes, c->sort_owned, dummy);
+  c->sort_cap = cap;
+}
+
+void check_ctx(sp_ctx* c) {
+  if (c == nullptr) raise(SP_ERR_BAD_INPUT, "null context");
+  SP_CUDA(cudaSetDevice(c->device));
+}
+
+VDev& vdev_for(sp_ctx* c, int dev) {
+  for (auto& v : c->vdevs)
+    if (v.vid == dev) return v;
+  raise(SP_ERR_BAD_INPUT, "device " + std::to_string(dev) + " is not held by this context");
+}
+
+void require_batch(sp_ctx* c) {
+  if (!c->has_batch) raise(SP_ERR_BAD_INPUT, "no lookup batch uploaded");
+}
+
+// ---- stages ---------------------------------------------------------------
+
+void stage_forward(sp_ctx* c, VDev& v) {
+  launch_tbe_forward(v.d_meta_grid, static_cast<int>(v.tables.size()),
+                     v.fwd_blocks, c->B, v.d_off, v.d_idx, c->d_w, v.d_pooled,
+                     v.W, c->stream);
+}
+
+// keys -> sort -> heads; leaves sorted keys in d_kb, bags in d_bb.
+void stage_sort(sp_ctx* c, VDev& v) {
+  const int T = static_cast<int>(v.tables.size());
+  launch_build_keys(v.d_meta_canon, T, c->B, v.d_off, v.d_idx, c->d_ka, c->d_ba,
+                    c->stream);
+  sort_pairs(c->d_temp, c->temp_bytes, c->d_ka, c->d_kb, c->d_ba, c->d_bb, v.nnz,
+             v.end_bit, c->stream);
+  select_heads(c->d_temp, c->temp_bytes, c->d_kb, v.nnz, c->d_seg, c->d_nseg,
+               c->stream);
+}
+
+void stage_backward(sp_ctx* c, VDev& v) {
+  if (v.nnz == 0) return;
+  stage_sort(c, v);
+  launch_sgd(v.d_meta_canon, v.d_rb_end, static_cast<int>(v.tables.size()),
+             c->d_kb, c->d_bb, c->d_seg, c->d_nseg, v.nnz, v.d_grad, v.W, c->lr,
+             c->d_w, c->sgd_grid, c->stream);
+}
+
+bool nccl_mode(const sp_ctx* c) { return c->world > 1; }
+
+void d2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes) SP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
+}
+
+// Fwd exchange sends of (virtual) device v (emulation: device-local copies).
+void a2a_fwd_emulated(sp_ctx* c, VDev& v) {
+  const int64_t R = rows_per_dst(c);
+  for (int j = 0; j < c->D; ++j)
+    d2d(c->d_recv + j * R * c->W_total + R * c->cumW[v.vid],
+        v.d_pooled + j * R * v.W, R * v.W * sizeof(float), c->stream);
+}
+
+void a2a_bwd_emulated(sp_ctx* c, VDev& v) {
+  const int64_t R = rows_per_dst(c);
+  for (int j = 0; j < c->D; ++j)
+    d2d(v.d_grad + j * R * v.W, c->d_gin + j * R * c->W_total + R * c->cumW[v.vid],
+        R * v.W * sizeof(float), c->stream);
+}
+
+void a2a_fwd_nccl(sp_ctx* c) {
+  VDev& v = c->vdevs[0];
+  const int64_t R = rows_per_dst(c);
+  SP_NCCL(nccl().GroupStart());
+  for (int j = 0; j < c->D; ++j) {
+    if (v.W > 0)
+      SP_NCCL(nccl().Send(v.d_pooled + j * R * v.W, R * v.W, ncclFloat, j, c->comm,
+                       c->stream));
+    if (c->dev_W[j] > 0)
+      SP_NCCL(nccl().Recv(c->d_recv + R * c->cumW[j], R * c->dev_W[j], ncclFloat, j,
+                       c->comm, c->stream));
+  }
+  SP_NCCL(nccl().GroupEnd());
+}
+
+void a2a_bwd_nccl(sp_ctx* c) {
+  VDev& v = c->vdevs[0];
+  const int64_t R = rows_per_dst(c);
+  SP_NCCL(nccl().GroupStart());
+  for (int j = 0; j < c->D; ++j) {
+    if (c->dev_W[j] > 0)
+      SP_NCCL(nccl().Send(c->d_gin + R * c->cumW[j], R * c->dev_W[j], ncclFloat, j,
+                       c->comm, c->stream));
+    if (v.W > 0)
+      SP_NCCL(nccl().Recv(v.d_grad + j * R * v.W, R * v.W, ncclFloat, j, c->comm,
+                       c->stream));
+  }
+  SP_NCCL(nccl().GroupEnd());
+}
+
+void barrier(sp_ctx* c) {
+  if (nccl_mode(c))
+    SP_NCCL(nccl().AllReduce(c->d_barrier, c->d_barrier, 1, ncclInt32, ncclSum,
+                          c->comm, c->stream));
+}
+
+bool exchange_needed(const sp_ctx* c) { return c->D > 1; }
+
+void enqueue_iteration(sp_ctx* c) {
+  for (auto& v : c->vdevs) stage_forward(c, v);
+  if (exchange_needed(c)) {
+    if (nccl_mode(c)) {
+      a2a_fwd_nccl(c);
+      a2a_bwd_nccl(c);
+    } else {
+      for (auto& v : c->vdevs) a2a_fwd_emulated(c, v);
+      for (auto& v : c->vdevs) a2a_bwd_emulated(c, v);
+    }
+  }
+  for (auto& v : c->vdevs) stage_backward(c, v);
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  SP_CUDA(cudaEventElapsedTime(&ms, a, b));
+  return ms;
+}
+
+}  // namespace
+}  // namespace sp
+
+using namespace sp;
+
+extern "C" {
+
+int sp_abi_version(void) { return SP_ABI_VERSION; }
+const char* sp_last_error(void) { return g_last_error.c_str(); }
+uint64_t sp_kernel_launches(void) { return g_launches.load(); }
+
+int sp_host_alloc(uint64_t bytes, void** out) {
+  return guarded([&] {
+    if (out == nullptr) raise(SP_ERR_BAD_INPUT, "null output pointer");
+    *out = nullptr;
+    SP_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable));
+  });
+}
+
+void sp_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int sp_nccl_unique_id(uint8_t out_id[SP_NCCL_ID_BYTES]) {
+  return guarded([&] {
+    ncclUniqueId id;
+    SP_NCCL(nccl().GetUniqueId(&id));
+    static_assert(sizeof(id.internal) == SP_NCCL_ID_BYTES, "nccl id size");
+    std::memcpy(out_id, id.internal, SP_NCCL_ID_BYTES);
+  });
+}
+
+int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
+                  int32_t num_devices, const int32_t* placement,
+                  int32_t batch_size, double mem_cap_gb, float lr,
+                  int32_t rank, int32_t world_size, const uint8_t* nccl_id,
+                  int32_t cuda_device, sp_ctx** out) {
+  return guarded([&] {
+    if (out == nullptr) raise(SP_ERR_BAD_INPUT, "null output handle");
+    *out = nullptr;
+    if (num_tables < 0 || (num_tables > 0 && (tables == nullptr || placement == nullptr)))
+      raise(SP_ERR_BAD_INPUT, "tables/placement missing");
+    if (num_devices < 1) raise(SP_ERR_BAD_INPUT, "num_devices must be >= 1");
+    if (batch_size < 1) raise(SP_ERR_BAD_INPUT, "batch_size must be >= 1");
+    if (batch_size % num_devices != 0)
+      raise(SP_ERR_SHAPE_MISMATCH, "batch_size must be divisible by num_devices");
+    if (!(world_size == 1 || world_size == num_devices))
+      raise(SP_ERR_BAD_INPUT, "world_size must be 1 (emulation) or num_devices");
+    if (rank < 0 || rank >= world_size) raise(SP_ERR_BAD_INPUT, "rank out of range");
+    if (world_size > 1 && nccl_id == nullptr)
+      raise(SP_ERR_BAD_INPUT, "multi-rank context needs an NCCL unique id");
+
+    // Placement legality, as evaluate_placement (oracle.hpp:190-204).
+    std::vector<double> mem(num_devices, 0.0);
+    for (int i = 0; i < num_tables; ++i) {
+      const int d = placement[i];
+      if (d < 0 || d >= num_devices) raise(SP_ERR_BAD_INPUT, "device id out of range");
+      const sp_table_spec& t = tables[i];
+      if (t.dim < 1 || t.hash_size < 1)
+        raise(SP_ERR_BAD_INPUT, "dim and hash_size must be >= 1");
+      if (t.hash_size > 0x7fffffffLL)
+        raise(SP_ERR_BAD_INPUT, "hash_size above 2^31-1 is not supported (int32 ids)");
+      mem[d] += t.table_size_gb;
+    }
+    if (mem_cap_gb > 0.0) {
+      std::string offenders;
+      for (int d = 0; d < num_devices; ++d)
+        if (mem[d] > mem_cap_gb + 1e-9) {
+          if (!offenders.empty()) offenders += ", ";
+          offenders += std::to_string(d);
+        }
+      if (!offenders.empty())
+        raise(SP_ERR_MEMORY_VIOLATION, "memory cap exceeded on device(s) " + offenders);
+    }
+
+    auto c = std::make_unique<sp_ctx>();
+    c->M = num_tables;
+    c->D = num_devices;
+    c->world = world_size;
+    c->rank = rank;
+    c->B = batch_size;
+    c->lr = lr;
+    c->cap = mem_cap_gb;
+    c->device = cuda_device;
+    c->tables.assign(tables, tables + num_tables);
+    c->placement.assign(placement, placement + num_tables);
+    SP_CUDA(cudaSetDevice(cuda_device));
+    SP_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+
+    // Columns: global table order; per-device widths.
+    c->gcol.resize(num_tables);
+    c->dev_W.assign(num_devices, 0);
+    int64_t col = 0;
+    for (int i = 0; i < num_tables; ++i) {
+      c->gcol[i] = col;
+      col += tables[i].dim;
+      c->dev_W[placement[i]] += tables[i].dim;
+    }
+    c->W_total = col;
+    c->cumW.assign(num_devices + 1, 0);
+    for (int d = 0; d < num_devices; ++d) c->cumW[d + 1] = c->cumW[d] + c->dev_W[d];
+
+    // Which devices live here.
+    std::vector<int> held;
+    if (world_size == 1)
+      for (int d = 0; d < num_devices; ++d) held.push_back(d);
+    else
+      held.push_back(rank);
+
+    // Weight slab.
+    c->woff.assign(num_tables, -1);
+    int64_t slab = 0;
+    for (int d : held)
+      for (int i = 0; i < num_tables; ++i)
+        if (placement[i] == d) {
+          c->woff[i] = slab;
+          slab += tables[i].hash_size * tables[i].dim;
+          slab = (slab + 3) & ~int64_t(3);
+        }
+    c->d_w = dalloc<float>(slab, c->owned, c->dev_bytes);
+
+    const int64_t R = static_cast<int64_t>(batch_size) / num_devices;
+    for (int d : held) {
+      VDev v;
+      v.vid = d;
+      for (int i = 0; i < num_tables; ++i)
+        if (placement[i] == d) v.tables.push_back(i);
+      const int T = static_cast<int>(v.tables.size());
+      int64_t lcol = 0;
+      uint64_t rb = 0;
+      for (int li = 0; li < T; ++li) {
+        const int g = v.tables[li];
+        const sp_table_spec& t = tables[g];
+        TableMeta m{};
+        m.woff = c->woff[g];
+        m.rows = t.hash_size;
+        m.dim = t.dim;
+        m.lcol = static_cast<int32_t>(lcol);
+        m.rowbase = static_cast<uint32_t>(rb);
+        m.cls = dim_class(t.dim);
+        m.local = li;
+        m.gid = g;
+        v.meta_canon.push_back(m);
+        for (int k = 0; k < t.dim; ++k) v.colmap.push_back(static_cast<int32_t>(c->gcol[g] + k));
+        lcol += t.dim;
+        rb += static_cast<uint64_t>(t.hash_size);
+        if (rb > 0xffffffffULL)
+          raise(SP_ERR_BAD_INPUT, "rows per device above 2^32 (32-bit sort keys)");
+        v.rb_end.push_back(static_cast<uint32_t>(rb));
+      }
+      v.W = lcol;
+      v.rows_total = static_cast<int64_t>(rb);
+      v.end_bit = 1;
+      while (v.end_bit < 32 && (1ULL << v.end_bit) < static_cast<uint64_t>(std::max<int64_t>(v.rows_total, 2)))
+        ++v.end_bit;
+      // K1 grid order: heaviest tables (pf * dim) first so the long blocks
+      // start early (LPT), each table a contiguous block range.
+      std::vector<int> order(T);
+      std::iota(order.begin(), order.end(), 0);
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        const auto& ta = tables[v.tables[a]];
+        const auto& tb = tables[v.tables[b]];
+        return ta.pooling_factor * ta.dim > tb.pooling_factor * tb.dim;
+      });
+      int64_t blk = 0;
+      for (int li : order) {
+        TableMeta m = v.meta_canon[li];
+        m.block_start = blk;
+        const int per_block = kWarpsPerBlock * rows_per_warp(m.cls);
+        blk += (batch_size + per_block - 1) / per_block;
+        v.meta_grid.push_back(m);
+      }
+      v.fwd_blocks = blk;
+      v.d_meta_grid = dalloc<TableMeta>(T, c->owned, c->dev_bytes);
+      v.d_meta_canon = dalloc<TableMeta>(T, c->owned, c->dev_bytes);
+      v.d_rb_end = dalloc<uint32_t>(T, c->owned, c->dev_bytes);
+      v.d_colmap = dalloc<int32_t>(v.W, c->owned, c->dev_bytes);
+      if (T) {
+        SP_CUDA(cudaMemcpy(v.d_meta_grid, v.meta_grid.data(), T * sizeof(TableMeta), cudaMemcpyHostToDevice));
+        SP_CUDA(cudaMemcpy(v.d_meta_canon, v.meta_canon.data(), T * sizeof(TableMeta), cudaMemcpyHostToDevice));
+        SP_CUDA(cudaMemcpy(v.d_rb_end, v.rb_end.data(), T * sizeof(uint32_t), cudaMemcpyHostToDevice));
+      }
+      if (v.W)
+        SP_CUDA(cudaMemcpy(v.d_colmap, v.colmap.data(), v.W * sizeof(int32_t), cudaMemcpyHostToDevice));
+      v.d_off = dalloc<int32_t>(static_cast<int64_t>(T) * batch_size + 1, c->owned, c->dev_bytes);
+      v.d_pooled = dalloc<float>(static_cast<int64_t>(batch_size) * v.W, c->owned, c->dev_bytes);
+      v.d_grad = num_devices == 1
+                     ? nullptr
+                     : dalloc<float>(static_cast<int64_t>(batch_size) * v.W, c->owned, c->dev_bytes);
+      for (auto& e : v.ev) SP_CUDA(cudaEventCreate(&e));
+      c->vdevs.push_back(std::move(v));
+    }
+
+    c->n_dst = world_size == 1 ? num_devices : 1;
+    if (num_devices == 1) {
+      // D == 1: the exchange is the identity; alias the buffers.
+      c->d_recv = c->vdevs[0].d_pooled;
+      c->d_gin = dalloc<float>(static_cast<int64_t>(batch_size) * c->W_total, c->owned, c->dev_bytes);
+      c->vdevs[0].d_grad = c->d_gin;
+    } else {
+      c->d_recv = dalloc<float>(c->n_dst * R * c->W_total, c->owned, c->dev_bytes);
+      c->d_gin = dalloc<float>(c->n_dst * R * c->W_total, c->owned, c->dev_bytes);
+    }
+    c->d_nseg = dalloc<int32_t>(1, c->owned, c->dev_bytes);
+    c->d_flag = dalloc<int32_t>(1, c->owned, c->dev_bytes);
+    c->d_bd = dalloc<double>(8 * static_cast<int64_t>(num_devices), c->owned, c->dev_bytes);
+    c->d_barrier = dalloc<int32_t>(1, c->owned, c->dev_bytes);
+    SP_CUDA(cudaMemset(c->d_barrier, 0, sizeof(int32_t)));
+    for (auto& e : c->ev_a2a) SP_CUDA(cudaEventCreate(&e));
+    c->sgd_grid = sgd_grid(cuda_device);
+
+    if (world_size > 1) {
+      ncclUniqueId id;
+      std::memcpy(id.internal, nccl_id, SP_NCCL_ID_BYTES);
+      SP_NCCL(nccl().CommInitRank(&c->comm, world_size, id, rank));
+    }
+    *out = c.release();
+  });
+}
+
+void sp_ctx_destroy(sp_ctx* ctx) { delete ctx; }
+
+int sp_ctx_stream(sp_ctx* ctx, void** stream) {
+  return guarded([&] {
+    check_ctx(ctx);
+    *stream = ctx->stream;
+  });
+}
+
+int sp_ctx_device_bytes(sp_ctx* ctx, uint64_t* bytes) {
+  return guarded([&] {
+    check_ctx(ctx);
+    uint64_t b = ctx->dev_bytes;
+    b += ctx->sort_cap * 4 * 5 + ctx->temp_bytes + ctx->stage_cap * 8;
+    for (auto& v : ctx->vdevs) b += v.idx_cap * 4;
+    *bytes = b;
+  });
+}
+
+int sp_ctx_local_tables(sp_ctx* ctx, int32_t* ids, int32_t* n_out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    int32_t n = 0;
+    for (auto& v : ctx->vdevs)
+      for (int g : v.tables) {
+        if (ids) ids[n] = g;
+        ++n;
+      }
+    if (ids) std::sort(ids, ids + n);
+    *n_out = n;
+  });
+}
+
+int sp_init_tables(sp_ctx* ctx, uint64_t seed) {
+  return guarded([&] {
+    check_ctx(ctx);
+    for (auto& v : ctx->vdevs)
+      for (int g : v.tables)
+        launch_init_weights(ctx->d_w + ctx->woff[g], ctx->tables[g].hash_size,
+                            ctx->tables[g].dim, g, seed, ctx->stream);
+    SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sp_set_table(sp_ctx* ctx, int32_t table_id, const float* rows) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (table_id < 0 || table_id >= ctx->M || ctx->woff[table_id] < 0)
+      raise(SP_ERR_UNKNOWN_TABLE, "table id " + std::to_string(table_id) + " is not local");
+    const auto& t = ctx->tables[table_id];
+    SP_CUDA(cudaMemcpyAsync(ctx->d_w + ctx->woff[table_id], rows,
+                            t.hash_size * t.dim * sizeof(float),
+                            cudaMemcpyHostToDevice, ctx->stream));
+    SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sp_get_table(sp_ctx* ctx, int32_t table_id, float* rows) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (table_id < 0 || table_id >= ctx->M || ctx->woff[table_id] < 0)
+      raise(SP_ERR_UNKNOWN_TABLE, "table id " + std::to_string(table_id) + " is not local");
+    const auto& t = ctx->tables[table_id];
+    SP_CUDA(cudaMemcpyAsync(rows, ctx->d_w + ctx->woff[table_id],
+                            t.hash_size * t.dim * sizeof(float),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+static void finish_batch(sp_ctx* c) {
+  int64_t max_nnz = 0;
+  for (auto& v : c->vdevs) max_nnz = std::max(max_nnz, v.nnz);
+  ensure_sort_capacity(c, max_nnz);
+  c->has_batch = true;
+  if (c->graph_exec) {
+    cudaGraphExecDestroy(c->graph_exec);
+    c->graph_exec = nullptr;
+  }
+}
+
+static void alloc_indices(sp_ctx* c, VDev& v, int64_t nnz) {
+  if (nnz > 0x7fffffffLL)
+    raise(SP_ERR_BAD_INPUT, "more than 2^31-1 lookups on one device (int32 CSR)");
+  if (nnz > v.idx_cap || v.d_idx == nullptr) {
+    SP_CUDA(cudaStreamSynchronize(c->stream));
+    if (v.d_idx) cudaFree(v.d_idx);
+    const int64_t cap = std::max<int64_t>(nnz, 1);
+    SP_CUDA(cudaMalloc(&v.d_idx, cap * sizeof(int32_t)));
+    v.idx_cap = cap;
+  }
+  v.nnz = nnz;
+}
+
+int sp_upload_batch(sp_ctx* ctx, const int64_t* offsets, int64_t offsets_len,
+                    const int64_t* indices, int64_t indices_len) {
+  return guarded([&] {
+    check_ctx(ctx);
+    sp_ctx* c = ctx;
+    const int64_t B = c->B;
+    // validate_batch (table.hpp:167-184), O(1) parts on the host; the
+    // monotonicity and index range are checked on the device.
+    if (offsets_len != static_cast<int64_t>(c->M) * B + 1)
+      raise(SP_ERR_MALFORMED_BATCH, "offsets length " + std::to_string(offsets_len) +
+                                        ", expected " + std::to_string(c->M * B + 1));
+    if (offsets[0] != 0) raise(SP_ERR_MALFORMED_BATCH, "offsets must start at 0");
+    if (offsets[offsets_len - 1] != indices_len)
+      raise(SP_ERR_MALFORMED_BATCH, "last offset != indices length");
+    for (int t = 0; t <= c->M; ++t) {
+      const int64_t o = offsets[t * B];
+      if (o < 0 || o > indices_len || (t > 0 && o < offsets[(t - 1) * B]))
+        raise(SP_ERR_MALFORMED_BATCH, "offsets decrease at table " + std::to_string(t));
+    }
+    int64_t stage_need = 0;
+    for (auto& v : c->vdevs) {
+      v.table_nnz.clear();
+      int64_t n = 0, st = 0;
+      for (int g : v.tables) {
+        const int64_t tn = offsets[(g + 1) * B] - offsets[g * B];
+        v.table_nnz.push_back(tn);
+        n += tn;
+        st += tn + B + 1;
+      }
+      alloc_indices(c, v, n);
+      stage_need = std::max(stage_need, st);
+    }
+    if (stage_need > c->stage_cap) {
+      SP_CUDA(cudaStreamSynchronize(c->stream));
+      if (c->d_stage64) cudaFree(c->d_stage64);
+      SP_CUDA(cudaMalloc(&c->d_stage64, std::max<int64_t>(stage_need, 1) * sizeof(int64_t)));
+      c->stage_cap = std::max<int64_t>(stage_need, 1);
+    }
+    SP_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int32_t), c->stream));
+    for (auto& v : c->vdevs) {
+      int64_t so = 0;
+      int32_t base = 0;
+      for (size_t li = 0; li < v.tables.size(); ++li) {
+        const int g = v.tables[li];
+        const int64_t tn = v.table_nnz[li];
+        int64_t* s_off = c->d_stage64 + so;
+        int64_t* s_idx = s_off + B + 1;
+        SP_CUDA(cudaMemcpyAsync(s_off, offsets + g * B, (B + 1) * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, c->stream));
+        if (tn)
+          SP_CUDA(cudaMemcpyAsync(s_idx, indices + offsets[g * B], tn * sizeof(int64_t),
+                                  cudaMemcpyHostToDevice, c->stream));
+        launch_narrow_table(s_off, s_idx, c->B, tn, c->tables[g].hash_size, base,
+                            v.d_off + li * B, v.d_idx + base, c->d_flag, c->stream);
+        // indices of this table land after the earlier tables' indices
+        so += tn + B + 1;
+        base += static_cast<int32_t>(tn);
+      }
+      if (v.tables.empty())
+        SP_CUDA(cudaMemsetAsync(v.d_off, 0, sizeof(int32_t), c->stream));
+    }
+    int32_t flag = 0;
+    SP_CUDA(cudaMemcpyAsync(&flag, c->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    SP_CUDA(cudaStreamSynchronize(c->stream));
+    if (flag & 1) raise(SP_ERR_MALFORMED_BATCH, "offsets decrease inside a table");
+    if (flag & 2) raise(SP_ERR_BAD_INPUT, "lookup index outside [0, hash_size)");
+    finish_batch(c);
+  });
+}
+
+int sp_synth_batch(sp_ctx* ctx, uint64_t seed) {
+  return guarded([&] {
+    check_ctx(ctx);
+    sp_ctx* c = ctx;
+    for (auto& v : c->vdevs) {
+      const int T = static_cast<int>(v.tables.size());
+      const int64_t nb = static_cast<int64_t>(T) * c->B;
+      std::vector<int32_t> gid(T);
+      std::vector<int64_t> lmax(T), rows(T);
+      std::vector<uint64_t> thr(T);
+      for (int li = 0; li < T; ++li) {
+        const auto& t = c->tables[v.tables[li]];
+        gid[li] = v.tables[li];
+        lmax[li] = static_cast<int64_t>(std::floor(2.0 * t.pooling_factor));
+        rows[li] = t.hash_size;
+        double h = 0.0;  // hot_mass (oracle.hpp:119-123)
+        for (int b = 4; b < SP_NUM_BINS; ++b) h += t.dist[b];
+        thr[li] = hot_threshold(h);
+      }
+      std::vector<void*> tmp;
+      uint64_t dummy = 0;
+      int32_t* d_gid = dalloc<int32_t>(T, tmp, dummy);
+      int64_t* d_lmax = dalloc<int64_t>(T, tmp, dummy);
+      int64_t* d_rows = dalloc<int64_t>(T, tmp, dummy);
+      uint64_t* d_thr = dalloc<uint64_t>(T, tmp, dummy);
+      int32_t* d_len = dalloc<int32_t>(nb + 1, tmp, dummy);
+      size_t tb = exclusive_scan_i32(nullptr, 0, d_len, v.d_off, nb + 1, c->stream);
+      void* d_tmp = dalloc<uint8_t>(tb, tmp, dummy);
+      auto cleanup = [&] {
+        cudaStreamSynchronize(c->stream);
+        for (void* p : tmp) cudaFree(p);
+      };
+      try {
+        if (T) {
+          SP_CUDA(cudaMemcpy(d_gid, gid.data(), T * 4, cudaMemcpyHostToDevice));
+          SP_CUDA(cudaMemcpy(d_lmax, lmax.data(), T * 8, cudaMemcpyHostToDevice));
+          SP_CUDA(cudaMemcpy(d_rows, rows.data(), T * 8, cudaMemcpyHostToDevice));
+          SP_CUDA(cudaMemcpy(d_thr, thr.data(), T * 8, cudaMemcpyHostToDevice));
+        }
+        SP_CUDA(cudaMemsetAsync(d_len + nb, 0, sizeof(int32_t), c->stream));
+        if (T) launch_synth_lengths(d_gid, d_lmax, T, c->B, seed, d_len, c->stream);
+        exclusive_scan_i32(d_tmp, tb, d_len, v.d_off, nb + 1, c->stream);
+        int32_t total = 0;
+        SP_CUDA(cudaMemcpyAsync(&total, v.d_off + nb, 4, cudaMemcpyDeviceToHost, c->stream));
+        SP_CUDA(cudaStreamSynchronize(c->stream));
+        alloc_indices(c, v, total);
+        v.table_nnz.assign(T, 0);
+        if (T) launch_synth_indices(d_gid, d_rows, d_thr, T, c->B, seed, v.d_off, v.d_idx, c->stream);
+        // per-table nnz (host copy of the table boundaries)
+        std::vector<int32_t> bounds(T + 1);
+        for (int li = 0; li <= T; ++li)
+          SP_CUDA(cudaMemcpyAsync(&bounds[li], v.d_off + static_cast<int64_t>(li) * c->B, 4,
+                                  cudaMemcpyDeviceToHost, c->stream));
+        SP_CUDA(cudaStreamSynchronize(c->stream));
+        for (int li = 0; li < T; ++li) v.table_nnz[li] = bounds[li + 1] - bounds[li];
+      } catch (...) {
+        cleanup();
+        throw;
+      }
+      cleanup();
+    }
+    finish_batch(c);
+  });
+}
+
+int sp_batch_nnz(sp_ctx* ctx, int64_t* nnz) {
+  return guarded([&] {
+    check_ctx(ctx);
+    int64_t n = 0;
+    for (auto& v : ctx->vdevs) n += v.nnz;
+    *nnz = n;
+  });
+}
+
+int sp_forward(sp_ctx* ctx) {
+  return guarded([&] {
+    check_ctx(ctx);
+    require_batch(ctx);
+    for (auto& v : ctx->vdevs) stage_forward(ctx, v);
+  });
+}
+
+int sp_a2a_forward(sp_ctx* ctx) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!exchange_needed(ctx)) return;
+    if (nccl_mode(ctx)) a2a_fwd_nccl(ctx);
+    else for (auto& v : ctx->vdevs) a2a_fwd_emulated(ctx, v);
+  });
+}
+
+int sp_a2a_backward(sp_ctx* ctx) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!exchange_needed(ctx)) return;
+    if (nccl_mode(ctx)) a2a_bwd_nccl(ctx);
+    else for (auto& v : ctx->vdevs) a2a_bwd_emulated(ctx, v);
+  });
+}
+
+int sp_backward_sgd(sp_ctx* ctx) {
+  return guarded([&] {
+    check_ctx(ctx);
+    require_batch(ctx);
+    for (auto& v : ctx->vdevs) stage_backward(ctx, v);
+  });
+}
+
+// Host permutations between the global [rows, W_total] order and the
+// grouped-by-source exchange layout of one destination slice.
+static void grouped_to_global(const sp_ctx* c, const float* grouped, float* global,
+                              int64_t R) {
+  for (int i = 0; i < c->D; ++i) {
+    const float* src = grouped + R * c->cumW[i];
+    const int64_t Wi = c->dev_W[i];
+    std::vector<int64_t> cols;
+    for (int t = 0; t < c->M; ++t)
+      if (c->placement[t] == i)
+        for (int k = 0; k < c->tables[t].dim; ++k) cols.push_back(c->gcol[t] + k);
+    for (int64_t r = 0; r < R; ++r)
+      for (int64_t k = 0; k < Wi; ++k) global[r * c->W_total + cols[k]] = src[r * Wi + k];
+  }
+}
+
+static void global_to_grouped(const sp_ctx* c, const float* global, float* grouped,
+                              int64_t R) {
+  for (int i = 0; i < c->D; ++i) {
+    float* dst = grouped + R * c->cumW[i];
+    const int64_t Wi = c->dev_W[i];
+    std::vector<int64_t> cols;
+    for (int t = 0; t < c->M; ++t)
+      if (c->placement[t] == i)
+        for (int k = 0; k < c->tables[t].dim; ++k) cols.push_back(c->gcol[t] + k);
+    for (int64_t r = 0; r < R; ++r)
+      for (int64_t k = 0; k < Wi; ++k) dst[r * Wi + k] = global[r * c->W_total + cols[k]];
+  }
+}
+
+int sp_set_grad(sp_ctx* ctx, const float* grad) {
+  return guarded([&] {
+    check_ctx(ctx);
+    const int64_t R = rows_per_dst(ctx);
+    const int64_t n = ctx->n_dst * R * ctx->W_total;
+    std::vector<float> grouped(n);
+    for (int j = 0; j < ctx->n_dst; ++j)
+      global_to_grouped(ctx, grad + j * R * ctx->W_total, grouped.data() + j * R * ctx->W_total, R);
+    SP_CUDA(cudaMemcpyAsync(ctx->d_gin, grouped.data(), n * sizeof(float),
+                            cudaMemcpyHostToDevice, ctx->stream));
+    SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sp_synth_grad(sp_ctx* ctx, uint64_t seed) {
+  return guarded([&] {
+    check_ctx(ctx);
+    const int64_t R = rows_per_dst(ctx);
+    // colmap of every source device (all ranks know the placement)
+    std::vector<std::vector<int32_t>> cm(ctx->D);
+    for (int t = 0; t < ctx->M; ++t)
+      for (int k = 0; k < ctx->tables[t].dim; ++k)
+        cm[ctx->placement[t]].push_back(static_cast<int32_t>(ctx->gcol[t] + k));
+    std::vector<void*> tmp;
+    uint64_t dummy = 0;
+    for (int j = 0; j < ctx->n_dst; ++j) {
+      const int dst = ctx->world == 1 ? j : ctx->rank;
+      for (int i = 0; i < ctx->D; ++i) {
+        if (cm[i].empty()) continue;
+        int32_t* d_cm = dalloc<int32_t>(cm[i].size(), tmp, dummy);
+        SP_CUDA(cudaMemcpy(d_cm, cm[i].data(), cm[i].size() * 4, cudaMemcpyHostToDevice));
+        launch_synth_grad(ctx->d_gin + j * R * ctx->W_total + R * ctx->cumW[i], R,
+                          static_cast<int64_t>(dst) * R, d_cm, ctx->dev_W[i], seed,
+                          ctx->stream);
+      }
+    }
+    SP_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (void* p : tmp) cudaFree(p);
+  });
+}
+
+int sp_get_pooled(sp_ctx* ctx, float* pooled) {
+  return guarded([&] {
+    check_ctx(ctx);
+    const int64_t R = rows_per_dst(ctx);
+    const int64_t n = ctx->n_dst * R * ctx->W_total;
+    std::vector<float> grouped(n);
+    SP_CUDA(cudaMemcpyAsync(grouped.data(), ctx->d_recv, n * sizeof(float),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    SP_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int j = 0; j < ctx->n_dst; ++j)
+      grouped_to_global(ctx, grouped.data() + j * R * ctx->W_total, pooled + j * R * ctx->W_total, R);
+  });
+}
+
+int sp_get_local_pooled(sp_ctx* ctx, int32_t dev, float* pooled) {
+  return guarded([&] {
+    check_ctx(ctx);
+    VDev& v = vdev_for(ctx, dev);
+    SP_CUDA(cudaMemcpyAsync(pooled, v.d_pooled, static_cast<int64_t>(ctx->B) * v.W * sizeof(float),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sp_get_sorted(sp_ctx* ctx, int32_t dev, uint32_t* keys, uint32_t* bags,
+                  int64_t* n_keys, uint32_t* seg_heads, int64_t* n_unique) {
+  return guarded([&] {
+    check_ctx(ctx);
+    require_batch(ctx);
+    VDev& v = vdev_for(ctx, dev);
+    int32_t nseg = 0;
+    if (v.nnz > 0) {
+      stage_sort(ctx, v);
+      SP_CUDA(cudaMemcpyAsync(&nseg, ctx->d_nseg, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      if (keys) SP_CUDA(cudaMemcpyAsync(keys, ctx->d_kb, v.nnz * 4, cudaMemcpyDeviceToHost, ctx->stream));
+      if (bags) SP_CUDA(cudaMemcpyAsync(bags, ctx->d_bb, v.nnz * 4, cudaMemcpyDeviceToHost, ctx->stream));
+      SP_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (seg_heads && nseg)
+        SP_CUDA(cudaMemcpy(seg_heads, ctx->d_seg, static_cast<int64_t>(nseg) * 4, cudaMemcpyDeviceToHost));
+    }
+    if (n_keys) *n_keys = v.nnz;
+    if (n_unique) *n_unique = nseg;
+  });
+}
+
+int sp_run_iteration(sp_ctx* ctx, sp_breakdown* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    require_batch(ctx);
+    sp_ctx* c = ctx;
+    cudaStream_t st = c->stream;
+    const int D = c->D;
+    std::vector<double> fwd(D, 0.0), bwd(D, 0.0), cf(D, 0.0), cb(D, 0.0);
+    // stage 1: fwd compute per (virtual) device
+    for (auto& v : c->vdevs) {
+      SP_CUDA(cudaEventRecord(v.ev[0], st));
+      stage_forward(c, v);
+      SP_CUDA(cudaEventRecord(v.ev[1], st));
+    }
+    // stages 2-3: exchanges (a barrier first so a rank's exchange time is
+    // not its wait for the slowest rank's compute)
+    if (exchange_needed(c)) {
+      if (nccl_mode(c)) {
+        barrier(c);
+        SP_CUDA(cudaEventRecord(c->ev_a2a[0], st));
+        a2a_fwd_nccl(c);
+        SP_CUDA(cudaEventRecord(c->ev_a2a[1], st));
+        barrier(c);
+        SP_CUDA(cudaEventRecord(c->ev_a2a[2], st));
+        a2a_bwd_nccl(c);
+        SP_CUDA(cudaEventRecord(c->ev_a2a[3], st));
+      } else {
+        for (auto& v : c->vdevs) {
+          SP_CUDA(cudaEventRecord(v.ev[2], st));
+          a2a_fwd_emulated(c, v);
+          SP_CUDA(cudaEventRecord(v.ev[3], st));
+        }
+        for (auto& v : c->vdevs) {
+          SP_CUDA(cudaEventRecord(v.ev[4], st));
+          a2a_bwd_emulated(c, v);
+          SP_CUDA(cudaEventRecord(v.ev[5], st));
+        }
+      }
+    }
+    // stage 4: bwd compute
+    for (auto& v : c->vdevs) {
+      SP_CUDA(cudaEventRecord(v.ev[6], st));
+      stage_backward(c, v);
+      SP_CUDA(cudaEventRecord(v.ev[7], st));
+    }
+    SP_CUDA(cudaStreamSynchronize(st));
+    for (auto& v : c->vdevs) {
+      fwd[v.vid] = elapsed(v.ev[0], v.ev[1]);
+      bwd[v.vid] = elapsed(v.ev[6], v.ev[7]);
+      if (exchange_needed(c)) {
+        if (nccl_mode(c)) {
+          cf[v.vid] = elapsed(c->ev_a2a[0], c->ev_a2a[1]);
+          cb[v.vid] = elapsed(c->ev_a2a[2], c->ev_a2a[3]);
+        } else {
+          cf[v.vid] = elapsed(v.ev[2], v.ev[3]);
+          cb[v.vid] = elapsed(v.ev[4], v.ev[5]);
+        }
+      }
+    }
+    if (nccl_mode(c)) {
+      // gather every rank's four numbers
+      double mine[4] = {fwd[c->rank], bwd[c->rank], cf[c->rank], cb[c->rank]};
+      SP_CUDA(cudaMemcpyAsync(c->d_bd + 4 * c->rank, mine, sizeof(mine), cudaMemcpyHostToDevice, st));
+      SP_NCCL(nccl().AllGather(c->d_bd + 4 * c->rank, c->d_bd, 4, ncclFloat64, c->comm, st));
+      std::vector<double> all(4 * D);
+      SP_CUDA(cudaMemcpyAsync(all.data(), c->d_bd, all.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+      SP_CUDA(cudaStreamSynchronize(st));
+      for (int d = 0; d < D; ++d) {
+        fwd[d] = all[4 * d];
+        bwd[d] = all[4 * d + 1];
+        cf[d] = all[4 * d + 2];
+        cb[d] = all[4 * d + 3];
+      }
+    }
+    // composition of oracle.hpp:222-227
+    const double max_fwd = *std::max_element(fwd.begin(), fwd.end());
+    const double max_bwd = *std::max_element(bwd.begin(), bwd.end());
+    const double fstage = *std::max_element(cf.begin(), cf.end());
+    const double bstage = *std::max_element(cb.begin(), cb.end());
+    if (out) {
+      for (int d = 0; d < D; ++d) {
+        if (out->fwd_ms) out->fwd_ms[d] = fwd[d];
+        if (out->bwd_ms) out->bwd_ms[d] = bwd[d];
+        if (out->comm_ms) out->comm_ms[d] = cb[d];
+      }
+      out->fwd_comm_stage_ms = fstage;
+      out->bwd_comm_stage_ms = bstage;
+      out->overall_ms = max_fwd + fstage + bstage + max_bwd;
+    }
+  });
+}
+
+int sp_enqueue_iteration(sp_ctx* ctx) {
+  return guarded([&] {
+    check_ctx(ctx);
+    require_batch(ctx);
+    enqueue_iteration(ctx);
+  });
+}
+
+int sp_graph_replay(sp_ctx* ctx, int32_t iters, int32_t* kernels_per_iter) {
+  return guarded([&] {
+    check_ctx(ctx);
+    require_batch(ctx);
+    sp_ctx* c = ctx;
+    if (!c->graph_exec) {
+      cudaGraph_t g = nullptr;
+      SP_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        enqueue_iteration(c);
+      } catch (...) {
+        cudaStreamEndCapture(c->stream, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      SP_CUDA(cudaStreamEndCapture(c->stream, &g));
+      size_t n = 0;
+      SP_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+      std::vector<cudaGraphNode_t> nodes(n);
+      if (n) SP_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+      int k = 0;
+      for (auto nd : nodes) {
+        cudaGraphNodeType ty;
+        SP_CUDA(cudaGraphNodeGetType(nd, &ty));
+        if (ty == cudaGraphNodeTypeKernel) ++k;
+      }
+      c->graph_kernels = k;
+      SP_CUDA(cudaGraphInstantiate(&c->graph_exec, g, 0));
+      SP_CUDA(cudaGraphDestroy(g));
+    }
+    for (int i = 0; i < iters; ++i) {
+      SP_CUDA(cudaGraphLaunch(c->graph_exec, c->stream));
+      count_launch(c->graph_kernels);
+    }
+    if (kernels_per_iter) *kernels_per_iter = c->graph_kernels;
+  });
+}
+
+int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]) {
+  return guarded([&] {
+    check_ctx(ctx);
+    require_batch(ctx);
+    sp_ctx* c = ctx;
+    // Max over the (virtual) devices held here of the SURVEY §8d formulas.
+    double fwd = 0, a2a = 0, bwd = 0, sort = 0;
+    for (auto& v : c->vdevs) {
+      const int T = static_cast<int>(v.tables.size());
+      double rows_bytes = 0;
+      for (int li = 0; li < T; ++li)
+        rows_bytes += 4.0 * static_cast<double>(v.table_nnz[li]) * c->tables[v.tables[li]].dim;
+      const double csr = 4.0 * (static_cast<double>(T) * c->B + 1) + 4.0 * v.nnz;
+      const double outb = 4.0 * c->B * v.W;
+      fwd = std::max(fwd, csr + rows_bytes + outb);
+      a2a = std::max(a2a, 4.0 * c->B * v.W * (c->D - 1) / c->D);
+      // unique rows per table from the run heads
+      double uniq_dim = 0;
+      if (v.nnz) {
+        uint32_t *keys = nullptr;
+        std::vector<uint32_t> k(v.nnz), heads;
+        keys = k.data();
+        int64_t nk = 0, nu = 0;
+        stage_sort(c, v);
+        int32_t nseg = 0;
+        SP_CUDA(cudaMemcpyAsync(&nseg, c->d_nseg, 4, cudaMemcpyDeviceToHost, c->stream));
+        SP_CUDA(cudaMemcpyAsync(keys, c->d_kb, v.nnz * 4, cudaMemcpyDeviceToHost, c->stream));
+        SP_CUDA(cudaStreamSynchronize(c->stream));
+        heads.resize(nseg);
+        if (nseg) SP_CUDA(cudaMemcpy(heads.data(), c->d_seg, static_cast<int64_t>(nseg) * 4, cudaMemcpyDeviceToHost));
+        (void)nk;
+        nu = nseg;
+        for (int64_t u = 0; u < nu; ++u) {
+          const uint32_t key = keys[heads[u]];
+          const int li = static_cast<int>(std::upper_bound(v.rb_end.begin(), v.rb_end.end(), key) - v.rb_end.begin());
+          uniq_dim += c->tables[v.tables[li]].dim;
+        }
+      }
+      bwd = std::max(bwd, outb + csr + 8.0 * uniq_dim);
+      // onesweep radix sort: ~ (passes) x read+write of 8-byte pairs
+      const int passes = (v.end_bit + 7) / 8;
+      sort = std::max(sort, 16.0 * v.nnz * passes);
+    }
+    out[0] = fwd;
+    out[1] = a2a;
+    out[2] = bwd;
+    out[3] = sort;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,109 @@
+// tbe.h — device-side layout of one (virtual) device's embedding shard and
+// the launchers of the hot kernels (K1 forward, K4 backward).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sp {
+
+// One local table of a (virtual) device, in kernel order.
+struct TableMeta {
+  int64_t woff;         // float offset of row 0 in the weight slab
+  int64_t rows;         // hash_size
+  int64_t block_start;  // K1: first block of this table in the grid
+  int32_t dim;
+  int32_t lcol;         // first column in the local pooled [B, W_local]
+  uint32_t rowbase;     // K4 key base: sum of rows of earlier local tables
+  int32_t cls;          // dim class, see dim_class(); -1 = generic path
+  int32_t local;        // canonical local index (ascending global id)
+  int32_t gid;          // global table id
+};
+
+// Dim class: 0..5 for dim = 4,8,16,32,64,128 (float4 row slices), -1 else.
+inline int dim_class(int dim) {
+  switch (dim) {
+    case 4: return 0;
+    case 8: return 1;
+    case 16: return 2;
+    case 32: return 3;
+    case 64: return 4;
+    case 128: return 5;
+    default: return -1;
+  }
+}
+
+// Bags (K1) or unique rows (K4) per warp for each dim class: the warp is
+// split into P spans of 32/P lanes; a span sums one bag / one row's
+// gradients with (32/P)/(dim/4) row groups.
+inline int rows_per_warp(int cls) {
+  switch (cls) {
+    case 0: return 8;
+    case 1: return 8;
+    case 2: return 4;
+    case 3: return 2;
+    case 4: return 2;
+    case 5: return 1;
+    default: return 1;
+  }
+}
+
+constexpr int kWarpsPerBlock = 8;
+constexpr int kBlockThreads = 32 * kWarpsPerBlock;
+
+// ---- K1: fused multi-table sum-pooled forward ----------------------------
+// One launch over all local tables: out[b, lcol_t : lcol_t + dim_t] =
+// sum_{p in [off[i*B+b], off[i*B+b+1])} W_t[idx[p], :]  (int32 CSR).
+void launch_tbe_forward(const TableMeta* d_meta, int n_tables,
+                        int64_t n_blocks, int batch, const int32_t* d_off,
+                        const int32_t* d_idx, const float* d_w, float* d_out,
+                        int64_t ldo, cudaStream_t st);
+
+// ---- K4: backward = keys -> stable radix sort -> segments -> SGD ---------
+// keys[p] = rowbase_i + idx[p], bags[p] = b for every position of the CSR.
+void launch_build_keys(const TableMeta* d_meta_canon, int n_tables, int batch,
+                       const int32_t* d_off, const int32_t* d_idx,
+                       uint32_t* d_keys, uint32_t* d_bags, cudaStream_t st);
+// Segment heads of sorted keys: seg[u] = first position of the u-th run,
+// *d_nseg = number of runs. temp: CUB scratch (query with temp == nullptr).
+size_t select_heads(void* temp, size_t temp_bytes, const uint32_t* d_keys,
+                    int64_t n, uint32_t* d_seg, int32_t* d_nseg,
+                    cudaStream_t st);
+size_t sort_pairs(void* temp, size_t temp_bytes, uint32_t* keys_in,
+                  uint32_t* keys_out, uint32_t* vals_in, uint32_t* vals_out,
+                  int64_t n, int end_bit, cudaStream_t st);
+// Row-wise SGD over the segments (persistent grid):
+// W[row] -= lr * sum_{k in segment, sorted order} grad[bags[k], lcol..].
+void launch_sgd(const TableMeta* d_meta_canon, const uint32_t* d_rowbase_end,
+                int n_tables, const uint32_t* d_keys, const uint32_t* d_bags,
+                const uint32_t* d_seg, const int32_t* d_nseg, int64_t n,
+                const float* d_grad, int64_t ldg, float lr, float* d_w,
+                int grid, cudaStream_t st);
+int sgd_grid(int device);
+
+// ---- generator / layout helpers ------------------------------------------
+void launch_init_weights(float* d_w, int64_t rows, int dim, int32_t gid,
+                         uint64_t seed, cudaStream_t st);
+// lengths of the bags of local tables (gid, lmax per table) into d_len[i*B+b]
+void launch_synth_lengths(const int32_t* d_gid, const int64_t* d_lmax,
+                          int n_tables, int batch, uint64_t seed,
+                          int32_t* d_len, cudaStream_t st);
+size_t exclusive_scan_i32(void* temp, size_t temp_bytes, const int32_t* in,
+                          int32_t* out, int64_t n, cudaStream_t st);
+void launch_synth_indices(const int32_t* d_gid, const int64_t* d_rows,
+                          const uint64_t* d_thr, int n_tables, int batch,
+                          uint64_t seed, const int32_t* d_off, int32_t* d_idx,
+                          cudaStream_t st);
+// int64 LookupBatch segment -> int32 local CSR with validation flags.
+// off64: B+1 offsets of one table (absolute); idx64: its indices.
+void launch_narrow_table(const int64_t* d_off64, const int64_t* d_idx64,
+                         int batch, int64_t nnz, int64_t rows, int32_t base,
+                         int32_t* d_off, int32_t* d_idx, int32_t* d_flag,
+                         cudaStream_t st);
+// grad_in grouped layout: [src][rows_per_dst][W_src] per destination slice.
+void launch_synth_grad(float* d_grad, int64_t n_rows, int64_t bag0,
+                       const int32_t* d_colmap, int64_t width, uint64_t seed,
+                       cudaStream_t st);
+
+}  // namespace sp
