@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -48,12 +49,15 @@ T* dalloc(size_t n, std::vector<void*>& owned, uint64_t& bytes) {
 struct VDev {
   int vid = 0;
   std::vector<int> tables;  // global ids, ascending
-  std::vector<TableMeta> meta_canon, meta_grid;
+  std::vector<TableMeta> meta_canon;
   std::vector<uint32_t> rb_end;
   std::vector<int32_t> colmap;  // local col -> global col
-  int64_t W = 0, rows_total = 0, fwd_blocks = 0;
+  int64_t W = 0, rows_total = 0, n_tiles = 0;
   int end_bit = 1;
-  TableMeta* d_meta_grid = nullptr;
+  int4* d_tiles = nullptr;      // K1 tiles in launch order
+  uint32_t* d_keys = nullptr;   // backward sort pairs (written by K1)
+  uint32_t* d_bags = nullptr;
+  bool keys_valid = false;
   TableMeta* d_meta_canon = nullptr;
   uint32_t* d_rb_end = nullptr;
   int32_t* d_colmap = nullptr;
@@ -85,8 +89,9 @@ struct sp_ctx {
   float* d_recv = nullptr;     // rows_per_dst * W_total per destination
   float* d_gin = nullptr;
   int n_dst = 1;               // destinations held here (D in emulation)
-  uint32_t *d_ka = nullptr, *d_kb = nullptr, *d_ba = nullptr, *d_bb = nullptr;
+  uint32_t *d_kb = nullptr, *d_bb = nullptr;  // sorted keys / bags
   uint32_t* d_seg = nullptr;
+  bool fuse_keys = true;       // K1 emits the backward's sort pairs
   int32_t* d_nseg = nullptr;
   int32_t* d_flag = nullptr;
   int64_t sort_cap = 0;
@@ -94,7 +99,6 @@ struct sp_ctx {
   size_t temp_bytes = 0;
   int64_t* d_stage64 = nullptr;
   int64_t stage_cap = 0;
-  int sgd_grid = 0;
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
   double* d_bd = nullptr;      // breakdown gather buffer
@@ -116,6 +120,11 @@ struct sp_ctx {
         if (e) cudaEventDestroy(e);
     for (auto& e : ev_a2a)
       if (e) cudaEventDestroy(e);
+    for (auto& v : vdevs)
+      for (void* p : {static_cast<void*>(v.d_idx), static_cast<void*>(v.d_keys),
+                       static_cast<void*>(v.d_bags)})
+        if (p) cudaFree(p);
+    if (d_stage64) cudaFree(d_stage64);
     for (void* p : sort_owned) cudaFree(p);
     for (void* p : owned) cudaFree(p);
     if (comm) sp::nccl().CommDestroy(comm);
@@ -128,7 +137,7 @@ namespace {
 
 int64_t rows_per_dst(const sp_ctx* c) { return c->B / c->D; }
 
-// Frees and re-allocates the sort scratch for n positions.
+// Frees and re-allocates the shared sort scratch for n positions.
 void ensure_sort_capacity(sp_ctx* c, int64_t n) {
   if (n <= c->sort_cap && c->d_temp) return;
   SP_CUDA(cudaStreamSynchronize(c->stream));
@@ -136,20 +145,16 @@ void ensure_sort_capacity(sp_ctx* c, int64_t n) {
   c->sort_owned.clear();
   const int64_t cap = std::max<int64_t>(n, 1);
   uint64_t dummy = 0;
-  c->d_ka = dalloc<uint32_t>(cap, c->sort_owned, dummy);
   c->d_kb = dalloc<uint32_t>(cap, c->sort_owned, dummy);
-  c->d_ba = dalloc<uint32_t>(cap, c->sort_owned, dummy);
   c->d_bb = dalloc<uint32_t>(cap, c->sort_owned, dummy);
   c->d_seg = dalloc<uint32_t>(cap + 1, c->sort_owned, dummy);
   int max_bit = 1;
   for (auto& v : c->vdevs) max_bit = std::max(max_bit, v.end_bit);
-  size_t t1 = sort_pairs(nullptr, 0, c->d_ka, c->d_kb, c->d_ba, c->d_bb, cap,
-                         max_bit, c->stream);
-  size_t t2 = select_heads(nullptr, 0, c->d_kb, cap, c->d_seg, c->d_nseg,
-                           c->stream);
-  size_t t3 = exclusive_scan_i32(nullptr, 0, nullptr, nullptr,
-                                 static_cast<int64_t>(c->B) * 256 + 1, c->stream);
-  c->temp_bytes = std::max({t1, t2, t3, static_cast<size_t>(256)});
+  const size_t t1 = sort_pairs(nullptr, 0, c->d_kb, c->d_kb, c->d_bb, c->d_bb, cap,
+                               max_bit, c->stream);
+  const size_t t2 = select_heads(nullptr, 0, c->d_kb, cap, c->d_seg, c->d_nseg,
+                                 c->stream);
+  c->temp_bytes = std::max({t1, t2, static_cast<size_t>(256)});
   c->d_temp = dalloc<uint8_t>(c->temp_bytes, c->sort_owned, dummy);
   c->sort_cap = cap;
 }
@@ -172,28 +177,29 @@ void require_batch(sp_ctx* c) {
 // ---- stages ---------------------------------------------------------------
 
 void stage_forward(sp_ctx* c, VDev& v) {
-  launch_tbe_forward(v.d_meta_grid, static_cast<int>(v.tables.size()),
-                     v.fwd_blocks, c->B, v.d_off, v.d_idx, c->d_w, v.d_pooled,
-                     v.W, c->stream);
+  const bool emit = c->fuse_keys && v.nnz > 0;
+  launch_tbe_forward(v.d_meta_canon, v.d_tiles, v.n_tiles, c->B, v.d_off, v.d_idx,
+                     c->d_w, v.d_pooled, v.W, emit ? v.d_keys : nullptr,
+                     emit ? v.d_bags : nullptr, c->stream);
+  if (emit) v.keys_valid = true;
 }
 
-// keys -> sort -> heads; leaves sorted keys in d_kb, bags in d_bb.
+// (keys) -> stable radix sort; leaves sorted keys in d_kb, bags in d_bb.
 void stage_sort(sp_ctx* c, VDev& v) {
-  const int T = static_cast<int>(v.tables.size());
-  launch_build_keys(v.d_meta_canon, T, c->B, v.d_off, v.d_idx, c->d_ka, c->d_ba,
-                    c->stream);
-  sort_pairs(c->d_temp, c->temp_bytes, c->d_ka, c->d_kb, c->d_ba, c->d_bb, v.nnz,
+  if (!v.keys_valid) {
+    launch_build_keys(v.d_meta_canon, static_cast<int>(v.tables.size()), c->B, v.d_off,
+                      v.d_idx, v.d_keys, v.d_bags, c->stream);
+    v.keys_valid = true;
+  }
+  sort_pairs(c->d_temp, c->temp_bytes, v.d_keys, c->d_kb, v.d_bags, c->d_bb, v.nnz,
              v.end_bit, c->stream);
-  select_heads(c->d_temp, c->temp_bytes, c->d_kb, v.nnz, c->d_seg, c->d_nseg,
-               c->stream);
 }
 
 void stage_backward(sp_ctx* c, VDev& v) {
   if (v.nnz == 0) return;
   stage_sort(c, v);
-  launch_sgd(v.d_meta_canon, v.d_rb_end, static_cast<int>(v.tables.size()),
-             c->d_kb, c->d_bb, c->d_seg, c->d_nseg, v.nnz, v.d_grad, v.W, c->lr,
-             c->d_w, c->sgd_grid, c->stream);
+  launch_sgd(v.d_meta_canon, v.d_rb_end, static_cast<int>(v.tables.size()), c->d_kb,
+             c->d_bb, v.nnz, v.d_grad, v.W, c->lr, c->d_w, c->stream);
 }
 
 bool nccl_mode(const sp_ctx* c) { return c->world > 1; }
@@ -439,21 +445,15 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
         const auto& tb = tables[v.tables[b]];
         return ta.pooling_factor * ta.dim > tb.pooling_factor * tb.dim;
       });
-      int64_t blk = 0;
-      for (int li : order) {
-        TableMeta m = v.meta_canon[li];
-        m.block_start = blk;
-        const int per_block = kWarpsPerBlock * rows_per_warp(m.cls);
-        blk += (batch_size + per_block - 1) / per_block;
-        v.meta_grid.push_back(m);
-      }
-      v.fwd_blocks = blk;
-      v.d_meta_grid = dalloc<TableMeta>(T, c->owned, c->dev_bytes);
+      const std::vector<int4> tiles = make_fwd_tiles(v.meta_canon, order, batch_size);
+      v.n_tiles = static_cast<int64_t>(tiles.size());
+      v.d_tiles = dalloc<int4>(tiles.size(), c->owned, c->dev_bytes);
+      if (!tiles.empty())
+        SP_CUDA(cudaMemcpy(v.d_tiles, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice));
       v.d_meta_canon = dalloc<TableMeta>(T, c->owned, c->dev_bytes);
       v.d_rb_end = dalloc<uint32_t>(T, c->owned, c->dev_bytes);
       v.d_colmap = dalloc<int32_t>(v.W, c->owned, c->dev_bytes);
       if (T) {
-        SP_CUDA(cudaMemcpy(v.d_meta_grid, v.meta_grid.data(), T * sizeof(TableMeta), cudaMemcpyHostToDevice));
         SP_CUDA(cudaMemcpy(v.d_meta_canon, v.meta_canon.data(), T * sizeof(TableMeta), cudaMemcpyHostToDevice));
         SP_CUDA(cudaMemcpy(v.d_rb_end, v.rb_end.data(), T * sizeof(uint32_t), cudaMemcpyHostToDevice));
       }
@@ -484,7 +484,7 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
     c->d_barrier = dalloc<int32_t>(1, c->owned, c->dev_bytes);
     SP_CUDA(cudaMemset(c->d_barrier, 0, sizeof(int32_t)));
     for (auto& e : c->ev_a2a) SP_CUDA(cudaEventCreate(&e));
-    c->sgd_grid = sgd_grid(cuda_device);
+    if (const char* f = std::getenv("SP_FUSE_KEYS")) c->fuse_keys = std::atoi(f) != 0;
 
     if (world_size > 1) {
       ncclUniqueId id;
@@ -508,8 +508,8 @@ int sp_ctx_device_bytes(sp_ctx* ctx, uint64_t* bytes) {
   return guarded([&] {
     check_ctx(ctx);
     uint64_t b = ctx->dev_bytes;
-    b += ctx->sort_cap * 4 * 5 + ctx->temp_bytes + ctx->stage_cap * 8;
-    for (auto& v : ctx->vdevs) b += v.idx_cap * 4;
+    b += ctx->sort_cap * 4 * 3 + ctx->temp_bytes + ctx->stage_cap * 8;
+    for (auto& v : ctx->vdevs) b += v.idx_cap * 12;
     *bytes = b;
   });
 }
@@ -581,12 +581,19 @@ static void alloc_indices(sp_ctx* c, VDev& v, int64_t nnz) {
     raise(SP_ERR_BAD_INPUT, "more than 2^31-1 lookups on one device (int32 CSR)");
   if (nnz > v.idx_cap || v.d_idx == nullptr) {
     SP_CUDA(cudaStreamSynchronize(c->stream));
-    if (v.d_idx) cudaFree(v.d_idx);
+    for (void* p : {static_cast<void*>(v.d_idx), static_cast<void*>(v.d_keys),
+                     static_cast<void*>(v.d_bags)})
+      if (p) cudaFree(p);
+    v.d_idx = nullptr;
+    v.d_keys = v.d_bags = nullptr;
     const int64_t cap = std::max<int64_t>(nnz, 1);
     SP_CUDA(cudaMalloc(&v.d_idx, cap * sizeof(int32_t)));
+    SP_CUDA(cudaMalloc(&v.d_keys, cap * sizeof(uint32_t)));
+    SP_CUDA(cudaMalloc(&v.d_bags, cap * sizeof(uint32_t)));
     v.idx_cap = cap;
   }
   v.nnz = nnz;
+  v.keys_valid = false;
 }
 
 int sp_upload_batch(sp_ctx* ctx, const int64_t* offsets, int64_t offsets_len,
@@ -871,6 +878,8 @@ int sp_get_sorted(sp_ctx* ctx, int32_t dev, uint32_t* keys, uint32_t* bags,
     int32_t nseg = 0;
     if (v.nnz > 0) {
       stage_sort(ctx, v);
+      select_heads(ctx->d_temp, ctx->temp_bytes, ctx->d_kb, v.nnz, ctx->d_seg, ctx->d_nseg,
+                   ctx->stream);
       SP_CUDA(cudaMemcpyAsync(&nseg, ctx->d_nseg, 4, cudaMemcpyDeviceToHost, ctx->stream));
       if (keys) SP_CUDA(cudaMemcpyAsync(keys, ctx->d_kb, v.nnz * 4, cudaMemcpyDeviceToHost, ctx->stream));
       if (bags) SP_CUDA(cudaMemcpyAsync(bags, ctx->d_bb, v.nnz * 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1045,13 +1054,13 @@ int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]) {
         keys = k.data();
         int64_t nk = 0, nu = 0;
         stage_sort(c, v);
+        select_heads(c->d_temp, c->temp_bytes, c->d_kb, v.nnz, c->d_seg, c->d_nseg, c->stream);
         int32_t nseg = 0;
         SP_CUDA(cudaMemcpyAsync(&nseg, c->d_nseg, 4, cudaMemcpyDeviceToHost, c->stream));
         SP_CUDA(cudaMemcpyAsync(keys, c->d_kb, v.nnz * 4, cudaMemcpyDeviceToHost, c->stream));
         SP_CUDA(cudaStreamSynchronize(c->stream));
         heads.resize(nseg);
         if (nseg) SP_CUDA(cudaMemcpy(heads.data(), c->d_seg, static_cast<int64_t>(nseg) * 4, cudaMemcpyDeviceToHost));
-        (void)nk;
         nu = nseg;
         for (int64_t u = 0; u < nu; ++u) {
           const uint32_t key = keys[heads[u]];

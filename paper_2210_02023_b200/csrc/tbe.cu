@@ -1,18 +1,21 @@
 // tbe.cu — hot kernels of the embedding stage on sm_100a.
 //
-//   K1 tbe_forward_kernel  — fused multi-table sum-pooled EmbeddingBag
-//                            forward (the reference's fused_kernel stage,
-//                            oracle.hpp:163-174, executed for real);
-//   K4 build_keys / CUB radix sort / head select / sgd_kernel — the
-//                            backward (oracle.hpp:149 bwd_comp): duplicate
-//                            rows are reduced in a fixed order before one
-//                            coalesced row-wise SGD write-back.
+//   K1 tbe_forward_kernel — fused multi-table sum-pooled EmbeddingBag
+//      forward (the reference's fused_kernel stage, oracle.hpp:163-174,
+//      executed for real). Optionally emits the backward's sort keys.
+//   K4 build_keys (when K1 did not emit them) -> CUB stable radix sort ->
+//      sgd_kernel — the backward (oracle.hpp:149 bwd_comp): duplicate rows
+//      are reduced in the sorted (= original) order before one coalesced
+//      row-wise SGD write-back.
 //
-// Both gathers are HBM-bound random row reads. A warp is split into P
-// spans (one bag / one unique row each); a span splits into GB row groups
-// of L = dim/4 lanes, each lane moving one 16-byte float4 slice. Every
-// group keeps U independent row loads in flight. Partial sums combine with
-// a fixed xor-shuffle tree, so results are bitwise reproducible run to run.
+// Both are HBM-bound random row gathers. Each block owns a tile: K1 a run
+// of consecutive bags of one table, K4 a run of sorted positions. The tile's
+// offsets/indices (K1) or keys/bags (K4) are staged in shared memory with
+// coalesced loads, so the only long-latency dependency left per bag/row is
+// the row gather itself. A warp is split into P spans (one bag / one unique
+// row each); a span splits into GB groups of L = dim/4 lanes, each lane
+// moving one 16-byte float4 slice, U rows in flight per group. Partial
+// sums combine with a fixed xor-shuffle tree: bitwise reproducible.
 #include <cub/cub.cuh>
 
 #include "common.h"
@@ -38,111 +41,169 @@ __device__ __forceinline__ float4 shfl_xor_f4(float4 v, int m) {
   return v;
 }
 
-// Config per dim class: L lanes per row, P spans per warp, U unroll.
-template <int CLS>
-struct Cfg;
-template <> struct Cfg<0> { static constexpr int L = 1, P = 8, U = 4; };
-template <> struct Cfg<1> { static constexpr int L = 2, P = 8, U = 4; };
-template <> struct Cfg<2> { static constexpr int L = 4, P = 4, U = 4; };
-template <> struct Cfg<3> { static constexpr int L = 8, P = 2, U = 4; };
-template <> struct Cfg<4> { static constexpr int L = 16, P = 2, U = 8; };
-template <> struct Cfg<5> { static constexpr int L = 32, P = 1, U = 8; };
+// Geometry per dim class (dim = 4, 8, 16, 32, 64, 128 for class 0..5):
+// a row is split over L lanes, each lane moving V float4 (16V bytes); a
+// warp holds P spans (one bag / one unique row each) of 32/P lanes; a span
+// holds GB = (32/P)/L row groups, each keeping U rows in flight.
+template <int L_, int V_, int P_, int U_>
+struct Geo {
+  static constexpr int L = L_, V = V_, P = P_, U = U_;
+  static constexpr int S = 32 / P, GB = S / L;
+  static_assert(S % L == 0 && GB >= 1, "bad geometry");
+};
+// K1: bags are ~2*pf long; GB*U rows of a bag in flight.
+template <int CLS> struct FwdGeo;
+template <> struct FwdGeo<0> : Geo<1, 1, 8, 4> {};
+template <> struct FwdGeo<1> : Geo<2, 1, 8, 4> {};
+template <> struct FwdGeo<2> : Geo<4, 1, 4, 4> {};
+template <> struct FwdGeo<3> : Geo<8, 1, 2, 4> {};
+template <> struct FwdGeo<4> : Geo<16, 1, 2, 8> {};
+template <> struct FwdGeo<5> : Geo<32, 1, 1, 8> {};
+// K4 SGD: most runs hold 1-2 positions, so more runs per warp (P) matter
+// more than rows per run; lanes move up to 64 B of a row.
+template <int CLS> struct SgdGeo;
+template <> struct SgdGeo<0> : Geo<1, 1, 16, 2> {};
+template <> struct SgdGeo<1> : Geo<2, 1, 16, 2> {};
+template <> struct SgdGeo<2> : Geo<2, 2, 16, 2> {};
+template <> struct SgdGeo<3> : Geo<4, 2, 8, 2> {};
+template <> struct SgdGeo<4> : Geo<4, 4, 8, 2> {};
+template <> struct SgdGeo<5> : Geo<8, 4, 4, 2> {};
+// K4 SGD, long runs (hot rows): the whole warp on one run.
+template <int CLS> struct LongGeo;
+template <> struct LongGeo<0> : Geo<1, 1, 1, 4> {};
+template <> struct LongGeo<1> : Geo<2, 1, 1, 4> {};
+template <> struct LongGeo<2> : Geo<4, 1, 1, 4> {};
+template <> struct LongGeo<3> : Geo<8, 1, 1, 4> {};
+template <> struct LongGeo<4> : Geo<16, 1, 1, 8> {};
+template <> struct LongGeo<5> : Geo<32, 1, 1, 8> {};
 
 // ---------------------------------------------------------------------------
 // K1
 
-// One warp: P consecutive bags [b0, b0+P) of table m.
-template <int CLS>
-__device__ __forceinline__ void fwd_warp(const TableMeta& m, int batch,
-                                         int b0, int lane,
-                                         const int32_t* __restrict__ off,
-                                         const int32_t* __restrict__ idx,
-                                         const float* __restrict__ w,
-                                         float* __restrict__ out,
-                                         int64_t ldo) {
-  constexpr int L = Cfg<CLS>::L, P = Cfg<CLS>::P, U = Cfg<CLS>::U;
-  constexpr int S = 32 / P, GB = S / L;
+struct FwdTile {
+  int32_t t;   // canonical local table index
+  int32_t b0;  // first bag
+  int32_t nb;  // bags in the tile
+  int32_t pad;
+};
+
+constexpr int kTileBags = 256;
+constexpr int kIdxCap = 4096;  // staged indices per tile (16 KB)
+
+template <class G>
+__device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb,
+                                              int p0, int warp, int lane,
+                                              const int32_t* s_off,
+                                              const int32_t* s_idx,
+                                              const int32_t* __restrict__ idx,
+                                              const float* __restrict__ w,
+                                              float* __restrict__ out,
+                                              int64_t ldo) {
+  constexpr int L = G::L, V = G::V, P = G::P, U = G::U, S = G::S, GB = G::GB;
   const int span = lane / S, ls = lane % S, g = ls / L, s = ls % L;
-  const int b = b0 + span;
-  const bool ok = b < batch;
-  int beg = 0, end = 0;
-  if (ok) {
-    const int64_t k = static_cast<int64_t>(m.local) * batch + b;
-    beg = off[k];
-    end = off[k + 1];
-  }
-  const float* wt = w + m.woff + 4 * s;
+  const float* wt = w + m.woff + 4 * V * s;
   const int dim = m.dim;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int k = beg + g; k < end; k += GB * U) {
-    int r[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int kk = k + u * GB;
-      r[u] = kk < end ? __ldg(idx + kk) : -1;
+  for (int bg = warp * P; bg < nb; bg += kWarpsPerBlock * P) {
+    const int bag = bg + span;
+    const bool ok = bag < nb;
+    int beg = 0, end = 0;
+    if (ok) {
+      beg = s_off[bag] - p0;
+      end = s_off[bag + 1] - p0;
     }
-    float4 v[U];
+    float4 acc[V];
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      v[u] = r[u] >= 0 ? ldg_f4(wt + static_cast<int64_t>(r[u]) * dim)
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < V; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = beg + g; k < end; k += GB * U) {
+      int r[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) acc = f4_add(acc, v[u]);
+      for (int u = 0; u < U; ++u) {
+        const int kk = k + u * GB;
+        r[u] = kk < end ? (kk < kIdxCap ? s_idx[kk] : __ldg(idx + p0 + kk)) : -1;
+      }
+      float4 v[U][V];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+          v[u][j] = r[u] >= 0 ? ldg_f4(wt + static_cast<int64_t>(r[u]) * dim + 4 * j)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] = f4_add(acc[j], v[u][j]);
+    }
+#pragma unroll
+    for (int o = L; o < S; o <<= 1)
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[j] = f4_add(acc[j], shfl_xor_f4(acc[j], o));
+    if (ok && g == 0) {
+      float* o = out + static_cast<int64_t>(b0 + bag) * ldo + m.lcol + 4 * V * s;
+#pragma unroll
+      for (int j = 0; j < V; ++j) *reinterpret_cast<float4*>(o + 4 * j) = acc[j];
+    }
   }
-#pragma unroll
-  for (int o = L; o < S; o <<= 1) acc = f4_add(acc, shfl_xor_f4(acc, o));
-  if (ok && g == 0)
-    *reinterpret_cast<float4*>(out + static_cast<int64_t>(b) * ldo + m.lcol +
-                               4 * s) = acc;
 }
 
 // Any dim: one warp per bag, 32 scalar columns at a time.
-__device__ __forceinline__ void fwd_warp_generic(
-    const TableMeta& m, int batch, int b, int lane,
-    const int32_t* __restrict__ off, const int32_t* __restrict__ idx,
+__device__ __forceinline__ void fwd_tile_warp_generic(
+    const TableMeta& m, int b0, int nb, int p0, int warp, int lane,
+    const int32_t* s_off, const int32_t* s_idx, const int32_t* __restrict__ idx,
     const float* __restrict__ w, float* __restrict__ out, int64_t ldo) {
-  if (b >= batch) return;
-  const int64_t k = static_cast<int64_t>(m.local) * batch + b;
-  const int beg = off[k], end = off[k + 1];
-  for (int c0 = 0; c0 < m.dim; c0 += 32) {
-    const int c = c0 + lane;
-    float acc = 0.f;
-    for (int p = beg; p < end; ++p) {
-      const int r = __ldg(idx + p);
-      if (c < m.dim) acc += __ldg(w + m.woff + static_cast<int64_t>(r) * m.dim + c);
+  for (int bag = warp; bag < nb; bag += kWarpsPerBlock) {
+    const int beg = s_off[bag] - p0, end = s_off[bag + 1] - p0;
+    for (int c0 = 0; c0 < m.dim; c0 += 32) {
+      const int c = c0 + lane;
+      float acc = 0.f;
+      for (int k = beg; k < end; ++k) {
+        const int r = k < kIdxCap ? s_idx[k] : __ldg(idx + p0 + k);
+        if (c < m.dim) acc += __ldg(w + m.woff + static_cast<int64_t>(r) * m.dim + c);
+      }
+      if (c < m.dim) out[static_cast<int64_t>(b0 + bag) * ldo + m.lcol + c] = acc;
     }
-    if (c < m.dim) out[static_cast<int64_t>(b) * ldo + m.lcol + c] = acc;
   }
 }
 
+template <bool kEmitKeys>
 __global__ void __launch_bounds__(kBlockThreads)
-    tbe_forward_kernel(const TableMeta* __restrict__ meta, int n_tables,
-                       int batch, const int32_t* __restrict__ off,
+    tbe_forward_kernel(const TableMeta* __restrict__ meta,
+                       const FwdTile* __restrict__ tiles, int batch,
+                       const int32_t* __restrict__ off,
                        const int32_t* __restrict__ idx,
                        const float* __restrict__ w, float* __restrict__ out,
-                       int64_t ldo) {
-  // block -> table (meta is in grid order; block_start ascending)
-  __shared__ int s_t;
-  if (threadIdx.x == 0) {
-    int lo = 0, hi = n_tables - 1;
-    const int64_t blk = blockIdx.x;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (meta[mid].block_start <= blk) lo = mid; else hi = mid - 1;
+                       int64_t ldo, uint32_t* __restrict__ keys,
+                       uint32_t* __restrict__ bags) {
+  __shared__ int32_t s_off[kTileBags + 1];
+  __shared__ int32_t s_idx[kIdxCap];
+  const FwdTile tile = tiles[blockIdx.x];
+  const TableMeta m = meta[tile.t];
+  const int64_t base = static_cast<int64_t>(tile.t) * batch + tile.b0;
+  for (int i = threadIdx.x; i <= tile.nb; i += kBlockThreads) s_off[i] = off[base + i];
+  __syncthreads();
+  const int p0 = s_off[0];
+  const int np = s_off[tile.nb] - p0;
+  for (int i = threadIdx.x; i < np; i += kBlockThreads) {
+    const int32_t v = __ldg(idx + p0 + i);
+    if (i < kIdxCap) s_idx[i] = v;
+    if (kEmitKeys) {
+      // bag of position i: last j with s_off[j] <= p0 + i
+      int lo = 0, hi = tile.nb - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_off[mid] <= p0 + i) lo = mid; else hi = mid - 1;
+      }
+      keys[p0 + i] = m.rowbase + static_cast<uint32_t>(v);
+      bags[p0 + i] = static_cast<uint32_t>(tile.b0 + lo);
     }
-    s_t = lo;
   }
   __syncthreads();
-  const TableMeta m = meta[s_t];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t blk_in_table = blockIdx.x - m.block_start;
   switch (m.cls) {
-#define SP_FWD_CASE(C)                                                     \
-  case C: {                                                                \
-    const int b0 = static_cast<int>((blk_in_table * kWarpsPerBlock + warp) * \
-                                    Cfg<C>::P);                            \
-    fwd_warp<C>(m, batch, b0, lane, off, idx, w, out, ldo);                \
-  } break;
+#define SP_FWD_CASE(C)                                                         \
+  case C:                                                                      \
+    fwd_tile_warp<FwdGeo<C>>(m, tile.b0, tile.nb, p0, warp, lane, s_off, s_idx, \
+                             idx, w, out, ldo);                                \
+    break;
     SP_FWD_CASE(0)
     SP_FWD_CASE(1)
     SP_FWD_CASE(2)
@@ -151,35 +212,31 @@ __global__ void __launch_bounds__(kBlockThreads)
     SP_FWD_CASE(5)
 #undef SP_FWD_CASE
     default:
-      fwd_warp_generic(m, batch,
-                       static_cast<int>(blk_in_table * kWarpsPerBlock + warp),
-                       lane, off, idx, w, out, ldo);
+      fwd_tile_warp_generic(m, tile.b0, tile.nb, p0, warp, lane, s_off, s_idx, idx,
+                            w, out, ldo);
   }
 }
 
 // ---------------------------------------------------------------------------
-// K4 step 1: keys. A block takes 256 bags of one table, stages their
-// offsets in shared memory and walks the positions coalesced.
+// K4 step 1 (only when K1 did not emit them): keys[p] = rowbase + idx[p],
+// bags[p] = bag of p. A block takes 256 bags of one table.
 
-constexpr int kKeyBags = 256;
-
-__global__ void __launch_bounds__(kKeyBags)
+__global__ void __launch_bounds__(kTileBags)
     build_keys_kernel(const TableMeta* __restrict__ meta, int batch,
                       int tiles_per_table, const int32_t* __restrict__ off,
                       const int32_t* __restrict__ idx,
                       uint32_t* __restrict__ keys, uint32_t* __restrict__ bags) {
-  __shared__ int32_t s_off[kKeyBags + 1];
+  __shared__ int32_t s_off[kTileBags + 1];
   const int t = blockIdx.x / tiles_per_table;
   const int tile = blockIdx.x % tiles_per_table;
-  const int b0 = tile * kKeyBags;
-  const int nb = min(kKeyBags, batch - b0);
+  const int b0 = tile * kTileBags;
+  const int nb = min(kTileBags, batch - b0);
   const TableMeta m = meta[t];
   const int64_t base = static_cast<int64_t>(m.local) * batch + b0;
   for (int i = threadIdx.x; i <= nb; i += blockDim.x) s_off[i] = off[base + i];
   __syncthreads();
   const int p0 = s_off[0], p1 = s_off[nb];
   for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-    // bag = last j with s_off[j] <= p (j < nb)
     int lo = 0, hi = nb - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -198,15 +255,33 @@ struct HeadFlag {
 };
 
 // ---------------------------------------------------------------------------
-// K4 step 4: SGD. Persistent warps walk units of kSegUnit consecutive
-// segments; a unit is processed in rounds of up to P segments of one table.
+// K4 step 3: SGD over the sorted (key, bag) pairs. A block owns the run
+// heads inside its tile of kTilePos sorted positions (a run that starts in
+// the tile is finished by the tile's block even past the tile end; a run
+// that started earlier belongs to the previous tile). Keys/bags/heads are
+// staged in shared memory; warps take contiguous slices of the tile's runs
+// and process them in rounds of up to P runs of the same table.
 
-constexpr int kSegUnit = 32;
+constexpr int kTilePos = 2048;
+constexpr int kPosPerThread = kTilePos / kBlockThreads;
+constexpr int kMaxSmemTables = 512;
 
-__device__ __forceinline__ int table_of_key(const uint32_t* __restrict__ rb_end,
-                                            int n_tables, uint32_t key) {
-  // first t with rowbase_end[t] > key
-  int lo = 0, hi = n_tables - 1;
+constexpr int kRunChunk = 16;  // runs claimed per warp at a time (>= max P)
+constexpr int kLongRun = 32;   // runs at least this long get the whole warp
+
+struct SgdShared {
+  uint32_t key[kTilePos];
+  uint32_t bag[kTilePos];
+  uint16_t head[kTilePos + 1];
+  uint32_t rb_end[kMaxSmemTables];
+  int nhead;
+  int last_end;  // end (tile-relative) of the last run
+  int next;      // next unclaimed run
+};
+
+__device__ __forceinline__ int table_of_key(const uint32_t* rb_end, int n_tables,
+                                            uint32_t key) {
+  int lo = 0, hi = n_tables - 1;  // first t with rb_end[t] > key
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
     if (rb_end[mid] > key) hi = mid; else lo = mid + 1;
@@ -214,86 +289,114 @@ __device__ __forceinline__ int table_of_key(const uint32_t* __restrict__ rb_end,
   return lo;
 }
 
-template <int CLS>
-__device__ __forceinline__ int sgd_round(
-    const TableMeta& m, uint32_t rb_end, int s, int uend, int nseg, int64_t n,
-    int lane, const uint32_t* __restrict__ keys,
-    const uint32_t* __restrict__ bags, const uint32_t* __restrict__ seg,
-    const float* __restrict__ grad, int64_t ldg, float lr,
-    float* __restrict__ w) {
-  constexpr int L = Cfg<CLS>::L, P = Cfg<CLS>::P, U = Cfg<CLS>::U;
-  constexpr int S = 32 / P, GB = S / L;
+__device__ __forceinline__ uint32_t pos_key(const SgdShared& sh, int i, int np,
+                                            int64_t p0,
+                                            const uint32_t* __restrict__ keys) {
+  return i < np ? sh.key[i] : __ldg(keys + p0 + i);
+}
+
+__device__ __forceinline__ uint32_t pos_bag(const SgdShared& sh, int i, int np,
+                                            int64_t p0,
+                                            const uint32_t* __restrict__ bags) {
+  return i < np ? sh.bag[i] : __ldg(bags + p0 + i);
+}
+
+// One round: runs [j, j+P) of the tile's head list that belong to table m.
+template <class G>
+__device__ __forceinline__ int sgd_round(const TableMeta& m, uint32_t rb_end,
+                                         int j, int jend, int np, int64_t p0,
+                                         int lane, const SgdShared& sh,
+                                         const uint32_t* __restrict__ bags,
+                                         const float* __restrict__ grad,
+                                         int64_t ldg, float lr,
+                                         float* __restrict__ w) {
+  constexpr int L = G::L, V = G::V, P = G::P, U = G::U, S = G::S, GB = G::GB;
   const int span = lane / S, ls = lane % S, g = ls / L, sub = ls % L;
-  const int u = s + span;
-  bool valid = u < uend;
+  const int u = j + span;
+  bool valid = u < jend;
   int beg = 0, end = 0;
   uint32_t key = 0;
   if (valid) {
-    beg = static_cast<int>(seg[u]);
-    end = u + 1 < nseg ? static_cast<int>(seg[u + 1]) : static_cast<int>(n);
-    key = keys[beg];
-    valid = key < rb_end;
+    beg = sh.head[u];
+    end = u + 1 < sh.nhead ? sh.head[u + 1] : sh.last_end;
+    key = sh.key[beg];
+    // same table; a long run (other than the first) gets its own round
+    valid = key < rb_end && (span == 0 || end - beg < kLongRun);
   }
-  // spans must be a contiguous prefix of valid segments
   const unsigned bal = __ballot_sync(0xffffffffu, valid && ls == 0);
+  // spans must be a contiguous prefix of valid runs
   int nvalid = 0;
 #pragma unroll
-  for (int j = 0; j < P; ++j) {
-    if (!(bal & (1u << (j * S)))) break;
+  for (int q = 0; q < P; ++q) {
+    if (!(bal & (1u << (q * S)))) break;
     ++nvalid;
   }
   const bool active = span < nvalid;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 acc[V], wold[V];
+#pragma unroll
+  for (int q = 0; q < V; ++q) {
+    acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    wold[q] = acc[q];
+  }
   float* wrow = nullptr;
-  float4 wold = make_float4(0.f, 0.f, 0.f, 0.f);
   if (active) {
     const int64_t row = static_cast<int64_t>(key - m.rowbase);
-    wrow = w + m.woff + row * m.dim + 4 * sub;
-    if (g == 0) wold = *reinterpret_cast<const float4*>(wrow);
-    const float* gcol = grad + m.lcol + 4 * sub;
+    wrow = w + m.woff + row * m.dim + 4 * V * sub;
+    if (g == 0)
+#pragma unroll
+      for (int q = 0; q < V; ++q) wold[q] = *reinterpret_cast<const float4*>(wrow + 4 * q);
+    const float* gcol = grad + m.lcol + 4 * V * sub;
     for (int k = beg + g; k < end; k += GB * U) {
       uint32_t bg[U];
 #pragma unroll
       for (int q = 0; q < U; ++q) {
         const int kk = k + q * GB;
-        bg[q] = kk < end ? __ldg(bags + kk) : 0xffffffffu;
+        bg[q] = kk < end ? pos_bag(sh, kk, np, p0, bags) : 0xffffffffu;
       }
-      float4 v[U];
+      float4 v[U][V];
 #pragma unroll
       for (int q = 0; q < U; ++q)
-        v[q] = bg[q] != 0xffffffffu
-                   ? ldg_f4(gcol + static_cast<int64_t>(bg[q]) * ldg)
-                   : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int q = 0; q < U; ++q) acc = f4_add(acc, v[q]);
+        for (int c = 0; c < V; ++c)
+          v[q][c] = bg[q] != 0xffffffffu
+                        ? ldg_f4(gcol + static_cast<int64_t>(bg[q]) * ldg + 4 * c)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int q = 0; q < U; ++q)
+#pragma unroll
+        for (int c = 0; c < V; ++c) acc[c] = f4_add(acc[c], v[q][c]);
     }
   }
 #pragma unroll
-  for (int o = L; o < S; o <<= 1) acc = f4_add(acc, shfl_xor_f4(acc, o));
+  for (int o = L; o < S; o <<= 1)
+#pragma unroll
+    for (int c = 0; c < V; ++c) acc[c] = f4_add(acc[c], shfl_xor_f4(acc[c], o));
   if (active && g == 0) {
-    float4 r;
-    r.x = fmaf(-lr, acc.x, wold.x);
-    r.y = fmaf(-lr, acc.y, wold.y);
-    r.z = fmaf(-lr, acc.z, wold.z);
-    r.w = fmaf(-lr, acc.w, wold.w);
-    *reinterpret_cast<float4*>(wrow) = r;
+#pragma unroll
+    for (int c = 0; c < V; ++c) {
+      float4 r;
+      r.x = fmaf(-lr, acc[c].x, wold[c].x);
+      r.y = fmaf(-lr, acc[c].y, wold[c].y);
+      r.z = fmaf(-lr, acc[c].z, wold[c].z);
+      r.w = fmaf(-lr, acc[c].w, wold[c].w);
+      *reinterpret_cast<float4*>(wrow + 4 * c) = r;
+    }
   }
   return nvalid;
 }
 
 __device__ __forceinline__ int sgd_round_generic(
-    const TableMeta& m, int s, int nseg, int64_t n, int lane,
-    const uint32_t* __restrict__ keys, const uint32_t* __restrict__ bags,
-    const uint32_t* __restrict__ seg, const float* __restrict__ grad,
-    int64_t ldg, float lr, float* __restrict__ w) {
-  const int beg = static_cast<int>(seg[s]);
-  const int end = s + 1 < nseg ? static_cast<int>(seg[s + 1]) : static_cast<int>(n);
-  const int64_t row = static_cast<int64_t>(keys[beg] - m.rowbase);
+    const TableMeta& m, int j, int np, int64_t p0, int lane, const SgdShared& sh,
+    const uint32_t* __restrict__ bags, const float* __restrict__ grad, int64_t ldg,
+    float lr, float* __restrict__ w) {
+  const int beg = sh.head[j];
+  const int end = j + 1 < sh.nhead ? sh.head[j + 1] : sh.last_end;
+  const int64_t row = static_cast<int64_t>(sh.key[beg] - m.rowbase);
   for (int c0 = 0; c0 < m.dim; c0 += 32) {
     const int c = c0 + lane;
     float acc = 0.f;
     for (int k = beg; k < end; ++k) {
-      const uint32_t bg = __ldg(bags + k);
+      const uint32_t bg = pos_bag(sh, k, np, p0, bags);
       if (c < m.dim) acc += __ldg(grad + static_cast<int64_t>(bg) * ldg + m.lcol + c);
     }
     if (c < m.dim) {
@@ -306,31 +409,93 @@ __device__ __forceinline__ int sgd_round_generic(
 
 __global__ void __launch_bounds__(kBlockThreads)
     sgd_kernel(const TableMeta* __restrict__ meta,
-               const uint32_t* __restrict__ rb_end, int n_tables,
+               const uint32_t* __restrict__ rb_end_g, int n_tables,
                const uint32_t* __restrict__ keys,
-               const uint32_t* __restrict__ bags,
-               const uint32_t* __restrict__ seg,
-               const int32_t* __restrict__ d_nseg, int64_t n,
+               const uint32_t* __restrict__ bags, int64_t n,
                const float* __restrict__ grad, int64_t ldg, float lr,
                float* __restrict__ w) {
-  const int nseg = *d_nseg;
-  const int units = (nseg + kSegUnit - 1) / kSegUnit;
-  const int lane = threadIdx.x & 31;
-  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int unit = gwarp; unit < units; unit += nwarps) {
-    int s = unit * kSegUnit;
-    const int uend = min(s + kSegUnit, nseg);
-    while (s < uend) {
-      const uint32_t key0 = keys[seg[s]];
-      const int t = table_of_key(rb_end, n_tables, key0);
+  __shared__ SgdShared sh;
+  using BlockScan = cub::BlockScan<int, kBlockThreads>;
+  __shared__ typename BlockScan::TempStorage scan_tmp;
+  const int64_t p0 = static_cast<int64_t>(blockIdx.x) * kTilePos;
+  const int np = n - p0 < kTilePos ? static_cast<int>(n - p0) : kTilePos;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < np; i += kBlockThreads) {
+    sh.key[i] = __ldg(keys + p0 + i);
+    sh.bag[i] = __ldg(bags + p0 + i);
+  }
+  const bool rb_in_smem = n_tables <= kMaxSmemTables;
+  if (rb_in_smem)
+    for (int i = tid; i < n_tables; i += kBlockThreads) sh.rb_end[i] = rb_end_g[i];
+  const uint32_t prev = p0 > 0 ? __ldg(keys + p0 - 1) : 0xffffffffu;
+  __syncthreads();
+  // run heads of the tile (tile-relative positions), in order
+  int flags[kPosPerThread];
+  int cnt = 0;
+#pragma unroll
+  for (int q = 0; q < kPosPerThread; ++q) {
+    const int i = tid * kPosPerThread + q;
+    const uint32_t before = i == 0 ? prev : sh.key[i - 1];
+    flags[q] = (i < np && (sh.key[i] != before || (p0 == 0 && i == 0))) ? 1 : 0;
+    cnt += flags[q];
+  }
+  int first = 0, total = 0;
+  BlockScan(scan_tmp).ExclusiveSum(cnt, first, total);
+#pragma unroll
+  for (int q = 0; q < kPosPerThread; ++q)
+    if (flags[q]) sh.head[first++] = static_cast<uint16_t>(tid * kPosPerThread + q);
+  if (tid == 0) {
+    sh.nhead = total;
+    sh.next = 0;
+  }
+  // end of the last run: it may continue past the tile
+  if (tid < 32) {
+    int end = np;
+    if (total > 0 && p0 + np < n) {
+      // all lanes: scan forward until the key changes
+      const uint32_t last_key = sh.key[np - 1];
+      for (int64_t base = p0 + np;; base += 32) {
+        const int64_t p = base + tid;
+        const bool diff = p >= n || __ldg(keys + p) != last_key;
+        const unsigned bal = __ballot_sync(0xffffffffu, diff);
+        if (bal) {
+          end = static_cast<int>(base - p0) + __ffs(bal) - 1;
+          break;
+        }
+      }
+    }
+    if (tid == 0) sh.last_end = end;
+  }
+  __syncthreads();
+  const int nh = sh.nhead;
+  if (nh == 0) return;
+  const int lane = tid & 31;
+  const uint32_t* rb = rb_in_smem ? sh.rb_end : rb_end_g;
+  // Warps claim chunks of kRunChunk runs dynamically (hot rows make run
+  // lengths very uneven). Inside a chunk: short runs go P at a time, a long
+  // run gets the whole warp (all row groups, U rows each in flight).
+  for (;;) {
+    int j0 = 0;
+    if (lane == 0) j0 = atomicAdd(&sh.next, kRunChunk);
+    j0 = __shfl_sync(0xffffffffu, j0, 0);
+    if (j0 >= nh) break;
+    const int jend = min(nh, j0 + kRunChunk);
+    int j = j0;
+    while (j < jend) {
+      const int beg = sh.head[j];
+      const int len = (j + 1 < nh ? sh.head[j + 1] : sh.last_end) - beg;
+      const uint32_t key0 = sh.key[beg];
+      const int t = table_of_key(rb, n_tables, key0);
       const TableMeta m = meta[t];
-      const uint32_t re = rb_end[t];
+      const uint32_t re = rb[t];
+      const bool lng = len >= kLongRun;
       switch (m.cls) {
-#define SP_SGD_CASE(C)                                                        \
-  case C:                                                                     \
-    s += sgd_round<C>(m, re, s, uend, nseg, n, lane, keys, bags, seg, grad,   \
-                      ldg, lr, w);                                            \
+#define SP_SGD_CASE(C)                                                           \
+  case C:                                                                        \
+    j += lng ? sgd_round<LongGeo<C>>(m, re, j, j + 1, np, p0, lane, sh, bags,    \
+                                     grad, ldg, lr, w)                           \
+             : sgd_round<SgdGeo<C>>(m, re, j, jend, np, p0, lane, sh, bags, grad, \
+                                    ldg, lr, w);                                 \
     break;
         SP_SGD_CASE(0)
         SP_SGD_CASE(1)
@@ -340,8 +505,7 @@ __global__ void __launch_bounds__(kBlockThreads)
         SP_SGD_CASE(5)
 #undef SP_SGD_CASE
         default:
-          s += sgd_round_generic(m, s, nseg, n, lane, keys, bags, seg, grad,
-                                 ldg, lr, w);
+          j += sgd_round_generic(m, j, np, p0, lane, sh, bags, grad, ldg, lr, w);
       }
     }
   }
@@ -441,13 +605,28 @@ int grid_for(int64_t n, int threads) {
 // ---------------------------------------------------------------------------
 // launchers
 
-void launch_tbe_forward(const TableMeta* d_meta, int n_tables, int64_t n_blocks,
-                        int batch, const int32_t* d_off, const int32_t* d_idx,
-                        const float* d_w, float* d_out, int64_t ldo,
+std::vector<int4> make_fwd_tiles(const std::vector<TableMeta>& canon,
+                                 const std::vector<int>& order, int batch) {
+  std::vector<int4> tiles;
+  for (int li : order)
+    for (int b0 = 0; b0 < batch; b0 += kTileBags)
+      tiles.push_back(make_int4(canon[li].local, b0, std::min(kTileBags, batch - b0), 0));
+  return tiles;
+}
+
+void launch_tbe_forward(const TableMeta* d_meta_canon, const int4* d_tiles,
+                        int64_t n_tiles, int batch, const int32_t* d_off,
+                        const int32_t* d_idx, const float* d_w, float* d_out,
+                        int64_t ldo, uint32_t* d_keys, uint32_t* d_bags,
                         cudaStream_t st) {
-  if (n_blocks <= 0) return;
-  tbe_forward_kernel<<<static_cast<unsigned>(n_blocks), kBlockThreads, 0, st>>>(
-      d_meta, n_tables, batch, d_off, d_idx, d_w, d_out, ldo);
+  if (n_tiles <= 0) return;
+  const FwdTile* tiles = reinterpret_cast<const FwdTile*>(d_tiles);
+  if (d_keys)
+    tbe_forward_kernel<true><<<static_cast<unsigned>(n_tiles), kBlockThreads, 0, st>>>(
+        d_meta_canon, tiles, batch, d_off, d_idx, d_w, d_out, ldo, d_keys, d_bags);
+  else
+    tbe_forward_kernel<false><<<static_cast<unsigned>(n_tiles), kBlockThreads, 0, st>>>(
+        d_meta_canon, tiles, batch, d_off, d_idx, d_w, d_out, ldo, nullptr, nullptr);
   SP_LAUNCHED();
 }
 
@@ -455,14 +634,14 @@ void launch_build_keys(const TableMeta* d_meta_canon, int n_tables, int batch,
                        const int32_t* d_off, const int32_t* d_idx,
                        uint32_t* d_keys, uint32_t* d_bags, cudaStream_t st) {
   if (n_tables <= 0) return;
-  const int tiles = (batch + kKeyBags - 1) / kKeyBags;
-  build_keys_kernel<<<n_tables * tiles, kKeyBags, 0, st>>>(
+  const int tiles = (batch + kTileBags - 1) / kTileBags;
+  build_keys_kernel<<<n_tables * tiles, kTileBags, 0, st>>>(
       d_meta_canon, batch, tiles, d_off, d_idx, d_keys, d_bags);
   SP_LAUNCHED();
 }
 
-size_t sort_pairs(void* temp, size_t temp_bytes, uint32_t* keys_in,
-                  uint32_t* keys_out, uint32_t* vals_in, uint32_t* vals_out,
+size_t sort_pairs(void* temp, size_t temp_bytes, const uint32_t* keys_in,
+                  uint32_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
                   int64_t n, int end_bit, cudaStream_t st) {
   size_t bytes = temp_bytes;
   SP_CUDA(cub::DeviceRadixSort::SortPairs(temp, bytes, keys_in, keys_out,
@@ -487,23 +666,14 @@ size_t exclusive_scan_i32(void* temp, size_t temp_bytes, const int32_t* in,
   return bytes;
 }
 
-int sgd_grid(int device) {
-  int sms = 148, per_sm = 1;
-  SP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sgd_kernel,
-                                                        kBlockThreads, 0));
-  return sms * (per_sm > 0 ? per_sm : 1);
-}
-
 void launch_sgd(const TableMeta* d_meta_canon, const uint32_t* d_rowbase_end,
                 int n_tables, const uint32_t* d_keys, const uint32_t* d_bags,
-                const uint32_t* d_seg, const int32_t* d_nseg, int64_t n,
-                const float* d_grad, int64_t ldg, float lr, float* d_w,
-                int grid, cudaStream_t st) {
+                int64_t n, const float* d_grad, int64_t ldg, float lr, float* d_w,
+                cudaStream_t st) {
   if (n <= 0 || n_tables <= 0) return;
-  sgd_kernel<<<grid, kBlockThreads, 0, st>>>(d_meta_canon, d_rowbase_end,
-                                             n_tables, d_keys, d_bags, d_seg,
-                                             d_nseg, n, d_grad, ldg, lr, d_w);
+  const int64_t blocks = (n + kTilePos - 1) / kTilePos;
+  sgd_kernel<<<static_cast<unsigned>(blocks), kBlockThreads, 0, st>>>(
+      d_meta_canon, d_rowbase_end, n_tables, d_keys, d_bags, n, d_grad, ldg, lr, d_w);
   SP_LAUNCHED();
 }
 

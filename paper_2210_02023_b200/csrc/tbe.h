@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 namespace sp {
 
@@ -12,7 +13,7 @@ namespace sp {
 struct TableMeta {
   int64_t woff;         // float offset of row 0 in the weight slab
   int64_t rows;         // hash_size
-  int64_t block_start;  // K1: first block of this table in the grid
+  int64_t reserved;
   int32_t dim;
   int32_t lcol;         // first column in the local pooled [B, W_local]
   uint32_t rowbase;     // K4 key base: sum of rows of earlier local tables
@@ -53,34 +54,38 @@ constexpr int kWarpsPerBlock = 8;
 constexpr int kBlockThreads = 32 * kWarpsPerBlock;
 
 // ---- K1: fused multi-table sum-pooled forward ----------------------------
-// One launch over all local tables: out[b, lcol_t : lcol_t + dim_t] =
-// sum_{p in [off[i*B+b], off[i*B+b+1])} W_t[idx[p], :]  (int32 CSR).
-void launch_tbe_forward(const TableMeta* d_meta, int n_tables,
-                        int64_t n_blocks, int batch, const int32_t* d_off,
+// One launch over all local tables; a block per tile of <= 256 bags of one
+// table: out[b, lcol_t : lcol_t + dim_t] =
+//   sum_{p in [off[i*B+b], off[i*B+b+1])} W_t[idx[p], :]   (int32 CSR).
+// With d_keys != nullptr also writes the backward's sort pairs
+// keys[p] = rowbase_i + idx[p], bags[p] = b.
+// Tiles (x = canonical table, y = first bag, z = bag count) in launch order.
+std::vector<int4> make_fwd_tiles(const std::vector<TableMeta>& canon,
+                                 const std::vector<int>& order, int batch);
+void launch_tbe_forward(const TableMeta* d_meta_canon, const int4* d_tiles,
+                        int64_t n_tiles, int batch, const int32_t* d_off,
                         const int32_t* d_idx, const float* d_w, float* d_out,
-                        int64_t ldo, cudaStream_t st);
+                        int64_t ldo, uint32_t* d_keys, uint32_t* d_bags,
+                        cudaStream_t st);
 
-// ---- K4: backward = keys -> stable radix sort -> segments -> SGD ---------
-// keys[p] = rowbase_i + idx[p], bags[p] = b for every position of the CSR.
+// ---- K4: backward = keys -> stable radix sort -> runs -> SGD -------------
 void launch_build_keys(const TableMeta* d_meta_canon, int n_tables, int batch,
                        const int32_t* d_off, const int32_t* d_idx,
                        uint32_t* d_keys, uint32_t* d_bags, cudaStream_t st);
-// Segment heads of sorted keys: seg[u] = first position of the u-th run,
-// *d_nseg = number of runs. temp: CUB scratch (query with temp == nullptr).
+// Run heads of sorted keys (test/diagnostic path; the SGD kernel finds the
+// heads itself): seg[u] = first position of the u-th run, *d_nseg = runs.
 size_t select_heads(void* temp, size_t temp_bytes, const uint32_t* d_keys,
                     int64_t n, uint32_t* d_seg, int32_t* d_nseg,
                     cudaStream_t st);
-size_t sort_pairs(void* temp, size_t temp_bytes, uint32_t* keys_in,
-                  uint32_t* keys_out, uint32_t* vals_in, uint32_t* vals_out,
+size_t sort_pairs(void* temp, size_t temp_bytes, const uint32_t* keys_in,
+                  uint32_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
                   int64_t n, int end_bit, cudaStream_t st);
-// Row-wise SGD over the segments (persistent grid):
-// W[row] -= lr * sum_{k in segment, sorted order} grad[bags[k], lcol..].
+// Row-wise SGD over the sorted pairs:
+// W[row] -= lr * sum_{k in run, sorted order} grad[bags[k], lcol..].
 void launch_sgd(const TableMeta* d_meta_canon, const uint32_t* d_rowbase_end,
                 int n_tables, const uint32_t* d_keys, const uint32_t* d_bags,
-                const uint32_t* d_seg, const int32_t* d_nseg, int64_t n,
-                const float* d_grad, int64_t ldg, float lr, float* d_w,
-                int grid, cudaStream_t st);
-int sgd_grid(int device);
+                int64_t n, const float* d_grad, int64_t ldg, float lr, float* d_w,
+                cudaStream_t st);
 
 // ---- generator / layout helpers ------------------------------------------
 void launch_init_weights(float* d_w, int64_t rows, int dim, int32_t gid,
