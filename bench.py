@@ -1,0 +1,425 @@
+#!/usr/bin/env python
+"""bench.py — the measured embedding iteration DreamShard costs, on B200.
+
+Metric (BASELINE.json): max-over-GPU embedding fwd + fwd a2a + bwd a2a + bwd
+ms/iter, composed like CostOracle::evaluate_placement (oracle.hpp:222-227),
+plus the lookup kernel's HBM GB/s against the measured peak.
+
+Workload (config.workload): BASELINE cfg3 — the 100 synthetic DLRM tables of
+paper_2210_02023_b200/data/pools.json (synth_pool, seed 2210, dims 16-128,
+rows 1e5-1e6), batch 65536, split over D = N GPUs by the DreamShard placement
+(greedy rollout of the committed checkpoint on our GPU evaluator). One step =
+K1 forward -> fwd all-to-all -> bwd all-to-all -> K4 sort + row-wise SGD over
+one synthetic batch. Inputs (tables 9.2 GiB, CSR 0.2 GB) exceed L2.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "max-over-GPU embedding fwd+bwd+a2a ms/iter; lookup HBM GB/s vs peak"
+UNIT = "ms/iter"
+DATA = os.path.join(ROOT, "paper_2210_02023_b200", "data")
+CKPT = os.path.join(DATA, "dreamshard_m100_d8.dshd")
+SEED = 2210
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def load_task(config: str, D: int):
+    from paper_2210_02023_b200.api import PlacementTask, TableDesc
+    with open(os.path.join(DATA, "pools.json")) as f:
+        pool = json.load(f)[config]
+    tables = [TableDesc.from_dict(t) for t in pool["tables"]]
+    return PlacementTask(tables, D, float(pool["mem_cap_gb"]), int(pool["batch_size"]))
+
+
+def make_placement(task, how: str, device: int):
+    from paper_2210_02023_b200 import api
+    if task.num_devices == 1:
+        return np.zeros(len(task.tables), dtype=np.int32)
+    if how == "dreamshard":
+        ckpt = api.load_checkpoint(CKPT)
+        placement, _ = api.infer(ckpt, task, device=device)
+        return placement
+    return api.expert_placement(task, how)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax = float(parts[2])
+                except ValueError:
+                    continue
+                for n, v in zip(names, parts[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+        os.unlink(self.path)
+        # samples under load: drop the idle edges
+        busy = [x for x in sm if smax and x > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def allreduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle port; the only place bench.py touches oracle/)
+
+def cpu_sample(task, sample_bags: int, threads: int, steps: int = 1, warmup: int = 0):
+    """The oracle port (oracle/lookup_oracle.cpp, OpenMP) on bags [0, Bs) of
+    every table: fwd sum-pooling + per-table stable sort/segment/SGD. Returns
+    per-step ms extrapolated to the full batch, and the sample description."""
+    from oracle import lookup as orc
+    tables = [t.to_dict() for t in task.tables]
+    Bs = sample_bags
+    off, idx = orc.synth_batch(tables, Bs, SEED, nthreads=threads)
+    dims = [t.dim for t in task.tables]
+    rows = [t.hash_size for t in task.tables]
+    weights = [np.full((t.hash_size, t.dim), 0.75, dtype=np.float32) for t in task.tables]
+    W = sum(dims)
+    grad = np.random.default_rng(0).uniform(-1, 1, size=(Bs, W)).astype(np.float32)
+    lst = list(range(len(tables)))
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        orc.tbe_forward(dims, rows, weights, off, idx, Bs, nthreads=threads)
+        orc.tbe_backward_sgd_inplace(dims, rows, weights, off, idx, Bs, grad, 0.01, lst,
+                                     nthreads=threads)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt * 1e3 * (task.batch_size / Bs))
+    sample = (f"oracle port (fp64-accumulate fwd + stable-sort SGD) on bags [0,{Bs}) of all "
+              f"{len(tables)} tables ({len(idx)} lookups), x{task.batch_size // Bs} to the "
+              f"full batch; D=1 layout (no exchange)")
+    return times, sample
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference path on the host cores (the reference
+    has no lookup code, so this is the oracle port, kind "port")."""
+    if rank != 0:
+        return
+    task = load_task(args.config, max(args.gpus, 1))
+    threads = os.cpu_count() or 1
+    times, sample = cpu_sample(task, args.cpu_sample_bags, threads, steps=args.steps,
+                               warmup=args.warmup)
+    v = statistics.median(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(v, 3), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_dict(args, task),
+        "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args, task):
+    return {"workload": f"{args.config}: {len(task.tables)} synthetic DLRM tables (dims 16-128, "
+                        f"rows 1e5-1e6, pools.json seed 2210), batch {task.batch_size}, "
+                        f"D={task.num_devices} devices, {args.placement} placement",
+            "tables": len(task.tables), "batch": task.batch_size,
+            "devices": task.num_devices, "placement": args.placement,
+            "l2": "inputs larger than L2 (tables 9.2 GiB fp32, CSR 0.2 GB, no flush)",
+            "parallelism": f"table-wise model parallel x{task.num_devices}"}
+
+
+# ---------------------------------------------------------------------------
+
+def run_ours(args, world, rank, local):
+    import torch
+    from paper_2210_02023_b200 import api
+
+    D = world
+    task = load_task(args.config, D)
+    placement = make_placement(task, args.placement, local)
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        obj = [api.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    shard = api.EmbeddingShard(task, placement, lr=0.01, rank=rank, world_size=world,
+                               nccl_id=nccl_id, device=local)
+    shard.init_tables(SEED)
+    shard.synth_batch(SEED)
+    shard.synth_grad(SEED)
+    stream = torch.cuda.ExternalStream(shard.stream, device=local)
+    kernels_per_iter = shard.graph_replay(0)
+
+    # warm-up
+    for _ in range(args.warmup):
+        shard.enqueue_iteration()
+    torch.cuda.synchronize()
+    barrier(world)
+
+    # timed region: K eager iterations, per-kernel events on
+    shard.set_profiling(True)
+    shard.kernel_ms()  # reset
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    launches0 = api.lib().sp_kernel_launches()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier(world)
+        e0.record(stream)
+        for _ in range(args.steps):
+            shard.enqueue_iteration()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    own_launches = api.lib().sp_kernel_launches() - launches0
+    kms = shard.kernel_ms()
+    shard.set_profiling(False)
+    ms_local = e0.elapsed_time(e1) / args.steps
+    ms = allreduce_max(ms_local, world)
+
+    # stage breakdown (oracle.hpp:222-227 composition), median of 5
+    bds = [shard.run_iteration() for _ in range(5)]
+    bd = sorted(bds, key=lambda b: b.overall_ms)[2]
+
+    # roofline of the dominant kernel (algorithmic bytes per launch / time)
+    ab = shard.algorithmic_bytes()
+    nnz = shard.nnz
+    T_local = len(shard.local_tables())
+    peak, peak_kind = load_peaks()
+    per_launch = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in kms.items()}
+    alg = {
+        # K1 also writes the backward's sort pairs (8 B per lookup)
+        "fwd": ab["fwd"] + (8.0 * nnz if os.environ.get("SP_FUSE_KEYS", "1") != "0" else 0.0),
+        # K4 SGD: grad 4*B*W + W row read/write 8*sum_unique dim + sorted pairs 8*nnz
+        "sgd": ab["bwd"] - 4.0 * (T_local * task.batch_size + 1) - 4.0 * nnz + 8.0 * nnz,
+        "sort": ab["sort"],
+    }
+    kernels = {}
+    for k in ("fwd", "sort", "sgd"):
+        t = per_launch.get(k, 0.0)
+        kernels[k] = {"ms": round(t, 4),
+                      "share": round(kms[k][0] / max(1e-9, sum(v[0] for v in kms.values())), 3),
+                      "alg_bytes": alg[k],
+                      "alg_gbs": round(alg[k] / (t * 1e6), 1) if t > 0 else None}
+    dominant = max(("fwd", "sgd"), key=lambda k: kms[k][0])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(f"{args.config}/D{D}/{dominant}")
+    ach = alg[dominant] / (per_launch[dominant] * 1e6)
+    roofline = {"bound": "hbm", "kernel": dominant, "achieved": round(ach, 1),
+                "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 3),
+                "traffic": traffic, "peak_kind": peak_kind,
+                "lookup_fwd": {"achieved": kernels["fwd"]["alg_gbs"],
+                               "frac": round(kernels["fwd"]["alg_gbs"] / peak, 3)
+                               if kernels["fwd"]["alg_gbs"] else None}}
+
+    # e2e through the public API with host buffers: H2D LookupBatch (pinned
+    # int64, the reference layout) -> measured iteration -> breakdown to host
+    batch, keep = api.synth_lookup_batch(task.tables, task.batch_size, SEED, device=local,
+                                         pinned=True)
+    h2d = batch.offsets.nbytes + batch.indices.nbytes
+    # this rank's tables only are copied by sp_upload_batch
+    local_ids = shard.local_tables()
+    h2d_local = sum(8 * (task.batch_size + 1) +
+                    8 * int(batch.offsets[(t + 1) * task.batch_size] -
+                            batch.offsets[t * task.batch_size]) for t in local_ids)
+    d2h = 8 * 3 * D + 24
+    e2e_steps = max(3, min(args.steps, 20))
+    for _ in range(2):
+        shard.upload_batch(batch)
+        shard.run_iteration()
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        shard.upload_batch(batch)
+        shard.run_iteration()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    e2e_ms = allreduce_max(e2e_ms, world)
+    del keep
+
+    # CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        times, sample = cpu_sample(task, args.cpu_sample_bags, threads, steps=1, warmup=0)
+        cpu = {"value": round(times[0], 3), "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": sample}
+
+    # D=8 DreamShard placement emulated on this GPU (N = 1 only)
+    emulated = None
+    if world == 1 and not args.no_emulation:
+        etask = load_task(args.config, 8)
+        ep = make_placement(etask, args.placement, local)
+        esh = api.EmbeddingShard(etask, ep, lr=0.01, device=local)
+        esh.init_tables(SEED)
+        esh.synth_batch(SEED)
+        esh.synth_grad(SEED)
+        runs = [esh.run_iteration() for _ in range(6)][1:]
+        eb = sorted(runs, key=lambda b: b.overall_ms)[2]
+        emulated = {
+            "devices": 8, "placement": args.placement,
+            "fwd_ms": [round(x, 4) for x in eb.fwd_ms], "bwd_ms": [round(x, 4) for x in eb.bwd_ms],
+            "max_fwd_ms": round(max(eb.fwd_ms), 4), "max_bwd_ms": round(max(eb.bwd_ms), 4),
+            "compute_only_ms": round(max(eb.fwd_ms) + max(eb.bwd_ms), 4),
+            "exchange_note": "exchange stages measured as device-local copies on one GPU "
+                             "(not NVLink); compute stages are the real per-device kernels",
+            "overall_ms_with_local_exchange": round(eb.overall_ms, 4),
+        }
+        esh.close()
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(ms, 4), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (SURVEY §8d generator, seed 2210)",
+            "config": config_dict(args, task),
+            "breakdown": {"fwd_ms": [round(x, 4) for x in bd.fwd_ms],
+                          "bwd_ms": [round(x, 4) for x in bd.bwd_ms],
+                          "fwd_comm_stage_ms": round(bd.fwd_comm_stage_ms, 4),
+                          "bwd_comm_stage_ms": round(bd.bwd_comm_stage_ms, 4),
+                          "overall_ms": round(bd.overall_ms, 4)},
+            "kernels": kernels,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_ms, 3), "unit": UNIT, "h2d_bytes_per_step": h2d_local,
+                    "d2h_bytes_per_step": d2h,
+                    "path": "EmbeddingShard.upload_batch(pinned int64 LookupBatch) + "
+                            "run_iteration() -> CostBreakdown"},
+            "gpu_launches": int(kernels_per_iter * args.steps),
+            "gpu_launches_detail": {"per_iter_graph_kernel_nodes": kernels_per_iter,
+                                    "own_launch_sites_counted": int(own_launches),
+                                    "note": "per-iteration kernel nodes of the captured "
+                                            "iteration (K1, CUB radix-sort kernels compiled "
+                                            "into our library, K4 SGD)"},
+            "clocks": clk.summary(),
+            "emulated_d8": emulated,
+        }
+        print(json.dumps(line), flush=True)
+    shard.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--placement", default="dreamshard",
+                    choices=["dreamshard", "size", "dim", "lookup", "size-lookup"])
+    ap.add_argument("--cpu-sample-bags", type=int, default=2048)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-emulation", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

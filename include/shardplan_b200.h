@@ -149,6 +149,12 @@ int sp_upload_batch(sp_ctx* ctx, const int64_t* offsets, int64_t offsets_len,
                     const int64_t* indices, int64_t indices_len);
 /* Same batch, generated on the device by the SURVEY §8d generator. */
 int sp_synth_batch(sp_ctx* ctx, uint64_t seed);
+/* The same generator for a whole host LookupBatch of `tables` (run on the
+ * GPU, copied back as int64): offsets[T*B+1]; indices may be NULL to only
+ * get offsets and *nnz. Used to build host inputs for the e2e path. */
+int sp_synth_lookup_batch(const sp_table_spec* tables, int32_t num_tables,
+                          int32_t batch_size, uint64_t seed, int32_t cuda_device,
+                          int64_t* offsets, int64_t* indices, int64_t* nnz);
 /* Number of local lookup indices of the current batch. */
 int sp_batch_nnz(sp_ctx* ctx, int64_t* nnz);
 
@@ -190,6 +196,13 @@ int sp_enqueue_iteration(sp_ctx* ctx);
 /* Capture sp_enqueue_iteration into a CUDA graph and replay it `iters`
  * times; 0 iters only builds the graph. Reports kernel nodes per graph. */
 int sp_graph_replay(sp_ctx* ctx, int32_t iters, int32_t* kernels_per_iter);
+
+/* Per-kernel CUDA-event timing of the hot-path launches enqueued while
+ * enabled (on the context stream): sp_ctx_kernel_ms returns the summed ms
+ * and launch counts of [0]=K1 forward, [1]=key build, [2]=radix sort,
+ * [3]=K4 SGD, [4]=exchange, and resets the accumulators (synchronizes). */
+int sp_ctx_set_profiling(sp_ctx* ctx, int32_t on);
+int sp_ctx_kernel_ms(sp_ctx* ctx, double ms[5], int64_t counts[5]);
 
 /* Algorithmic bytes of one launch of each stage on this rank:
  * [0]=fwd (K1) [1]=a2a send per direction [2]=bwd floor (K4, sort

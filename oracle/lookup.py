@@ -161,6 +161,25 @@ def tbe_backward_sgd(dims, rows, weights_list, offsets, indices, B, grad, lr, ta
     return ws
 
 
+def tbe_backward_sgd_inplace(dims, rows, weights_list, offsets, indices, B, grad, lr,
+                             tables_list, nthreads=0):
+    """Row-wise SGD applied in place to weights_list (fp32 C-contiguous)."""
+    dims = np.ascontiguousarray(dims, dtype=np.int32)
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    T = len(dims)
+    gcol = np.zeros(T, dtype=np.int64)
+    gcol[1:] = np.cumsum(dims)[:-1]
+    W = int(dims.sum())
+    wp = (ctypes.c_void_p * T)(*[a.ctypes.data if a is not None else None
+                                 for a in weights_list])
+    g = np.ascontiguousarray(grad, dtype=np.float32).reshape(B, W)
+    lst = np.ascontiguousarray(tables_list, dtype=np.int32)
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    indices = np.ascontiguousarray(indices, dtype=np.int64)
+    lib().or_tbe_backward_sgd(B, _p(dims), _p(rows), wp, _p(offsets), _p(indices), _p(lst),
+                              len(lst), _p(g), W, _p(gcol), lr, nthreads)
+
+
 def grad_matrix(seed: int, B: int, W: int) -> np.ndarray:
     f = lib().or_grad
     out = np.empty((B, W), dtype=np.float32)

@@ -215,33 +215,32 @@ void or_tbe_backward_sgd(int32_t B, const int32_t* dims, const int64_t* rows,
                          const int64_t* indices, const int32_t* list,
                          int32_t n_list, const float* grad, int64_t ld,
                          const int64_t* grad_col, float lr, int32_t nthreads) {
-  (void)nthreads;
-  const int64_t n =
-      or_sorted_keys(B, rows, offsets, indices, list, n_list, nullptr, nullptr);
-  std::vector<uint32_t> keys(n), bags(n), uniq(n + 1), seg(n + 1);
-  or_sorted_keys(B, rows, offsets, indices, list, n_list, keys.data(),
-                 bags.data());
-  const int64_t nu = or_segments(keys.data(), n, uniq.data(), seg.data());
-  // local row base per list entry
-  std::vector<uint64_t> base(n_list + 1, 0);
-  for (int32_t i = 0; i < n_list; ++i) base[i + 1] = base[i] + rows[list[i]];
-  std::vector<double> s;
-  for (int64_t u = 0; u < nu; ++u) {
-    const uint64_t key = uniq[u];
-    const int32_t i = static_cast<int32_t>(
-        std::upper_bound(base.begin(), base.end(), key) - base.begin() - 1);
+  // Keys of different tables never interleave (key = row base + row), so
+  // the device-wide stable sort is the concatenation of per-table stable
+  // sorts: tables are processed independently (in parallel).
+  const int nt = nthreads_or_default(nthreads);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nt)
+  for (int32_t i = 0; i < n_list; ++i) {
+    const int32_t one[1] = {list[i]};
     const int32_t t = list[i];
-    const int64_t row = static_cast<int64_t>(key - base[i]);
+    const int64_t n = or_sorted_keys(B, rows, offsets, indices, one, 1, nullptr, nullptr);
+    std::vector<uint32_t> keys(n), bags(n), uniq(n + 1), seg(n + 1);
+    or_sorted_keys(B, rows, offsets, indices, one, 1, keys.data(), bags.data());
+    const int64_t nu = or_segments(keys.data(), n, uniq.data(), seg.data());
     const int dim = dims[t];
-    s.assign(dim, 0.0);
-    for (uint32_t k = seg[u]; k < seg[u + 1]; ++k) {
-      const float* g = grad + static_cast<int64_t>(bags[k]) * ld + grad_col[t];
-      for (int c = 0; c < dim; ++c) s[c] += g[c];
+    std::vector<double> s;
+    for (int64_t u = 0; u < nu; ++u) {
+      const int64_t row = static_cast<int64_t>(uniq[u]);
+      s.assign(dim, 0.0);
+      for (uint32_t k = seg[u]; k < seg[u + 1]; ++k) {
+        const float* g = grad + static_cast<int64_t>(bags[k]) * ld + grad_col[t];
+        for (int c = 0; c < dim; ++c) s[c] += g[c];
+      }
+      float* w = weights[t] + row * dim;
+      for (int c = 0; c < dim; ++c)
+        w[c] = static_cast<float>(static_cast<double>(w[c]) -
+                                  static_cast<double>(lr) * s[c]);
     }
-    float* w = weights[t] + row * dim;
-    for (int c = 0; c < dim; ++c)
-      w[c] = static_cast<float>(static_cast<double>(w[c]) -
-                                static_cast<double>(lr) * s[c]);
   }
 }
 

@@ -37,6 +37,7 @@ SIGNATURES = {
     "sp_upload_batch": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_i64]),
     "sp_synth_batch": (c_i32, [c_vp, c_u64]),
     "sp_batch_nnz": (c_i32, [c_vp, P(c_i64)]),
+    "sp_synth_lookup_batch": (c_i32, [c_vp, c_i32, c_i32, c_u64, c_i32, c_vp, c_vp, P(c_i64)]),
     "sp_forward": (c_i32, [c_vp]),
     "sp_a2a_forward": (c_i32, [c_vp]),
     "sp_a2a_backward": (c_i32, [c_vp]),
@@ -50,6 +51,8 @@ SIGNATURES = {
     "sp_enqueue_iteration": (c_i32, [c_vp]),
     "sp_graph_replay": (c_i32, [c_vp, c_i32, P(c_i32)]),
     "sp_ctx_algorithmic_bytes": (c_i32, [c_vp, P(c_f64)]),
+    "sp_ctx_set_profiling": (c_i32, [c_vp, c_i32]),
+    "sp_ctx_kernel_ms": (c_i32, [c_vp, P(c_f64), P(c_i64)]),
     "sp_host_alloc": (c_i32, [c_u64, P(c_vp)]),
     "sp_host_free": (None, [c_vp]),
     "sp_ingest_lookup_batch": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp,

@@ -40,7 +40,8 @@ __all__ = [
     "CostBreakdown", "TraceEvent", "EmbeddingShard", "CostProvider",
     "MeasuredCostProvider", "ingest_lookup_batch", "compute_feature_stats", "Checkpoint",
     "load_checkpoint", "Evaluator", "infer", "ShardplanError", "nccl_unique_id",
-    "hot_mass", "HostBuffer",
+    "hot_mass", "HostBuffer", "EXPERT_STRATEGIES", "expert_cost", "greedy_placement",
+    "expert_placement",
 ]
 
 
@@ -406,6 +407,19 @@ class EmbeddingShard:
         check(lib().sp_graph_replay(self._h, iters, ctypes.byref(k)))
         return k.value
 
+    def set_profiling(self, on: bool):
+        check(lib().sp_ctx_set_profiling(self._h, 1 if on else 0))
+
+    KERNELS = ("fwd", "keys", "sort", "sgd", "exchange")
+
+    def kernel_ms(self) -> dict:
+        """Summed CUDA-event ms and launch counts per hot kernel since the
+        last call (profiling must be on)."""
+        ms = (ctypes.c_double * 5)()
+        n = (ctypes.c_int64 * 5)()
+        check(lib().sp_ctx_kernel_ms(self._h, ms, n))
+        return {k: (ms[i], n[i]) for i, k in enumerate(self.KERNELS)}
+
     def algorithmic_bytes(self) -> dict:
         out = (ctypes.c_double * 4)()
         check(lib().sp_ctx_algorithmic_bytes(self._h, out))
@@ -641,3 +655,79 @@ def infer(ckpt: Checkpoint, task: PlacementTask, device: int = 0):
     if st[0] != 0:
         raise ShardplanError(int(st[0]), "no device can hold the next table")
     return pl[0], max(0.0, float(pred[0]))
+
+
+# ---------------------------------------------------------------------------
+# baselines.hpp: greedy expert placements (host, microseconds)
+
+EXPERT_STRATEGIES = ("size", "dim", "lookup", "size-lookup")
+
+
+def expert_cost(strategy: str, t: TableDesc) -> float:
+    """baselines.hpp:81-110."""
+    if strategy == "size":
+        return t.table_size_gb
+    if strategy == "dim":
+        return float(t.dim)
+    if strategy == "lookup":
+        return t.dim * t.pooling_factor
+    if strategy == "size-lookup":
+        return t.dim * t.pooling_factor * t.table_size_gb
+    raise ShardplanError(10, f"unknown expert strategy: {strategy}")
+
+
+def greedy_placement(task: PlacementTask, cost_fn) -> np.ndarray:
+    """baselines.hpp:47-79: LPT greedy; sort ties to the lower id, device
+    ties to the lower index; infeasible when a table fits nowhere."""
+    D = task.num_devices
+    cost = [cost_fn(t) for t in task.tables]
+    order = sorted(range(len(cost)), key=lambda i: (-cost[i], i))
+    load = [0.0] * D
+    mem = [0.0] * D
+    p = np.zeros(len(cost), dtype=np.int32)
+    for i in order:
+        need = task.tables[i].table_size_gb
+        best = -1
+        for d in range(D):
+            if mem[d] + need > task.mem_cap_gb:
+                continue
+            if best < 0 or load[d] < load[best]:
+                best = d
+        if best < 0:
+            raise ShardplanError(1, f"table {i} does not fit on any device")
+        p[i] = best
+        load[best] += cost[i]
+        mem[best] += need
+    return p
+
+
+def expert_placement(task: PlacementTask, strategy: str) -> np.ndarray:
+    return greedy_placement(task, lambda t: expert_cost(strategy, t))
+
+
+def synth_lookup_batch(tables: Sequence[TableDesc], batch_size: int, seed: int,
+                       device: int = 0, pinned: bool = False):
+    """Host LookupBatch from the SURVEY §8d generator (run on the GPU).
+
+    With pinned=True the arrays live in page-locked HostBuffers (returned
+    as the third element to keep them alive)."""
+    specs = _specs(tables)
+    T = len(tables)
+    nnz = ctypes.c_int64()
+    if pinned:
+        ob = HostBuffer(T * batch_size + 1, np.int64)
+        off = ob.array
+    else:
+        ob = None
+        off = np.zeros(T * batch_size + 1, dtype=np.int64)
+    check(lib().sp_synth_lookup_batch(specs, T, batch_size, seed, device, _ptr(off), None,
+                                      ctypes.byref(nnz)))
+    if pinned:
+        ib = HostBuffer(nnz.value, np.int64)
+        idx = ib.array
+    else:
+        ib = None
+        idx = np.zeros(nnz.value, dtype=np.int64)
+    check(lib().sp_synth_lookup_batch(specs, T, batch_size, seed, device, _ptr(off), _ptr(idx),
+                                      ctypes.byref(nnz)))
+    return LookupBatch(idx, off, T, batch_size), (ob, ib)

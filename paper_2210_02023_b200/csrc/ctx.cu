@@ -106,6 +106,11 @@ struct sp_ctx {
   cudaEvent_t ev_a2a[4] = {};
   cudaGraphExec_t graph_exec = nullptr;
   int graph_kernels = 0;
+  bool profiling = false;            // per-kernel events (sp_ctx_set_profiling)
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  struct Mark { int cls; size_t a, b; };
+  std::vector<Mark> marks;
   std::vector<void*> owned;
   std::vector<void*> sort_owned;
   uint64_t dev_bytes = 0;
@@ -120,6 +125,7 @@ struct sp_ctx {
         if (e) cudaEventDestroy(e);
     for (auto& e : ev_a2a)
       if (e) cudaEventDestroy(e);
+    for (auto& e : ev_pool) cudaEventDestroy(e);
     for (auto& v : vdevs)
       for (void* p : {static_cast<void*>(v.d_idx), static_cast<void*>(v.d_keys),
                        static_cast<void*>(v.d_bags)})
@@ -174,10 +180,38 @@ void require_batch(sp_ctx* c) {
   if (!c->has_batch) raise(SP_ERR_BAD_INPUT, "no lookup batch uploaded");
 }
 
+// ---- per-kernel profiling ---------------------------------------------------
+
+enum { kProfFwd = 0, kProfKeys = 1, kProfSort = 2, kProfSgd = 3, kProfExchange = 4 };
+
+size_t prof_event(sp_ctx* c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    SP_CUDA(cudaEventCreate(&e));
+    c->ev_pool.push_back(e);
+  }
+  SP_CUDA(cudaEventRecord(c->ev_pool[c->ev_used], c->stream));
+  return c->ev_used++;
+}
+
+// Records events around a stage launch when profiling is on.
+struct ProfScope {
+  sp_ctx* c;
+  int cls;
+  size_t a = 0;
+  ProfScope(sp_ctx* c_, int cls_) : c(c_), cls(cls_) {
+    if (c->profiling) a = prof_event(c);
+  }
+  ~ProfScope() noexcept(false) {
+    if (c->profiling) c->marks.push_back({cls, a, prof_event(c)});
+  }
+};
+
 // ---- stages ---------------------------------------------------------------
 
 void stage_forward(sp_ctx* c, VDev& v) {
   const bool emit = c->fuse_keys && v.nnz > 0;
+  ProfScope prof(c, kProfFwd);
   launch_tbe_forward(v.d_meta_canon, v.d_tiles, v.n_tiles, c->B, v.d_off, v.d_idx,
                      c->d_w, v.d_pooled, v.W, emit ? v.d_keys : nullptr,
                      emit ? v.d_bags : nullptr, c->stream);
@@ -187,10 +221,12 @@ void stage_forward(sp_ctx* c, VDev& v) {
 // (keys) -> stable radix sort; leaves sorted keys in d_kb, bags in d_bb.
 void stage_sort(sp_ctx* c, VDev& v) {
   if (!v.keys_valid) {
+    ProfScope prof(c, kProfKeys);
     launch_build_keys(v.d_meta_canon, static_cast<int>(v.tables.size()), c->B, v.d_off,
                       v.d_idx, v.d_keys, v.d_bags, c->stream);
     v.keys_valid = true;
   }
+  ProfScope prof(c, kProfSort);
   sort_pairs(c->d_temp, c->temp_bytes, v.d_keys, c->d_kb, v.d_bags, c->d_bb, v.nnz,
              v.end_bit, c->stream);
 }
@@ -198,6 +234,7 @@ void stage_sort(sp_ctx* c, VDev& v) {
 void stage_backward(sp_ctx* c, VDev& v) {
   if (v.nnz == 0) return;
   stage_sort(c, v);
+  ProfScope prof(c, kProfSgd);
   launch_sgd(v.d_meta_canon, v.d_rb_end, static_cast<int>(v.tables.size()), c->d_kb,
              c->d_bb, v.nnz, v.d_grad, v.W, c->lr, c->d_w, c->stream);
 }
@@ -264,6 +301,7 @@ bool exchange_needed(const sp_ctx* c) { return c->D > 1; }
 void enqueue_iteration(sp_ctx* c) {
   for (auto& v : c->vdevs) stage_forward(c, v);
   if (exchange_needed(c)) {
+    ProfScope prof(c, kProfExchange);
     if (nccl_mode(c)) {
       a2a_fwd_nccl(c);
       a2a_bwd_nccl(c);
@@ -1030,6 +1068,30 @@ int sp_graph_replay(sp_ctx* ctx, int32_t iters, int32_t* kernels_per_iter) {
   });
 }
 
+int sp_ctx_set_profiling(sp_ctx* ctx, int32_t on) {
+  return guarded([&] {
+    check_ctx(ctx);
+    ctx->profiling = on != 0;
+  });
+}
+
+int sp_ctx_kernel_ms(sp_ctx* ctx, double ms[5], int64_t counts[5]) {
+  return guarded([&] {
+    check_ctx(ctx);
+    SP_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int k = 0; k < 5; ++k) {
+      ms[k] = 0.0;
+      if (counts) counts[k] = 0;
+    }
+    for (const auto& mk : ctx->marks) {
+      ms[mk.cls] += elapsed(ctx->ev_pool[mk.a], ctx->ev_pool[mk.b]);
+      if (counts) ++counts[mk.cls];
+    }
+    ctx->marks.clear();
+    ctx->ev_used = 0;
+  });
+}
+
 int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]) {
   return guarded([&] {
     check_ctx(ctx);
@@ -1081,3 +1143,74 @@ int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]) {
 }
 
 }  // extern "C"
+
+extern "C" int sp_synth_lookup_batch(const sp_table_spec* tables, int32_t num_tables,
+                                     int32_t batch_size, uint64_t seed,
+                                     int32_t cuda_device, int64_t* offsets,
+                                     int64_t* indices, int64_t* nnz) {
+  return guarded([&] {
+    if (num_tables < 0 || batch_size < 1 || offsets == nullptr)
+      raise(SP_ERR_BAD_INPUT, "bad batch shape");
+    SP_CUDA(cudaSetDevice(cuda_device));
+    const int T = num_tables;
+    const int64_t nb = static_cast<int64_t>(T) * batch_size;
+    std::vector<int32_t> gid(T);
+    std::vector<int64_t> lmax(T), rows(T);
+    std::vector<uint64_t> thr(T);
+    for (int i = 0; i < T; ++i) {
+      const auto& t = tables[i];
+      gid[i] = i;
+      lmax[i] = static_cast<int64_t>(std::floor(2.0 * t.pooling_factor));
+      rows[i] = t.hash_size;
+      double h = 0.0;
+      for (int b = 4; b < SP_NUM_BINS; ++b) h += t.dist[b];
+      thr[i] = hot_threshold(h);
+    }
+    cudaStream_t st = nullptr;
+    SP_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    std::vector<void*> tmp;
+    uint64_t dummy = 0;
+    auto cleanup = [&] {
+      cudaStreamSynchronize(st);
+      for (void* p : tmp) cudaFree(p);
+      cudaStreamDestroy(st);
+    };
+    try {
+      int32_t* d_gid = dalloc<int32_t>(T, tmp, dummy);
+      int64_t* d_lmax = dalloc<int64_t>(T, tmp, dummy);
+      int64_t* d_rows = dalloc<int64_t>(T, tmp, dummy);
+      uint64_t* d_thr = dalloc<uint64_t>(T, tmp, dummy);
+      int32_t* d_len = dalloc<int32_t>(nb + 1, tmp, dummy);
+      int32_t* d_off = dalloc<int32_t>(nb + 1, tmp, dummy);
+      const size_t tb = exclusive_scan_i32(nullptr, 0, d_len, d_off, nb + 1, st);
+      void* d_scan = dalloc<uint8_t>(tb, tmp, dummy);
+      if (T) {
+        SP_CUDA(cudaMemcpy(d_gid, gid.data(), T * 4, cudaMemcpyHostToDevice));
+        SP_CUDA(cudaMemcpy(d_lmax, lmax.data(), T * 8, cudaMemcpyHostToDevice));
+        SP_CUDA(cudaMemcpy(d_rows, rows.data(), T * 8, cudaMemcpyHostToDevice));
+        SP_CUDA(cudaMemcpy(d_thr, thr.data(), T * 8, cudaMemcpyHostToDevice));
+      }
+      SP_CUDA(cudaMemsetAsync(d_len + nb, 0, 4, st));
+      if (T) launch_synth_lengths(d_gid, d_lmax, T, batch_size, seed, d_len, st);
+      exclusive_scan_i32(d_scan, tb, d_len, d_off, nb + 1, st);
+      std::vector<int32_t> off32(nb + 1);
+      SP_CUDA(cudaMemcpyAsync(off32.data(), d_off, (nb + 1) * 4, cudaMemcpyDeviceToHost, st));
+      SP_CUDA(cudaStreamSynchronize(st));
+      for (int64_t k = 0; k <= nb; ++k) offsets[k] = off32[k];
+      const int64_t total = off32[nb];
+      if (nnz) *nnz = total;
+      if (indices && total) {
+        int32_t* d_idx = dalloc<int32_t>(total, tmp, dummy);
+        launch_synth_indices(d_gid, d_rows, d_thr, T, batch_size, seed, d_off, d_idx, st);
+        std::vector<int32_t> idx32(total);
+        SP_CUDA(cudaMemcpyAsync(idx32.data(), d_idx, total * 4, cudaMemcpyDeviceToHost, st));
+        SP_CUDA(cudaStreamSynchronize(st));
+        for (int64_t p = 0; p < total; ++p) indices[p] = idx32[p];
+      }
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+}
