@@ -158,6 +158,18 @@ int sp_synth_lookup_batch(const sp_table_spec* tables, int32_t num_tables,
 /* Number of local lookup indices of the current batch. */
 int sp_batch_nnz(sp_ctx* ctx, int64_t* nnz);
 
+/* The forward all-to-all plan of `rank` (host only, no GPU needed): per
+ * peer j the fp32 element offset/count sent from its pooled [B, W_rank]
+ * (rows [j*B/D, (j+1)*B/D)) and received into the grouped layout
+ * [B/D, W_total] (source-major), plus colmap[W_total]: grouped column ->
+ * global column (tables in id order). The backward exchange is the mirror.
+ * This is the exact plan the NCCL path executes. */
+int sp_exchange_plan(const sp_table_spec* tables, int32_t num_tables,
+                     int32_t num_devices, const int32_t* placement,
+                     int32_t batch_size, int32_t rank, int64_t* send_off,
+                     int64_t* send_count, int64_t* recv_off, int64_t* recv_count,
+                     int32_t* colmap);
+
 /* Stage entry points (asynchronous on the context stream). */
 int sp_forward(sp_ctx* ctx);
 int sp_a2a_forward(sp_ctx* ctx);

@@ -38,6 +38,8 @@ SIGNATURES = {
     "sp_synth_batch": (c_i32, [c_vp, c_u64]),
     "sp_batch_nnz": (c_i32, [c_vp, P(c_i64)]),
     "sp_synth_lookup_batch": (c_i32, [c_vp, c_i32, c_i32, c_u64, c_i32, c_vp, c_vp, P(c_i64)]),
+    "sp_exchange_plan": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp,
+                                 c_vp, c_vp]),
     "sp_forward": (c_i32, [c_vp]),
     "sp_a2a_forward": (c_i32, [c_vp]),
     "sp_a2a_backward": (c_i32, [c_vp]),

@@ -41,7 +41,7 @@ __all__ = [
     "MeasuredCostProvider", "ingest_lookup_batch", "compute_feature_stats", "Checkpoint",
     "load_checkpoint", "Evaluator", "infer", "ShardplanError", "nccl_unique_id",
     "hot_mass", "HostBuffer", "EXPERT_STRATEGIES", "expert_cost", "greedy_placement",
-    "expert_placement",
+    "expert_placement", "exchange_plan", "synth_lookup_batch",
 ]
 
 
@@ -226,6 +226,21 @@ def nccl_unique_id() -> bytes:
     buf = (ctypes.c_uint8 * 128)()
     check(lib().sp_nccl_unique_id(buf))
     return bytes(buf)
+
+
+def exchange_plan(task: PlacementTask, placement: Sequence[int], rank: int) -> dict:
+    """The forward all-to-all plan the NCCL path executes for `rank`
+    (sp_exchange_plan; host only). Offsets/counts are fp32 elements."""
+    D = task.num_devices
+    p = np.ascontiguousarray(placement, dtype=np.int32)
+    W = int(sum(t.dim for t in task.tables))
+    so, sc, ro, rc = (np.zeros(D, dtype=np.int64) for _ in range(4))
+    colmap = np.zeros(max(W, 1), dtype=np.int32)
+    check(lib().sp_exchange_plan(_specs(task.tables), len(task.tables), D, _ptr(p),
+                                 task.batch_size, rank, _ptr(so), _ptr(sc), _ptr(ro), _ptr(rc),
+                                 _ptr(colmap)))
+    return {"send_off": so, "send_count": sc, "recv_off": ro, "recv_count": rc,
+            "colmap": colmap[:W]}
 
 
 class HostBuffer:

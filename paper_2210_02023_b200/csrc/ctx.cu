@@ -71,6 +71,43 @@ struct VDev {
   cudaEvent_t ev[8] = {};
 };
 
+// Forward exchange of one rank: its pooled [B, W_r] is
+// batch-major, so the rows bound for peer j are the contiguous slice
+// [j*B/D, (j+1)*B/D); it receives [B/D, W_i] from every source i, grouped by
+// source. colmap maps a grouped column to its global column (tables in id
+// order). The backward exchange is the mirror (send <-> recv).
+struct ExchangePlan {
+  std::vector<int64_t> send_off, send_cnt;  // into local pooled / grad [B, W_r]
+  std::vector<int64_t> recv_off, recv_cnt;  // into grouped recv / gin [B/D, W_total]
+  std::vector<int32_t> colmap;              // W_total entries
+};
+
+inline ExchangePlan make_plan(const sp_table_spec* tables, int M, int D,
+                              const int32_t* placement, int B, int rank) {
+  ExchangePlan p;
+  const int64_t R = B / D;
+  std::vector<int64_t> W(D, 0), gcol(M, 0);
+  int64_t col = 0;
+  for (int t = 0; t < M; ++t) {
+    gcol[t] = col;
+    col += tables[t].dim;
+    W[placement[t]] += tables[t].dim;
+  }
+  int64_t cum = 0;
+  for (int j = 0; j < D; ++j) {
+    p.send_off.push_back(j * R * W[rank]);
+    p.send_cnt.push_back(R * W[rank]);
+    p.recv_off.push_back(R * cum);
+    p.recv_cnt.push_back(R * W[j]);
+    cum += W[j];
+  }
+  for (int i = 0; i < D; ++i)
+    for (int t = 0; t < M; ++t)
+      if (placement[t] == i)
+        for (int k = 0; k < tables[t].dim; ++k) p.colmap.push_back(static_cast<int32_t>(gcol[t] + k));
+  return p;
+}
+
 }  // namespace sp
 
 struct sp_ctx {
@@ -84,6 +121,7 @@ struct sp_ctx {
   std::vector<int64_t> cumW;   // prefix over devices
   int64_t W_total = 0;
   std::vector<sp::VDev> vdevs;
+  sp::ExchangePlan plan;       // NCCL mode: this rank's exchange
   std::vector<int64_t> woff;   // per global table (-1 if not local)
   float* d_w = nullptr;
   float* d_recv = nullptr;     // rows_per_dst * W_total per destination
@@ -260,32 +298,35 @@ void a2a_bwd_emulated(sp_ctx* c, VDev& v) {
         R * v.W * sizeof(float), c->stream);
 }
 
+// NCCL exchanges of this rank, driven by its ExchangePlan (the same plan
+// sp_exchange_plan exports for host-side checks).
 void a2a_fwd_nccl(sp_ctx* c) {
   VDev& v = c->vdevs[0];
-  const int64_t R = rows_per_dst(c);
+  const ExchangePlan& pl = c->plan;
   SP_NCCL(nccl().GroupStart());
   for (int j = 0; j < c->D; ++j) {
-    if (v.W > 0)
-      SP_NCCL(nccl().Send(v.d_pooled + j * R * v.W, R * v.W, ncclFloat, j, c->comm,
-                       c->stream));
-    if (c->dev_W[j] > 0)
-      SP_NCCL(nccl().Recv(c->d_recv + R * c->cumW[j], R * c->dev_W[j], ncclFloat, j,
-                       c->comm, c->stream));
+    if (pl.send_cnt[j] > 0)
+      SP_NCCL(nccl().Send(v.d_pooled + pl.send_off[j], pl.send_cnt[j], ncclFloat, j, c->comm,
+                          c->stream));
+    if (pl.recv_cnt[j] > 0)
+      SP_NCCL(nccl().Recv(c->d_recv + pl.recv_off[j], pl.recv_cnt[j], ncclFloat, j, c->comm,
+                          c->stream));
   }
   SP_NCCL(nccl().GroupEnd());
 }
 
+// Mirror of the forward exchange: gradients go back to the table owners.
 void a2a_bwd_nccl(sp_ctx* c) {
   VDev& v = c->vdevs[0];
-  const int64_t R = rows_per_dst(c);
+  const ExchangePlan& pl = c->plan;
   SP_NCCL(nccl().GroupStart());
   for (int j = 0; j < c->D; ++j) {
-    if (c->dev_W[j] > 0)
-      SP_NCCL(nccl().Send(c->d_gin + R * c->cumW[j], R * c->dev_W[j], ncclFloat, j,
-                       c->comm, c->stream));
-    if (v.W > 0)
-      SP_NCCL(nccl().Recv(v.d_grad + j * R * v.W, R * v.W, ncclFloat, j, c->comm,
-                       c->stream));
+    if (pl.recv_cnt[j] > 0)
+      SP_NCCL(nccl().Send(c->d_gin + pl.recv_off[j], pl.recv_cnt[j], ncclFloat, j, c->comm,
+                          c->stream));
+    if (pl.send_cnt[j] > 0)
+      SP_NCCL(nccl().Recv(v.d_grad + pl.send_off[j], pl.send_cnt[j], ncclFloat, j, c->comm,
+                          c->stream));
   }
   SP_NCCL(nccl().GroupEnd());
 }
@@ -525,6 +566,7 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
     if (const char* f = std::getenv("SP_FUSE_KEYS")) c->fuse_keys = std::atoi(f) != 0;
 
     if (world_size > 1) {
+      c->plan = make_plan(tables, num_tables, num_devices, placement, batch_size, rank);
       ncclUniqueId id;
       std::memcpy(id.internal, nccl_id, SP_NCCL_ID_BYTES);
       SP_NCCL(nccl().CommInitRank(&c->comm, world_size, id, rank));
@@ -1065,6 +1107,29 @@ int sp_graph_replay(sp_ctx* ctx, int32_t iters, int32_t* kernels_per_iter) {
       count_launch(c->graph_kernels);
     }
     if (kernels_per_iter) *kernels_per_iter = c->graph_kernels;
+  });
+}
+
+int sp_exchange_plan(const sp_table_spec* tables, int32_t num_tables, int32_t num_devices,
+                     const int32_t* placement, int32_t batch_size, int32_t rank,
+                     int64_t* send_off, int64_t* send_count, int64_t* recv_off,
+                     int64_t* recv_count, int32_t* colmap) {
+  return guarded([&] {
+    if (num_devices < 1 || rank < 0 || rank >= num_devices)
+      raise(SP_ERR_BAD_INPUT, "rank/num_devices out of range");
+    if (batch_size % num_devices != 0)
+      raise(SP_ERR_SHAPE_MISMATCH, "batch_size must be divisible by num_devices");
+    for (int i = 0; i < num_tables; ++i)
+      if (placement[i] < 0 || placement[i] >= num_devices)
+        raise(SP_ERR_BAD_INPUT, "device id out of range");
+    const ExchangePlan p = make_plan(tables, num_tables, num_devices, placement, batch_size, rank);
+    for (int j = 0; j < num_devices; ++j) {
+      send_off[j] = p.send_off[j];
+      send_count[j] = p.send_cnt[j];
+      recv_off[j] = p.recv_off[j];
+      recv_count[j] = p.recv_cnt[j];
+    }
+    if (colmap) std::copy(p.colmap.begin(), p.colmap.end(), colmap);
   });
 }
 
