@@ -221,6 +221,37 @@ def config_dict(args, task):
             "parallelism": f"table-wise model parallel x{task.num_devices}"}
 
 
+def bench_evaluator(args, device: int, n: int = 4096):
+    """Batched cost-net scoring and policy rollouts (K6/K7) of one task."""
+    import torch
+    from paper_2210_02023_b200 import api
+    task = load_task(args.config, 8)
+    ckpt = api.load_checkpoint(CKPT)
+    ev = api.Evaluator(ckpt, task, device=device)
+    M = len(task.tables)
+    rng = np.random.default_rng(0)
+    placements = rng.integers(0, 8, size=(n, M)).astype(np.int32)
+    uniforms = rng.random((n, M))
+    out = {"candidates": n, "tables": M, "devices": 8}
+    for name, fn in (
+            ("eval_batch_ms", lambda: ev.eval_batch(placements)),
+            ("greedy_rollouts_ms", lambda: ev.rollout(n, "greedy")),
+            ("sampled_rollouts_ms", lambda: ev.rollout(n, "sample", uniforms=uniforms))):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = fn()
+        torch.cuda.synchronize()
+        out[name] = round((time.perf_counter() - t0) * 1e3, 3)
+        if name != "eval_batch_ms":
+            out[name.replace("_ms", "_refined")] = int(r[3])
+    out["note"] = ("host wall time per call incl. H2D/D2H; reference CPU: infer (one greedy "
+                   "rollout) 65-91 ms at M=100, EstimatedCostProvider::overall 10-16 us per "
+                   "placement (SURVEY §6)")
+    ev.close()
+    return out
+
+
 # ---------------------------------------------------------------------------
 
 def run_ours(args, world, rank, local):
@@ -364,6 +395,12 @@ def run_ours(args, world, rank, local):
         }
         esh.close()
 
+    # K6/K7 evaluator throughput (SURVEY cfg5 shape): 4096 candidate
+    # placements of this task at D = 8, scored and rolled out on this GPU
+    evaluator = None
+    if rank == 0 and not args.no_evaluator:
+        evaluator = bench_evaluator(args, local)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(ms, 4), "unit": UNIT, "n_gpus": world,
@@ -391,6 +428,7 @@ def run_ours(args, world, rank, local):
                                             "into our library, K4 SGD)"},
             "clocks": clk.summary(),
             "emulated_d8": emulated,
+            "evaluator": evaluator,
         }
         print(json.dumps(line), flush=True)
     shard.close()
@@ -408,6 +446,7 @@ def main():
     ap.add_argument("--cpu-sample-bags", type=int, default=2048)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-emulation", action="store_true")
+    ap.add_argument("--no-evaluator", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
