@@ -9,7 +9,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_shardplan_b200.so")
+LIB_PATH = os.environ.get("SP_LIBRARY") or os.path.join(HERE, "_shardplan_b200.so")  # SP_LIBRARY: A/B builds
 
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64

@@ -18,8 +18,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "_shardplan_b200.so")
+# SP_BUILD_DIR / SP_LIB_OUT / SP_NVCC_EXTRA: side builds for A/B experiments
+BUILD = os.environ.get("SP_BUILD_DIR") or os.path.join(HERE, "_build")
+LIB = os.environ.get("SP_LIB_OUT") or os.path.join(HERE, "_shardplan_b200.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # NCCL is not linked: csrc/nccl_loader.h binds it at run time (torch ships
@@ -50,7 +51,8 @@ def _compile(src: str) -> tuple[str, str]:
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(
             os.path.getmtime(f) for f in [src] + _headers()):
         return obj, ""
-    cmd = [nvcc()] + ARCH + NVCC_FLAGS + ["-c", src, "-o", obj]
+    extra = os.environ.get("SP_NVCC_EXTRA", "").split()
+    cmd = [nvcc()] + ARCH + NVCC_FLAGS + extra + ["-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True, env=_host_compiler_env())
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

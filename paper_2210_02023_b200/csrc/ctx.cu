@@ -477,7 +477,10 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
         if (placement[i] == d) {
           c->woff[i] = slab;
           slab += tables[i].hash_size * tables[i].dim;
-          slab = (slab + 3) & ~int64_t(3);
+          // 256-byte aligned table bases: with dim a multiple of 16, every
+          // row starts on a 64-byte DRAM burst (a 16-byte aligned base can
+          // make each 64-byte row straddle two bursts)
+          slab = (slab + 63) & ~int64_t(63);
         }
     c->d_w = dalloc<float>(slab, c->owned, c->dev_bytes);
 

@@ -33,6 +33,22 @@ __device__ __forceinline__ float4 ldg_f4(const float* p) {
   return __ldg(reinterpret_cast<const float4*>(p));
 }
 
+// L2 eviction-priority policies (createpolicy) for loads that should stay
+// resident (the per-table gradient slice in K4) or stream through.
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ float4 ldg_f4_policy(const float* ptr, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(ptr), "l"(pol));
+  return v;
+}
+
 __device__ __forceinline__ float4 shfl_xor_f4(float4 v, int m) {
   v.x = __shfl_xor_sync(0xffffffffu, v.x, m);
   v.y = __shfl_xor_sync(0xffffffffu, v.y, m);
@@ -62,12 +78,28 @@ template <> struct FwdGeo<5> : Geo<32, 1, 1, 8> {};
 // K4 SGD: most runs hold 1-2 positions, so more runs per warp (P) matter
 // more than rows per run; lanes move up to 64 B of a row.
 template <int CLS> struct SgdGeo;
-template <> struct SgdGeo<0> : Geo<1, 1, 16, 2> {};
-template <> struct SgdGeo<1> : Geo<2, 1, 16, 2> {};
-template <> struct SgdGeo<2> : Geo<2, 2, 16, 2> {};
-template <> struct SgdGeo<3> : Geo<4, 2, 8, 2> {};
-template <> struct SgdGeo<4> : Geo<4, 4, 8, 2> {};
-template <> struct SgdGeo<5> : Geo<8, 4, 4, 2> {};
+#ifdef SP_GEO_HEADER  // A/B builds: -DSP_GEO_HEADER=\"geo.h\" overriding the knobs below
+#include SP_GEO_HEADER
+#endif
+#ifndef SP_SGD_G0
+// (L, V, P, U) per dim class; tuned on B200 at cfg3 (profiles/r01_notes.md):
+// short runs are mostly one position, so U = 1 and registers go to V/P.
+#define SP_SGD_G0 1, 1, 16, 2
+#define SP_SGD_G1 2, 1, 16, 1
+#define SP_SGD_G2 2, 2, 16, 1
+#define SP_SGD_G3 4, 2, 8, 1
+#define SP_SGD_G4 8, 2, 4, 1
+#define SP_SGD_G5 16, 2, 2, 1
+#endif
+#ifndef SP_SGD_INTERLEAVE  // lane float4 slices: 1 interleaved (s, s+L, ..), 0 blocked
+#define SP_SGD_INTERLEAVE 1
+#endif
+template <> struct SgdGeo<0> : Geo<SP_SGD_G0> {};
+template <> struct SgdGeo<1> : Geo<SP_SGD_G1> {};
+template <> struct SgdGeo<2> : Geo<SP_SGD_G2> {};
+template <> struct SgdGeo<3> : Geo<SP_SGD_G3> {};
+template <> struct SgdGeo<4> : Geo<SP_SGD_G4> {};
+template <> struct SgdGeo<5> : Geo<SP_SGD_G5> {};
 // K4 SGD, long runs (hot rows): the whole warp on one run.
 template <int CLS> struct LongGeo;
 template <> struct LongGeo<0> : Geo<1, 1, 1, 4> {};
@@ -101,7 +133,7 @@ __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb
                                               int64_t ldo) {
   constexpr int L = G::L, V = G::V, P = G::P, U = G::U, S = G::S, GB = G::GB;
   const int span = lane / S, ls = lane % S, g = ls / L, s = ls % L;
-  const float* wt = w + m.woff + 4 * V * s;
+  const float* wt = w + m.woff + 4 * s;  // lane s moves float4 s, s+L, s+2L, ... (coalesced)
   const int dim = m.dim;
   for (int bg = warp * P; bg < nb; bg += kWarpsPerBlock * P) {
     const int bag = bg + span;
@@ -126,7 +158,7 @@ __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int j = 0; j < V; ++j)
-          v[u][j] = r[u] >= 0 ? ldg_f4(wt + static_cast<int64_t>(r[u]) * dim + 4 * j)
+          v[u][j] = r[u] >= 0 ? ldg_f4(wt + static_cast<int64_t>(r[u]) * dim + 4 * L * j)
                               : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int u = 0; u < U; ++u)
@@ -138,9 +170,9 @@ __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb
 #pragma unroll
       for (int j = 0; j < V; ++j) acc[j] = f4_add(acc[j], shfl_xor_f4(acc[j], o));
     if (ok && g == 0) {
-      float* o = out + static_cast<int64_t>(b0 + bag) * ldo + m.lcol + 4 * V * s;
+      float* o = out + static_cast<int64_t>(b0 + bag) * ldo + m.lcol + 4 * s;
 #pragma unroll
-      for (int j = 0; j < V; ++j) *reinterpret_cast<float4*>(o + 4 * j) = acc[j];
+      for (int j = 0; j < V; ++j) __stcs(reinterpret_cast<float4*>(o + 4 * L * j), acc[j]);
     }
   }
 }
@@ -192,8 +224,8 @@ __global__ void __launch_bounds__(kBlockThreads)
         const int mid = (lo + hi + 1) >> 1;
         if (s_off[mid] <= p0 + i) lo = mid; else hi = mid - 1;
       }
-      keys[p0 + i] = m.rowbase + static_cast<uint32_t>(v);
-      bags[p0 + i] = static_cast<uint32_t>(tile.b0 + lo);
+      __stcs(keys + p0 + i, m.rowbase + static_cast<uint32_t>(v));
+      __stcs(bags + p0 + i, static_cast<uint32_t>(tile.b0 + lo));
     }
   }
   __syncthreads();
@@ -312,6 +344,7 @@ __device__ __forceinline__ int sgd_round(const TableMeta& m, uint32_t rb_end,
                                          float* __restrict__ w) {
   constexpr int L = G::L, V = G::V, P = G::P, U = G::U, S = G::S, GB = G::GB;
   const int span = lane / S, ls = lane % S, g = ls / L, sub = ls % L;
+  constexpr int kLane = SP_SGD_INTERLEAVE ? 1 : V, kStep = SP_SGD_INTERLEAVE ? L : 1;
   const int u = j + span;
   bool valid = u < jend;
   int beg = 0, end = 0;
@@ -341,11 +374,11 @@ __device__ __forceinline__ int sgd_round(const TableMeta& m, uint32_t rb_end,
   float* wrow = nullptr;
   if (active) {
     const int64_t row = static_cast<int64_t>(key - m.rowbase);
-    wrow = w + m.woff + row * m.dim + 4 * V * sub;
+    wrow = w + m.woff + row * m.dim + 4 * kLane * sub;
     if (g == 0)
 #pragma unroll
-      for (int q = 0; q < V; ++q) wold[q] = *reinterpret_cast<const float4*>(wrow + 4 * q);
-    const float* gcol = grad + m.lcol + 4 * V * sub;
+      for (int q = 0; q < V; ++q) wold[q] = *reinterpret_cast<const float4*>(wrow + 4 * kStep * q);
+    const float* gcol = grad + m.lcol + 4 * kLane * sub;
     for (int k = beg + g; k < end; k += GB * U) {
       uint32_t bg[U];
 #pragma unroll
@@ -359,7 +392,7 @@ __device__ __forceinline__ int sgd_round(const TableMeta& m, uint32_t rb_end,
 #pragma unroll
         for (int c = 0; c < V; ++c)
           v[q][c] = bg[q] != 0xffffffffu
-                        ? ldg_f4(gcol + static_cast<int64_t>(bg[q]) * ldg + 4 * c)
+                        ? ldg_f4(gcol + static_cast<int64_t>(bg[q]) * ldg + 4 * kStep * c)
                         : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int q = 0; q < U; ++q)
@@ -379,7 +412,7 @@ __device__ __forceinline__ int sgd_round(const TableMeta& m, uint32_t rb_end,
       r.y = fmaf(-lr, acc[c].y, wold[c].y);
       r.z = fmaf(-lr, acc[c].z, wold[c].z);
       r.w = fmaf(-lr, acc[c].w, wold[c].w);
-      *reinterpret_cast<float4*>(wrow + 4 * c) = r;
+      *reinterpret_cast<float4*>(wrow + 4 * kStep * c) = r;
     }
   }
   return nvalid;
@@ -407,7 +440,10 @@ __device__ __forceinline__ int sgd_round_generic(
   return 1;
 }
 
-__global__ void __launch_bounds__(kBlockThreads)
+#ifndef SP_SGD_MIN_BLOCKS
+#define SP_SGD_MIN_BLOCKS 4  // 4 x 256 threads per SM: <= 64 registers
+#endif
+__global__ void __launch_bounds__(kBlockThreads, SP_SGD_MIN_BLOCKS)
     sgd_kernel(const TableMeta* __restrict__ meta,
                const uint32_t* __restrict__ rb_end_g, int n_tables,
                const uint32_t* __restrict__ keys,
