@@ -312,13 +312,9 @@ def run_ours(args, world, rank, local):
     T_local = len(shard.local_tables())
     peak, peak_kind = load_peaks()
     per_launch = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in kms.items()}
-    alg = {
-        # K1 also writes the backward's sort pairs (8 B per lookup)
-        "fwd": ab["fwd"] + (8.0 * nnz if os.environ.get("SP_FUSE_KEYS", "1") != "0" else 0.0),
-        # K4 SGD: grad 4*B*W + W row read/write 8*sum_unique dim + sorted pairs 8*nnz
-        "sgd": ab["bwd"] - 4.0 * (T_local * task.batch_size + 1) - 4.0 * nnz + 8.0 * nnz,
-        "sort": ab["sort"],
-    }
+    # per-launch algorithmic bytes as the library runs each kernel
+    # (sp_ctx_algorithmic_bytes documents the formulas)
+    alg = {"fwd": ab["fwd"], "sgd": ab["bwd"], "sort": ab["sort"]}
     kernels = {}
     for k in ("fwd", "sort", "sgd"):
         t = per_launch.get(k, 0.0)

@@ -24,6 +24,7 @@
 #include "common.h"
 #include "nccl_loader.h"
 #include "synth.cuh"
+#include "bwd.h"
 #include "tbe.h"
 
 namespace sp {
@@ -58,6 +59,12 @@ struct VDev {
   uint32_t* d_keys = nullptr;   // backward sort pairs (written by K1)
   uint32_t* d_bags = nullptr;
   bool keys_valid = false;
+  // K4 v2 (bwd.cu): bucket layout of the current batch
+  bool bucketed = false;
+  std::vector<BucketMeta> bmeta;
+  BucketMeta* d_bm = nullptr;
+  int64_t n_cnt = 0;
+  int n_btiles = 0, n_buckets = 0;
   TableMeta* d_meta_canon = nullptr;
   uint32_t* d_rb_end = nullptr;
   int32_t* d_colmap = nullptr;
@@ -129,7 +136,13 @@ struct sp_ctx {
   int n_dst = 1;               // destinations held here (D in emulation)
   uint32_t *d_kb = nullptr, *d_bb = nullptr;  // sorted keys / bags
   uint32_t* d_seg = nullptr;
-  bool fuse_keys = true;       // K1 emits the backward's sort pairs
+  bool fuse_keys = true;       // K1 emits the backward's sort pairs (CUB path)
+  bool use_buckets = false;    // K4 v2 bucketed sort + SGD (SP_BWD=bucket); slower on
+                               // B200 so far (profiles/r01_notes.md), CUB path default
+  int32_t *d_prow = nullptr, *d_pbag = nullptr, *d_scr = nullptr;  // bucketed pairs
+  int32_t *d_cnt = nullptr, *d_cpos = nullptr;
+  int64_t cnt_cap = 0;
+  std::vector<void*> bucket_owned;
   int32_t* d_nseg = nullptr;
   int32_t* d_flag = nullptr;
   int64_t sort_cap = 0;
@@ -169,6 +182,7 @@ struct sp_ctx {
                        static_cast<void*>(v.d_bags)})
         if (p) cudaFree(p);
     if (d_stage64) cudaFree(d_stage64);
+    for (void* p : bucket_owned) cudaFree(p);
     for (void* p : sort_owned) cudaFree(p);
     for (void* p : owned) cudaFree(p);
     if (comm) sp::nccl().CommDestroy(comm);
@@ -200,7 +214,40 @@ void ensure_sort_capacity(sp_ctx* c, int64_t n) {
                                  c->stream);
   c->temp_bytes = std::max({t1, t2, static_cast<size_t>(256)});
   c->d_temp = dalloc<uint8_t>(c->temp_bytes, c->sort_owned, dummy);
+  // bucketed backward: (row, bag) pairs in bucket order + oversize scratch
+  c->d_prow = dalloc<int32_t>(cap, c->sort_owned, dummy);
+  c->d_pbag = dalloc<int32_t>(cap, c->sort_owned, dummy);
+  c->d_scr = dalloc<int32_t>(cap, c->sort_owned, dummy);
   c->sort_cap = cap;
+}
+
+// Bucket layouts of every (virtual) device for the current batch.
+void plan_buckets(sp_ctx* c) {
+  int64_t need = 0;
+  for (auto& v : c->vdevs) {
+    v.bucketed = c->use_buckets && !v.tables.empty() &&
+                 bucket_plan(v.meta_canon, v.table_nnz, c->B, v.bmeta, v.n_cnt, v.n_btiles,
+                             v.n_buckets);
+    if (!v.bucketed) continue;
+    if (!v.d_bm) v.d_bm = dalloc<BucketMeta>(v.tables.size(), c->bucket_owned, c->dev_bytes);
+    SP_CUDA(cudaMemcpy(v.d_bm, v.bmeta.data(), v.bmeta.size() * sizeof(BucketMeta),
+                       cudaMemcpyHostToDevice));
+    need = std::max(need, v.n_cnt);
+  }
+  if (need > c->cnt_cap) {
+    SP_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->d_cnt) cudaFree(c->d_cnt);
+    if (c->d_cpos) cudaFree(c->d_cpos);
+    SP_CUDA(cudaMalloc(&c->d_cnt, need * sizeof(int32_t)));
+    SP_CUDA(cudaMalloc(&c->d_cpos, need * sizeof(int32_t)));
+    c->cnt_cap = need;
+    const size_t tb = bwd_scan_temp_bytes(need, c->stream);
+    if (tb > c->temp_bytes) {
+      uint64_t dummy = 0;
+      c->temp_bytes = tb;
+      c->d_temp = dalloc<uint8_t>(tb, c->sort_owned, dummy);
+    }
+  }
 }
 
 void check_ctx(sp_ctx* c) {
@@ -248,7 +295,7 @@ struct ProfScope {
 // ---- stages ---------------------------------------------------------------
 
 void stage_forward(sp_ctx* c, VDev& v) {
-  const bool emit = c->fuse_keys && v.nnz > 0;
+  const bool emit = c->fuse_keys && !v.bucketed && v.nnz > 0;
   ProfScope prof(c, kProfFwd);
   launch_tbe_forward(v.d_meta_canon, v.d_tiles, v.n_tiles, c->B, v.d_off, v.d_idx,
                      c->d_w, v.d_pooled, v.W, emit ? v.d_keys : nullptr,
@@ -269,8 +316,29 @@ void stage_sort(sp_ctx* c, VDev& v) {
              v.end_bit, c->stream);
 }
 
+// Bucketed backward (bwd.cu): partition pairs into row buckets, then one
+// block per bucket sorts by row and applies the SGD. sorted_* non-null also
+// writes the sorted (key, bag) pairs (test API) and do_sgd gates the update.
+void stage_backward_bucketed(sp_ctx* c, VDev& v, uint32_t* sorted_keys, uint32_t* sorted_bags,
+                             bool do_sgd) {
+  const int T = static_cast<int>(v.tables.size());
+  {
+    ProfScope prof(c, kProfSort);
+    launch_bwd_partition(v.d_bm, T, v.n_btiles, v.n_cnt, c->B, v.d_off, v.d_idx, c->d_cnt,
+                         c->d_cpos, c->d_temp, c->temp_bytes, c->d_prow, c->d_pbag, c->stream);
+  }
+  ProfScope prof(c, kProfSgd);
+  launch_bwd_buckets(v.d_meta_canon, v.d_bm, T, v.n_buckets, c->d_cpos, v.nnz, c->d_prow,
+                     c->d_pbag, c->d_scr, v.d_grad, v.W, c->lr, c->d_w, sorted_keys, sorted_bags,
+                     do_sgd, c->stream);
+}
+
 void stage_backward(sp_ctx* c, VDev& v) {
   if (v.nnz == 0) return;
+  if (v.bucketed) {
+    stage_backward_bucketed(c, v, nullptr, nullptr, true);
+    return;
+  }
   stage_sort(c, v);
   ProfScope prof(c, kProfSgd);
   launch_sgd(v.d_meta_canon, v.d_rb_end, static_cast<int>(v.tables.size()), c->d_kb,
@@ -567,6 +635,7 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
     SP_CUDA(cudaMemset(c->d_barrier, 0, sizeof(int32_t)));
     for (auto& e : c->ev_a2a) SP_CUDA(cudaEventCreate(&e));
     if (const char* f = std::getenv("SP_FUSE_KEYS")) c->fuse_keys = std::atoi(f) != 0;
+    if (const char* f = std::getenv("SP_BWD")) c->use_buckets = std::string(f) == "bucket";
 
     if (world_size > 1) {
       c->plan = make_plan(tables, num_tables, num_devices, placement, batch_size, rank);
@@ -652,6 +721,7 @@ static void finish_batch(sp_ctx* c) {
   int64_t max_nnz = 0;
   for (auto& v : c->vdevs) max_nnz = std::max(max_nnz, v.nnz);
   ensure_sort_capacity(c, max_nnz);
+  plan_buckets(c);
   c->has_batch = true;
   if (c->graph_exec) {
     cudaGraphExecDestroy(c->graph_exec);
@@ -960,7 +1030,8 @@ int sp_get_sorted(sp_ctx* ctx, int32_t dev, uint32_t* keys, uint32_t* bags,
     VDev& v = vdev_for(ctx, dev);
     int32_t nseg = 0;
     if (v.nnz > 0) {
-      stage_sort(ctx, v);
+      if (v.bucketed) stage_backward_bucketed(ctx, v, ctx->d_kb, ctx->d_bb, false);
+      else stage_sort(ctx, v);
       select_heads(ctx->d_temp, ctx->temp_bytes, ctx->d_kb, v.nnz, ctx->d_seg, ctx->d_nseg,
                    ctx->stream);
       SP_CUDA(cudaMemcpyAsync(&nseg, ctx->d_nseg, 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1165,47 +1236,58 @@ int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]) {
     check_ctx(ctx);
     require_batch(ctx);
     sp_ctx* c = ctx;
-    // Max over the (virtual) devices held here of the SURVEY §8d formulas.
-    double fwd = 0, a2a = 0, bwd = 0, sort = 0;
+    // Max over the (virtual) devices held here; SURVEY §8d formulas, 4-byte
+    // ids, per launch of each kernel as this build runs it:
+    //  [0] K1: offsets + ids + gathered rows + pooled out (+ 8 B/lookup of
+    //      sort pairs when K1 emits them for the CUB path)
+    //  [1] exchange sent per direction
+    //  [2] K4 SGD kernel: gradient 4*B*W + touched rows read+write
+    //      8*sum_unique dim + the pairs it reads (8 B/lookup, the bucketed
+    //      kernel also re-reads rows for its histogram: +4 B)
+    //  [3] sort / partition: CUB 16 B/lookup/pass; bucketed: ids twice +
+    //      pair write (8+8 B/lookup) + offsets
+    double fwd = 0, a2a = 0, sgd = 0, sort = 0;
     for (auto& v : c->vdevs) {
       const int T = static_cast<int>(v.tables.size());
       double rows_bytes = 0;
       for (int li = 0; li < T; ++li)
         rows_bytes += 4.0 * static_cast<double>(v.table_nnz[li]) * c->tables[v.tables[li]].dim;
-      const double csr = 4.0 * (static_cast<double>(T) * c->B + 1) + 4.0 * v.nnz;
+      const double offs = 4.0 * (static_cast<double>(T) * c->B + 1);
+      const double csr = offs + 4.0 * v.nnz;
       const double outb = 4.0 * c->B * v.W;
-      fwd = std::max(fwd, csr + rows_bytes + outb);
+      const bool emit = c->fuse_keys && !v.bucketed;
+      fwd = std::max(fwd, csr + rows_bytes + outb + (emit ? 8.0 * v.nnz : 0.0));
       a2a = std::max(a2a, 4.0 * c->B * v.W * (c->D - 1) / c->D);
-      // unique rows per table from the run heads
       double uniq_dim = 0;
       if (v.nnz) {
-        uint32_t *keys = nullptr;
-        std::vector<uint32_t> k(v.nnz), heads;
-        keys = k.data();
-        int64_t nk = 0, nu = 0;
-        stage_sort(c, v);
+        if (v.bucketed) stage_backward_bucketed(c, v, c->d_kb, c->d_bb, false);
+        else stage_sort(c, v);
         select_heads(c->d_temp, c->temp_bytes, c->d_kb, v.nnz, c->d_seg, c->d_nseg, c->stream);
         int32_t nseg = 0;
+        std::vector<uint32_t> keys(v.nnz), heads;
         SP_CUDA(cudaMemcpyAsync(&nseg, c->d_nseg, 4, cudaMemcpyDeviceToHost, c->stream));
-        SP_CUDA(cudaMemcpyAsync(keys, c->d_kb, v.nnz * 4, cudaMemcpyDeviceToHost, c->stream));
+        SP_CUDA(cudaMemcpyAsync(keys.data(), c->d_kb, v.nnz * 4, cudaMemcpyDeviceToHost, c->stream));
         SP_CUDA(cudaStreamSynchronize(c->stream));
         heads.resize(nseg);
-        if (nseg) SP_CUDA(cudaMemcpy(heads.data(), c->d_seg, static_cast<int64_t>(nseg) * 4, cudaMemcpyDeviceToHost));
-        nu = nseg;
-        for (int64_t u = 0; u < nu; ++u) {
+        if (nseg)
+          SP_CUDA(cudaMemcpy(heads.data(), c->d_seg, static_cast<int64_t>(nseg) * 4,
+                             cudaMemcpyDeviceToHost));
+        for (int32_t u = 0; u < nseg; ++u) {
           const uint32_t key = keys[heads[u]];
-          const int li = static_cast<int>(std::upper_bound(v.rb_end.begin(), v.rb_end.end(), key) - v.rb_end.begin());
+          const int li = static_cast<int>(
+              std::upper_bound(v.rb_end.begin(), v.rb_end.end(), key) - v.rb_end.begin());
           uniq_dim += c->tables[v.tables[li]].dim;
         }
       }
-      bwd = std::max(bwd, outb + csr + 8.0 * uniq_dim);
-      // onesweep radix sort: ~ (passes) x read+write of 8-byte pairs
-      const int passes = (v.end_bit + 7) / 8;
-      sort = std::max(sort, 16.0 * v.nnz * passes);
+      sgd = std::max(sgd, outb + 8.0 * uniq_dim + (v.bucketed ? 12.0 : 8.0) * v.nnz);
+      if (v.bucketed)
+        sort = std::max(sort, 2.0 * csr + 8.0 * v.nnz + 8.0 * v.n_cnt);
+      else
+        sort = std::max(sort, 16.0 * v.nnz * ((v.end_bit + 7) / 8));
     }
     out[0] = fwd;
     out[1] = a2a;
-    out[2] = bwd;
+    out[2] = sgd;
     out[3] = sort;
   });
 }

@@ -80,9 +80,17 @@ def test_forward_hand_case():
     np.testing.assert_array_equal(got, want)
 
 
+@pytest.fixture(params=["cub", "bucket"])
+def bwd_path(request, monkeypatch):
+    """Both backward implementations: CUB radix sort + tiled SGD (default)
+    and the bucketed counting sort fused with the SGD (SP_BWD=bucket)."""
+    monkeypatch.setenv("SP_BWD", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("dims", list(DIM_SETS))
 @pytest.mark.parametrize("D", [1, 2])
-def test_backward_matches_oracle(dims, D):
+def test_backward_matches_oracle(dims, D, bwd_path):
     B = 64
     task, placement = random_task(19 + D, DIM_SETS[dims], D, B, rows_range=(1, 200))
     weights = random_weights(3, task.tables)
@@ -111,7 +119,7 @@ def test_backward_matches_oracle(dims, D):
         np.testing.assert_allclose(sh.get_table(i), want[i], rtol=RTOL, atol=ATOL)
 
 
-def test_device_generator_matches_oracle():
+def test_device_generator_matches_oracle(bwd_path):
     """sp_synth_batch / sp_init_tables / sp_synth_grad are bit-identical to the
     oracle generator: same sorted keys, same pooled sums, same update."""
     B = 128
@@ -198,7 +206,7 @@ def test_memory_cap_enforced():
     assert e.value.kind == "memory_violation" and e.value.exit_code == 2
 
 
-def test_hot_rows_and_empty_tables():
+def test_hot_rows_and_empty_tables(bwd_path):
     """All-hot table (long duplicate runs), a never-accessed table (pf 0)."""
     B = 512
     tables = make_tables([32, 16, 128], [5000, 300, 70], [20.0, 0.0, 3.0], hot=[1.0, 0.0, 0.9])
