@@ -151,6 +151,8 @@ struct sp_ctx {
   int64_t* d_stage64 = nullptr;
   int64_t stage_cap = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // H2D of uploaded batches
+  std::vector<cudaEvent_t> upload_events;
   ncclComm_t comm = nullptr;
   double* d_bd = nullptr;      // breakdown gather buffer
   int32_t* d_barrier = nullptr;
@@ -186,6 +188,9 @@ struct sp_ctx {
     for (void* p : sort_owned) cudaFree(p);
     for (void* p : owned) cudaFree(p);
     if (comm) sp::nccl().CommDestroy(comm);
+    if (copy_stream) cudaStreamSynchronize(copy_stream);
+    for (auto& e : upload_events) cudaEventDestroy(e);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -516,6 +521,7 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
     c->placement.assign(placement, placement + num_tables);
     SP_CUDA(cudaSetDevice(cuda_device));
     SP_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    SP_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
 
     // Columns: global table order; per-device widths.
     c->gcol.resize(num_tables);
@@ -779,7 +785,7 @@ int sp_upload_batch(sp_ctx* ctx, const int64_t* offsets, int64_t offsets_len,
         st += tn + B + 1;
       }
       alloc_indices(c, v, n);
-      stage_need = std::max(stage_need, st);
+      stage_need += st;  // copies run ahead of the narrows: no reuse across devices
     }
     if (stage_need > c->stage_cap) {
       SP_CUDA(cudaStreamSynchronize(c->stream));
@@ -788,24 +794,65 @@ int sp_upload_batch(sp_ctx* ctx, const int64_t* offsets, int64_t offsets_len,
       c->stage_cap = std::max<int64_t>(stage_need, 1);
     }
     SP_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int32_t), c->stream));
+    // Coalesced, pipelined H2D: local tables with consecutive global ids
+    // are adjacent in the reference CSR, so each such run is copied with two
+    // large memcpys, cut into chunks of <= kUploadChunk indices on the copy
+    // stream while the compute stream narrows the previous chunk.
+    constexpr int64_t kUploadChunk = int64_t(8) << 20;
+    size_t n_ev = 0;
+    auto next_event = [&]() {
+      if (n_ev == c->upload_events.size()) {
+        cudaEvent_t e;
+        SP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->upload_events.push_back(e);
+      }
+      return c->upload_events[n_ev++];
+    };
+    {
+      // the staging buffer may still be read by the previous upload's narrows
+      cudaEvent_t e = next_event();
+      SP_CUDA(cudaEventRecord(e, c->stream));
+      SP_CUDA(cudaStreamWaitEvent(c->copy_stream, e, 0));
+    }
+    int64_t so = 0;  // staging offset (int64 elements), across all devices
     for (auto& v : c->vdevs) {
-      int64_t so = 0;
+      const int T = static_cast<int>(v.tables.size());
       int32_t base = 0;
-      for (size_t li = 0; li < v.tables.size(); ++li) {
-        const int g = v.tables[li];
-        const int64_t tn = v.table_nnz[li];
-        int64_t* s_off = c->d_stage64 + so;
-        int64_t* s_idx = s_off + B + 1;
-        SP_CUDA(cudaMemcpyAsync(s_off, offsets + g * B, (B + 1) * sizeof(int64_t),
-                                cudaMemcpyHostToDevice, c->stream));
-        if (tn)
-          SP_CUDA(cudaMemcpyAsync(s_idx, indices + offsets[g * B], tn * sizeof(int64_t),
-                                  cudaMemcpyHostToDevice, c->stream));
-        launch_narrow_table(s_off, s_idx, c->B, tn, c->tables[g].hash_size, base,
-                            v.d_off + li * B, v.d_idx + base, c->d_flag, c->stream);
-        // indices of this table land after the earlier tables' indices
-        so += tn + B + 1;
-        base += static_cast<int32_t>(tn);
+      int li = 0;
+      while (li < T) {
+        int run_end = li + 1;
+        while (run_end < T && v.tables[run_end] == v.tables[run_end - 1] + 1) ++run_end;
+        int c0 = li;
+        while (c0 < run_end) {
+          int c1 = c0 + 1;
+          int64_t acc = v.table_nnz[c0];
+          while (c1 < run_end && acc + v.table_nnz[c1] <= kUploadChunk) acc += v.table_nnz[c1++];
+          const int64_t g0 = v.tables[c0], g1 = v.tables[c1 - 1] + 1;
+          const int64_t n_off = (g1 - g0) * B + 1;
+          const int64_t i0 = offsets[g0 * B];
+          const int64_t n_idx = offsets[g1 * B] - i0;
+          int64_t* s_off = c->d_stage64 + so;
+          int64_t* s_idx = s_off + n_off;
+          SP_CUDA(cudaMemcpyAsync(s_off, offsets + g0 * B, n_off * sizeof(int64_t),
+                                  cudaMemcpyHostToDevice, c->copy_stream));
+          if (n_idx)
+            SP_CUDA(cudaMemcpyAsync(s_idx, indices + i0, n_idx * sizeof(int64_t),
+                                    cudaMemcpyHostToDevice, c->copy_stream));
+          cudaEvent_t e = next_event();
+          SP_CUDA(cudaEventRecord(e, c->copy_stream));
+          SP_CUDA(cudaStreamWaitEvent(c->stream, e, 0));
+          for (int t = c0; t < c1; ++t) {
+            const int g = v.tables[t];
+            const int64_t tn = v.table_nnz[t];
+            launch_narrow_table(s_off + (g - g0) * B, s_idx + (offsets[g * B] - i0), c->B, tn,
+                                c->tables[g].hash_size, base, v.d_off + int64_t(t) * B,
+                                v.d_idx + base, c->d_flag, c->stream);
+            base += static_cast<int32_t>(tn);
+          }
+          so += n_off + n_idx;
+          c0 = c1;
+        }
+        li = run_end;
       }
       if (v.tables.empty())
         SP_CUDA(cudaMemsetAsync(v.d_off, 0, sizeof(int32_t), c->stream));
