@@ -119,6 +119,7 @@ inline ExchangePlan make_plan(const sp_table_spec* tables, int M, int D,
 
 struct sp_ctx {
   int M = 0, D = 1, world = 1, rank = 0, B = 0, device = 0;
+  bool bags16 = false;  // B <= 65536: 16-bit bag payload through the sort
   float lr = 0.01f;
   double cap = 0.0;
   std::vector<sp_table_spec> tables;
@@ -213,7 +214,7 @@ void ensure_sort_capacity(sp_ctx* c, int64_t n) {
   c->d_seg = dalloc<uint32_t>(cap + 1, c->sort_owned, dummy);
   int max_bit = 1;
   for (auto& v : c->vdevs) max_bit = std::max(max_bit, v.end_bit);
-  const size_t t1 = sort_pairs(nullptr, 0, c->d_kb, c->d_kb, c->d_bb, c->d_bb, cap,
+  const size_t t1 = sort_pairs(nullptr, 0, c->d_kb, c->d_kb, c->d_bb, c->d_bb, c->bags16, cap,
                                max_bit, c->stream);
   const size_t t2 = select_heads(nullptr, 0, c->d_kb, cap, c->d_seg, c->d_nseg,
                                  c->stream);
@@ -304,7 +305,7 @@ void stage_forward(sp_ctx* c, VDev& v) {
   ProfScope prof(c, kProfFwd);
   launch_tbe_forward(v.d_meta_canon, v.d_tiles, v.n_tiles, c->B, v.d_off, v.d_idx,
                      c->d_w, v.d_pooled, v.W, emit ? v.d_keys : nullptr,
-                     emit ? v.d_bags : nullptr, c->stream);
+                     emit ? v.d_bags : nullptr, c->bags16, c->stream);
   if (emit) v.keys_valid = true;
 }
 
@@ -313,12 +314,12 @@ void stage_sort(sp_ctx* c, VDev& v) {
   if (!v.keys_valid) {
     ProfScope prof(c, kProfKeys);
     launch_build_keys(v.d_meta_canon, static_cast<int>(v.tables.size()), c->B, v.d_off,
-                      v.d_idx, v.d_keys, v.d_bags, c->stream);
+                      v.d_idx, v.d_keys, v.d_bags, c->bags16, c->stream);
     v.keys_valid = true;
   }
   ProfScope prof(c, kProfSort);
-  sort_pairs(c->d_temp, c->temp_bytes, v.d_keys, c->d_kb, v.d_bags, c->d_bb, v.nnz,
-             v.end_bit, c->stream);
+  sort_pairs(c->d_temp, c->temp_bytes, v.d_keys, c->d_kb, v.d_bags, c->d_bb, c->bags16,
+             v.nnz, v.end_bit, c->stream);
 }
 
 // Bucketed backward (bwd.cu): partition pairs into row buckets, then one
@@ -347,7 +348,7 @@ void stage_backward(sp_ctx* c, VDev& v) {
   stage_sort(c, v);
   ProfScope prof(c, kProfSgd);
   launch_sgd(v.d_meta_canon, v.d_rb_end, static_cast<int>(v.tables.size()), c->d_kb,
-             c->d_bb, v.nnz, v.d_grad, v.W, c->lr, c->d_w, c->stream);
+             c->d_bb, c->bags16, v.nnz, v.d_grad, v.W, c->lr, c->d_w, c->stream);
 }
 
 bool nccl_mode(const sp_ctx* c) { return c->world > 1; }
@@ -514,6 +515,7 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
     c->world = world_size;
     c->rank = rank;
     c->B = batch_size;
+    c->bags16 = batch_size <= 65536;
     c->lr = lr;
     c->cap = mem_cap_gb;
     c->device = cuda_device;
@@ -1083,7 +1085,17 @@ int sp_get_sorted(sp_ctx* ctx, int32_t dev, uint32_t* keys, uint32_t* bags,
                    ctx->stream);
       SP_CUDA(cudaMemcpyAsync(&nseg, ctx->d_nseg, 4, cudaMemcpyDeviceToHost, ctx->stream));
       if (keys) SP_CUDA(cudaMemcpyAsync(keys, ctx->d_kb, v.nnz * 4, cudaMemcpyDeviceToHost, ctx->stream));
-      if (bags) SP_CUDA(cudaMemcpyAsync(bags, ctx->d_bb, v.nnz * 4, cudaMemcpyDeviceToHost, ctx->stream));
+      std::vector<uint16_t> b16;
+      const bool narrow = ctx->bags16 && !v.bucketed;  // CUB path sorts 16-bit bags
+      if (bags && narrow) {
+        b16.resize(v.nnz);
+        SP_CUDA(cudaMemcpyAsync(b16.data(), ctx->d_bb, v.nnz * 2, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+      } else if (bags) {
+        SP_CUDA(cudaMemcpyAsync(bags, ctx->d_bb, v.nnz * 4, cudaMemcpyDeviceToHost, ctx->stream));
+      }
+      SP_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (bags && narrow) std::copy(b16.begin(), b16.end(), bags);
       SP_CUDA(cudaStreamSynchronize(ctx->stream));
       if (seg_heads && nseg)
         SP_CUDA(cudaMemcpy(seg_heads, ctx->d_seg, static_cast<int64_t>(nseg) * 4, cudaMemcpyDeviceToHost));
@@ -1303,7 +1315,8 @@ int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]) {
       const double csr = offs + 4.0 * v.nnz;
       const double outb = 4.0 * c->B * v.W;
       const bool emit = c->fuse_keys && !v.bucketed;
-      fwd = std::max(fwd, csr + rows_bytes + outb + (emit ? 8.0 * v.nnz : 0.0));
+      const double pair = c->bags16 ? 6.0 : 8.0;  // sort key + bag payload bytes
+      fwd = std::max(fwd, csr + rows_bytes + outb + (emit ? pair * v.nnz : 0.0));
       a2a = std::max(a2a, 4.0 * c->B * v.W * (c->D - 1) / c->D);
       double uniq_dim = 0;
       if (v.nnz) {
@@ -1326,11 +1339,11 @@ int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]) {
           uniq_dim += c->tables[v.tables[li]].dim;
         }
       }
-      sgd = std::max(sgd, outb + 8.0 * uniq_dim + (v.bucketed ? 12.0 : 8.0) * v.nnz);
+      sgd = std::max(sgd, outb + 8.0 * uniq_dim + (v.bucketed ? 12.0 : pair) * v.nnz);
       if (v.bucketed)
         sort = std::max(sort, 2.0 * csr + 8.0 * v.nnz + 8.0 * v.n_cnt);
       else
-        sort = std::max(sort, 16.0 * v.nnz * ((v.end_bit + 7) / 8));
+        sort = std::max(sort, 2.0 * pair * v.nnz * ((v.end_bit + 7) / 8));
     }
     out[0] = fwd;
     out[1] = a2a;

@@ -196,7 +196,9 @@ __device__ __forceinline__ void fwd_tile_warp_generic(
   }
 }
 
-template <bool kEmitKeys>
+// BagT: the sort payload — uint16_t when the batch fits 16 bits (6-byte
+// pairs through the radix sort instead of 8), else uint32_t.
+template <bool kEmitKeys, class BagT>
 __global__ void __launch_bounds__(kBlockThreads)
     tbe_forward_kernel(const TableMeta* __restrict__ meta,
                        const FwdTile* __restrict__ tiles, int batch,
@@ -204,7 +206,7 @@ __global__ void __launch_bounds__(kBlockThreads)
                        const int32_t* __restrict__ idx,
                        const float* __restrict__ w, float* __restrict__ out,
                        int64_t ldo, uint32_t* __restrict__ keys,
-                       uint32_t* __restrict__ bags) {
+                       BagT* __restrict__ bags) {
   __shared__ int32_t s_off[kTileBags + 1];
   __shared__ int32_t s_idx[kIdxCap];
   const FwdTile tile = tiles[blockIdx.x];
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(kBlockThreads)
         if (s_off[mid] <= p0 + i) lo = mid; else hi = mid - 1;
       }
       __stcs(keys + p0 + i, m.rowbase + static_cast<uint32_t>(v));
-      __stcs(bags + p0 + i, static_cast<uint32_t>(tile.b0 + lo));
+      bags[p0 + i] = static_cast<BagT>(tile.b0 + lo);
     }
   }
   __syncthreads();
@@ -253,11 +255,12 @@ __global__ void __launch_bounds__(kBlockThreads)
 // K4 step 1 (only when K1 did not emit them): keys[p] = rowbase + idx[p],
 // bags[p] = bag of p. A block takes 256 bags of one table.
 
+template <class BagT>
 __global__ void __launch_bounds__(kTileBags)
     build_keys_kernel(const TableMeta* __restrict__ meta, int batch,
                       int tiles_per_table, const int32_t* __restrict__ off,
                       const int32_t* __restrict__ idx,
-                      uint32_t* __restrict__ keys, uint32_t* __restrict__ bags) {
+                      uint32_t* __restrict__ keys, BagT* __restrict__ bags) {
   __shared__ int32_t s_off[kTileBags + 1];
   const int t = blockIdx.x / tiles_per_table;
   const int tile = blockIdx.x % tiles_per_table;
@@ -275,7 +278,7 @@ __global__ void __launch_bounds__(kTileBags)
       if (s_off[mid] <= p) lo = mid; else hi = mid - 1;
     }
     keys[p] = m.rowbase + static_cast<uint32_t>(__ldg(idx + p));
-    bags[p] = static_cast<uint32_t>(b0 + lo);
+    bags[p] = static_cast<BagT>(b0 + lo);
   }
 }
 
@@ -327,18 +330,19 @@ __device__ __forceinline__ uint32_t pos_key(const SgdShared& sh, int i, int np,
   return i < np ? sh.key[i] : __ldg(keys + p0 + i);
 }
 
+template <class BagT>
 __device__ __forceinline__ uint32_t pos_bag(const SgdShared& sh, int i, int np,
                                             int64_t p0,
-                                            const uint32_t* __restrict__ bags) {
-  return i < np ? sh.bag[i] : __ldg(bags + p0 + i);
+                                            const BagT* __restrict__ bags) {
+  return i < np ? sh.bag[i] : static_cast<uint32_t>(__ldg(bags + p0 + i));
 }
 
 // One round: runs [j, j+P) of the tile's head list that belong to table m.
-template <class G>
+template <class G, class BagT>
 __device__ __forceinline__ int sgd_round(const TableMeta& m, uint32_t rb_end,
                                          int j, int jend, int np, int64_t p0,
                                          int lane, const SgdShared& sh,
-                                         const uint32_t* __restrict__ bags,
+                                         const BagT* __restrict__ bags,
                                          const float* __restrict__ grad,
                                          int64_t ldg, float lr,
                                          float* __restrict__ w) {
@@ -418,9 +422,10 @@ __device__ __forceinline__ int sgd_round(const TableMeta& m, uint32_t rb_end,
   return nvalid;
 }
 
+template <class BagT>
 __device__ __forceinline__ int sgd_round_generic(
     const TableMeta& m, int j, int np, int64_t p0, int lane, const SgdShared& sh,
-    const uint32_t* __restrict__ bags, const float* __restrict__ grad, int64_t ldg,
+    const BagT* __restrict__ bags, const float* __restrict__ grad, int64_t ldg,
     float lr, float* __restrict__ w) {
   const int beg = sh.head[j];
   const int end = j + 1 < sh.nhead ? sh.head[j + 1] : sh.last_end;
@@ -443,11 +448,12 @@ __device__ __forceinline__ int sgd_round_generic(
 #ifndef SP_SGD_MIN_BLOCKS
 #define SP_SGD_MIN_BLOCKS 4  // 4 x 256 threads per SM: <= 64 registers
 #endif
+template <class BagT>
 __global__ void __launch_bounds__(kBlockThreads, SP_SGD_MIN_BLOCKS)
     sgd_kernel(const TableMeta* __restrict__ meta,
                const uint32_t* __restrict__ rb_end_g, int n_tables,
                const uint32_t* __restrict__ keys,
-               const uint32_t* __restrict__ bags, int64_t n,
+               const BagT* __restrict__ bags, int64_t n,
                const float* __restrict__ grad, int64_t ldg, float lr,
                float* __restrict__ w) {
   __shared__ SgdShared sh;
@@ -528,10 +534,10 @@ __global__ void __launch_bounds__(kBlockThreads, SP_SGD_MIN_BLOCKS)
       switch (m.cls) {
 #define SP_SGD_CASE(C)                                                           \
   case C:                                                                        \
-    j += lng ? sgd_round<LongGeo<C>>(m, re, j, j + 1, np, p0, lane, sh, bags,    \
-                                     grad, ldg, lr, w)                           \
-             : sgd_round<SgdGeo<C>>(m, re, j, jend, np, p0, lane, sh, bags, grad, \
-                                    ldg, lr, w);                                 \
+    j += lng ? sgd_round<LongGeo<C>, BagT>(m, re, j, j + 1, np, p0, lane, sh,    \
+                                           bags, grad, ldg, lr, w)               \
+             : sgd_round<SgdGeo<C>, BagT>(m, re, j, jend, np, p0, lane, sh, bags, \
+                                          grad, ldg, lr, w);                     \
     break;
         SP_SGD_CASE(0)
         SP_SGD_CASE(1)
@@ -653,35 +659,51 @@ std::vector<int4> make_fwd_tiles(const std::vector<TableMeta>& canon,
 void launch_tbe_forward(const TableMeta* d_meta_canon, const int4* d_tiles,
                         int64_t n_tiles, int batch, const int32_t* d_off,
                         const int32_t* d_idx, const float* d_w, float* d_out,
-                        int64_t ldo, uint32_t* d_keys, uint32_t* d_bags,
+                        int64_t ldo, uint32_t* d_keys, void* d_bags, bool bags16,
                         cudaStream_t st) {
   if (n_tiles <= 0) return;
   const FwdTile* tiles = reinterpret_cast<const FwdTile*>(d_tiles);
-  if (d_keys)
-    tbe_forward_kernel<true><<<static_cast<unsigned>(n_tiles), kBlockThreads, 0, st>>>(
-        d_meta_canon, tiles, batch, d_off, d_idx, d_w, d_out, ldo, d_keys, d_bags);
-  else
-    tbe_forward_kernel<false><<<static_cast<unsigned>(n_tiles), kBlockThreads, 0, st>>>(
+  const unsigned g = static_cast<unsigned>(n_tiles);
+  if (!d_keys)
+    tbe_forward_kernel<false, uint32_t><<<g, kBlockThreads, 0, st>>>(
         d_meta_canon, tiles, batch, d_off, d_idx, d_w, d_out, ldo, nullptr, nullptr);
+  else if (bags16)
+    tbe_forward_kernel<true, uint16_t><<<g, kBlockThreads, 0, st>>>(
+        d_meta_canon, tiles, batch, d_off, d_idx, d_w, d_out, ldo, d_keys,
+        static_cast<uint16_t*>(d_bags));
+  else
+    tbe_forward_kernel<true, uint32_t><<<g, kBlockThreads, 0, st>>>(
+        d_meta_canon, tiles, batch, d_off, d_idx, d_w, d_out, ldo, d_keys,
+        static_cast<uint32_t*>(d_bags));
   SP_LAUNCHED();
 }
 
 void launch_build_keys(const TableMeta* d_meta_canon, int n_tables, int batch,
                        const int32_t* d_off, const int32_t* d_idx,
-                       uint32_t* d_keys, uint32_t* d_bags, cudaStream_t st) {
+                       uint32_t* d_keys, void* d_bags, bool bags16, cudaStream_t st) {
   if (n_tables <= 0) return;
   const int tiles = (batch + kTileBags - 1) / kTileBags;
-  build_keys_kernel<<<n_tables * tiles, kTileBags, 0, st>>>(
-      d_meta_canon, batch, tiles, d_off, d_idx, d_keys, d_bags);
+  if (bags16)
+    build_keys_kernel<uint16_t><<<n_tables * tiles, kTileBags, 0, st>>>(
+        d_meta_canon, batch, tiles, d_off, d_idx, d_keys, static_cast<uint16_t*>(d_bags));
+  else
+    build_keys_kernel<uint32_t><<<n_tables * tiles, kTileBags, 0, st>>>(
+        d_meta_canon, batch, tiles, d_off, d_idx, d_keys, static_cast<uint32_t*>(d_bags));
   SP_LAUNCHED();
 }
 
 size_t sort_pairs(void* temp, size_t temp_bytes, const uint32_t* keys_in,
-                  uint32_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
+                  uint32_t* keys_out, const void* vals_in, void* vals_out, bool bags16,
                   int64_t n, int end_bit, cudaStream_t st) {
   size_t bytes = temp_bytes;
-  SP_CUDA(cub::DeviceRadixSort::SortPairs(temp, bytes, keys_in, keys_out,
-                                          vals_in, vals_out, n, 0, end_bit, st));
+  if (bags16)
+    SP_CUDA(cub::DeviceRadixSort::SortPairs(temp, bytes, keys_in, keys_out,
+                                            static_cast<const uint16_t*>(vals_in),
+                                            static_cast<uint16_t*>(vals_out), n, 0, end_bit, st));
+  else
+    SP_CUDA(cub::DeviceRadixSort::SortPairs(temp, bytes, keys_in, keys_out,
+                                            static_cast<const uint32_t*>(vals_in),
+                                            static_cast<uint32_t*>(vals_out), n, 0, end_bit, st));
   return bytes;
 }
 
@@ -703,13 +725,19 @@ size_t exclusive_scan_i32(void* temp, size_t temp_bytes, const int32_t* in,
 }
 
 void launch_sgd(const TableMeta* d_meta_canon, const uint32_t* d_rowbase_end,
-                int n_tables, const uint32_t* d_keys, const uint32_t* d_bags,
+                int n_tables, const uint32_t* d_keys, const void* d_bags, bool bags16,
                 int64_t n, const float* d_grad, int64_t ldg, float lr, float* d_w,
                 cudaStream_t st) {
   if (n <= 0 || n_tables <= 0) return;
-  const int64_t blocks = (n + kTilePos - 1) / kTilePos;
-  sgd_kernel<<<static_cast<unsigned>(blocks), kBlockThreads, 0, st>>>(
-      d_meta_canon, d_rowbase_end, n_tables, d_keys, d_bags, n, d_grad, ldg, lr, d_w);
+  const unsigned blocks = static_cast<unsigned>((n + kTilePos - 1) / kTilePos);
+  if (bags16)
+    sgd_kernel<uint16_t><<<blocks, kBlockThreads, 0, st>>>(
+        d_meta_canon, d_rowbase_end, n_tables, d_keys, static_cast<const uint16_t*>(d_bags), n,
+        d_grad, ldg, lr, d_w);
+  else
+    sgd_kernel<uint32_t><<<blocks, kBlockThreads, 0, st>>>(
+        d_meta_canon, d_rowbase_end, n_tables, d_keys, static_cast<const uint32_t*>(d_bags), n,
+        d_grad, ldg, lr, d_w);
   SP_LAUNCHED();
 }
 

@@ -65,25 +65,26 @@ std::vector<int4> make_fwd_tiles(const std::vector<TableMeta>& canon,
 void launch_tbe_forward(const TableMeta* d_meta_canon, const int4* d_tiles,
                         int64_t n_tiles, int batch, const int32_t* d_off,
                         const int32_t* d_idx, const float* d_w, float* d_out,
-                        int64_t ldo, uint32_t* d_keys, uint32_t* d_bags,
+                        int64_t ldo, uint32_t* d_keys, void* d_bags, bool bags16,
                         cudaStream_t st);
 
 // ---- K4: backward = keys -> stable radix sort -> runs -> SGD -------------
 void launch_build_keys(const TableMeta* d_meta_canon, int n_tables, int batch,
                        const int32_t* d_off, const int32_t* d_idx,
-                       uint32_t* d_keys, uint32_t* d_bags, cudaStream_t st);
+                       uint32_t* d_keys, void* d_bags, bool bags16, cudaStream_t st);
 // Run heads of sorted keys (test/diagnostic path; the SGD kernel finds the
 // heads itself): seg[u] = first position of the u-th run, *d_nseg = runs.
 size_t select_heads(void* temp, size_t temp_bytes, const uint32_t* d_keys,
                     int64_t n, uint32_t* d_seg, int32_t* d_nseg,
                     cudaStream_t st);
+// vals are uint16_t (bags16: batch <= 65536) or uint32_t bag ids.
 size_t sort_pairs(void* temp, size_t temp_bytes, const uint32_t* keys_in,
-                  uint32_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
+                  uint32_t* keys_out, const void* vals_in, void* vals_out, bool bags16,
                   int64_t n, int end_bit, cudaStream_t st);
 // Row-wise SGD over the sorted pairs:
 // W[row] -= lr * sum_{k in run, sorted order} grad[bags[k], lcol..].
 void launch_sgd(const TableMeta* d_meta_canon, const uint32_t* d_rowbase_end,
-                int n_tables, const uint32_t* d_keys, const uint32_t* d_bags,
+                int n_tables, const uint32_t* d_keys, const void* d_bags, bool bags16,
                 int64_t n, const float* d_grad, int64_t ldg, float lr, float* d_w,
                 cudaStream_t st);
 
