@@ -47,8 +47,23 @@ T* dalloc(size_t n, std::vector<void*>& owned, uint64_t& bytes) {
   return static_cast<T*>(p);
 }
 
+// Consecutive local tables sorted together in the CUB backward: keys are
+// relative to the group (rowbase/rb_end of its tables are group-relative),
+// so a group of <= 2^24 rows needs three 8-bit radix passes instead of the
+// four a device-wide 26-bit key would.
+constexpr uint64_t kSortGroupRows = uint64_t(1) << 24;
+struct SortGroup {
+  int t0 = 0, t1 = 0;      // local tables [t0, t1)
+  int end_bit = 1;         // key bits
+  int64_t row_base = 0;    // device rows before the group (key offset)
+  int64_t p0 = 0, p1 = 0;  // positions of its lookups in the CSR
+};
+
 struct VDev {
   int vid = 0;
+  std::vector<SortGroup> groups;
+  int64_t* d_gstart = nullptr;  // [groups + 1] first position (last = nnz)
+  int32_t* d_gt0 = nullptr;     // [groups + 1] first local table (last = T)
   std::vector<int> tables;  // global ids, ascending
   std::vector<TableMeta> meta_canon;
   std::vector<uint32_t> rb_end;
@@ -318,8 +333,14 @@ void stage_sort(sp_ctx* c, VDev& v) {
     v.keys_valid = true;
   }
   ProfScope prof(c, kProfSort);
-  sort_pairs(c->d_temp, c->temp_bytes, v.d_keys, c->d_kb, v.d_bags, c->d_bb, c->bags16,
-             v.nnz, v.end_bit, c->stream);
+  const size_t bb = c->bags16 ? 2 : 4;
+  for (const SortGroup& g : v.groups) {
+    if (g.p1 == g.p0) continue;
+    sort_pairs(c->d_temp, c->temp_bytes, v.d_keys + g.p0, c->d_kb + g.p0,
+               reinterpret_cast<const char*>(v.d_bags) + g.p0 * bb,
+               reinterpret_cast<char*>(c->d_bb) + g.p0 * bb, c->bags16, g.p1 - g.p0, g.end_bit,
+               c->stream);
+  }
 }
 
 // Bucketed backward (bwd.cu): partition pairs into row buckets, then one
@@ -347,8 +368,9 @@ void stage_backward(sp_ctx* c, VDev& v) {
   }
   stage_sort(c, v);
   ProfScope prof(c, kProfSgd);
-  launch_sgd(v.d_meta_canon, v.d_rb_end, static_cast<int>(v.tables.size()), c->d_kb,
-             c->d_bb, c->bags16, v.nnz, v.d_grad, v.W, c->lr, c->d_w, c->stream);
+  launch_sgd(v.d_meta_canon, v.d_rb_end, static_cast<int>(v.tables.size()), v.d_gstart,
+             v.d_gt0, static_cast<int>(v.groups.size()), c->d_kb, c->d_bb, c->bags16, v.nnz,
+             v.d_grad, v.W, c->lr, c->d_w, c->stream);
 }
 
 bool nccl_mode(const sp_ctx* c) { return c->world > 1; }
@@ -438,6 +460,35 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 }  // namespace sp
 
 using namespace sp;
+
+namespace sp {
+namespace {
+// Runs this device's backward sort (no update) and returns the sorted keys
+// as device-wide keys (local row base + row); bags (optional) receives the
+// bag payload in sorted order.
+std::vector<uint32_t> sorted_keys_host(sp_ctx* c, VDev& v, uint32_t* bags) {
+  std::vector<uint32_t> keys(v.nnz);
+  if (v.nnz == 0) return keys;
+  if (v.bucketed) stage_backward_bucketed(c, v, c->d_kb, c->d_bb, false);
+  else stage_sort(c, v);
+  SP_CUDA(cudaMemcpyAsync(keys.data(), c->d_kb, v.nnz * 4, cudaMemcpyDeviceToHost, c->stream));
+  std::vector<uint16_t> b16;
+  const bool narrow = c->bags16 && !v.bucketed;  // the CUB path sorts 16-bit bags
+  if (bags && narrow) {
+    b16.resize(v.nnz);
+    SP_CUDA(cudaMemcpyAsync(b16.data(), c->d_bb, v.nnz * 2, cudaMemcpyDeviceToHost, c->stream));
+  } else if (bags) {
+    SP_CUDA(cudaMemcpyAsync(bags, c->d_bb, v.nnz * 4, cudaMemcpyDeviceToHost, c->stream));
+  }
+  SP_CUDA(cudaStreamSynchronize(c->stream));
+  if (bags && narrow) std::copy(b16.begin(), b16.end(), bags);
+  // keys are sort-group relative on the device
+  for (const SortGroup& g : v.groups)
+    for (int64_t p = g.p0; p < g.p1; ++p) keys[p] += static_cast<uint32_t>(g.row_base);
+  return keys;
+}
+}  // namespace
+}  // namespace sp
 
 extern "C" {
 
@@ -567,11 +618,33 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
       for (int i = 0; i < num_tables; ++i)
         if (placement[i] == d) v.tables.push_back(i);
       const int T = static_cast<int>(v.tables.size());
+      // greedy packing makes at most 2*ceil(rows/limit) groups: keep <= 30
+      uint64_t dev_rows = 0;
+      for (int g : v.tables) dev_rows += static_cast<uint64_t>(tables[g].hash_size);
+      uint64_t group_rows = kSortGroupRows;
+      while (2 * ((dev_rows + group_rows - 1) / group_rows) > 30) group_rows *= 2;
       int64_t lcol = 0;
-      uint64_t rb = 0;
+      uint64_t rb = 0;     // row base inside the current sort group
+      int64_t gbase = 0;   // rows of the device before the current group
+      int gstart = 0;
+      auto close_group = [&](int t1) {
+        SortGroup sg;
+        sg.t0 = gstart;
+        sg.t1 = t1;
+        sg.row_base = gbase;
+        sg.end_bit = 1;
+        while (sg.end_bit < 32 && (1ULL << sg.end_bit) < std::max<uint64_t>(rb, 2)) ++sg.end_bit;
+        v.groups.push_back(sg);
+        gbase += static_cast<int64_t>(rb);
+        rb = 0;
+        gstart = t1;
+      };
       for (int li = 0; li < T; ++li) {
         const int g = v.tables[li];
         const sp_table_spec& t = tables[g];
+        // sort groups of <= 2^24 rows: 24-bit keys, three radix passes
+        if (li > gstart && rb + static_cast<uint64_t>(t.hash_size) > group_rows)
+          close_group(li);
         TableMeta m{};
         m.woff = c->woff[g];
         m.rows = t.hash_size;
@@ -589,11 +662,21 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
           raise(SP_ERR_BAD_INPUT, "rows per device above 2^32 (32-bit sort keys)");
         v.rb_end.push_back(static_cast<uint32_t>(rb));
       }
+      if (T > 0) close_group(T);
+      {
+        std::vector<int32_t> gt0;
+        for (const SortGroup& sg : v.groups) gt0.push_back(sg.t0);
+        gt0.push_back(T);
+        v.d_gt0 = dalloc<int32_t>(gt0.size(), c->owned, c->dev_bytes);
+        v.d_gstart = dalloc<int64_t>(gt0.size(), c->owned, c->dev_bytes);
+        SP_CUDA(cudaMemcpy(v.d_gt0, gt0.data(), gt0.size() * sizeof(int32_t),
+                           cudaMemcpyHostToDevice));
+        SP_CUDA(cudaMemset(v.d_gstart, 0, gt0.size() * sizeof(int64_t)));
+      }
       v.W = lcol;
-      v.rows_total = static_cast<int64_t>(rb);
+      v.rows_total = gbase;
       v.end_bit = 1;
-      while (v.end_bit < 32 && (1ULL << v.end_bit) < static_cast<uint64_t>(std::max<int64_t>(v.rows_total, 2)))
-        ++v.end_bit;
+      for (const SortGroup& sg : v.groups) v.end_bit = std::max(v.end_bit, sg.end_bit);
       // K1 grid order: heaviest tables (pf * dim) first so the long blocks
       // start early (LPT), each table a contiguous block range.
       std::vector<int> order(T);
@@ -727,7 +810,21 @@ int sp_get_table(sp_ctx* ctx, int32_t table_id, float* rows) {
 
 static void finish_batch(sp_ctx* c) {
   int64_t max_nnz = 0;
-  for (auto& v : c->vdevs) max_nnz = std::max(max_nnz, v.nnz);
+  for (auto& v : c->vdevs) {
+    max_nnz = std::max(max_nnz, v.nnz);
+    int64_t p = 0;  // positions of each sort group in the device CSR
+    std::vector<int64_t> gs;
+    for (SortGroup& g : v.groups) {
+      g.p0 = p;
+      gs.push_back(p);
+      for (int t = g.t0; t < g.t1; ++t) p += v.table_nnz[t];
+      g.p1 = p;
+    }
+    gs.push_back(p);
+    if (v.d_gstart)
+      SP_CUDA(cudaMemcpy(v.d_gstart, gs.data(), gs.size() * sizeof(int64_t),
+                         cudaMemcpyHostToDevice));
+  }
   ensure_sort_capacity(c, max_nnz);
   plan_buckets(c);
   c->has_batch = true;
@@ -1077,29 +1174,14 @@ int sp_get_sorted(sp_ctx* ctx, int32_t dev, uint32_t* keys, uint32_t* bags,
     check_ctx(ctx);
     require_batch(ctx);
     VDev& v = vdev_for(ctx, dev);
-    int32_t nseg = 0;
-    if (v.nnz > 0) {
-      if (v.bucketed) stage_backward_bucketed(ctx, v, ctx->d_kb, ctx->d_bb, false);
-      else stage_sort(ctx, v);
-      select_heads(ctx->d_temp, ctx->temp_bytes, ctx->d_kb, v.nnz, ctx->d_seg, ctx->d_nseg,
-                   ctx->stream);
-      SP_CUDA(cudaMemcpyAsync(&nseg, ctx->d_nseg, 4, cudaMemcpyDeviceToHost, ctx->stream));
-      if (keys) SP_CUDA(cudaMemcpyAsync(keys, ctx->d_kb, v.nnz * 4, cudaMemcpyDeviceToHost, ctx->stream));
-      std::vector<uint16_t> b16;
-      const bool narrow = ctx->bags16 && !v.bucketed;  // CUB path sorts 16-bit bags
-      if (bags && narrow) {
-        b16.resize(v.nnz);
-        SP_CUDA(cudaMemcpyAsync(b16.data(), ctx->d_bb, v.nnz * 2, cudaMemcpyDeviceToHost,
-                                ctx->stream));
-      } else if (bags) {
-        SP_CUDA(cudaMemcpyAsync(bags, ctx->d_bb, v.nnz * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    std::vector<uint32_t> k = sorted_keys_host(ctx, v, bags);
+    int64_t nseg = 0;
+    for (int64_t p = 0; p < static_cast<int64_t>(k.size()); ++p)
+      if (p == 0 || k[p] != k[p - 1]) {
+        if (seg_heads) seg_heads[nseg] = static_cast<uint32_t>(p);
+        ++nseg;
       }
-      SP_CUDA(cudaStreamSynchronize(ctx->stream));
-      if (bags && narrow) std::copy(b16.begin(), b16.end(), bags);
-      SP_CUDA(cudaStreamSynchronize(ctx->stream));
-      if (seg_heads && nseg)
-        SP_CUDA(cudaMemcpy(seg_heads, ctx->d_seg, static_cast<int64_t>(nseg) * 4, cudaMemcpyDeviceToHost));
-    }
+    if (keys) std::copy(k.begin(), k.end(), keys);
     if (n_keys) *n_keys = v.nnz;
     if (n_unique) *n_unique = nseg;
   });
@@ -1319,31 +1401,26 @@ int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]) {
       fwd = std::max(fwd, csr + rows_bytes + outb + (emit ? pair * v.nnz : 0.0));
       a2a = std::max(a2a, 4.0 * c->B * v.W * (c->D - 1) / c->D);
       double uniq_dim = 0;
-      if (v.nnz) {
-        if (v.bucketed) stage_backward_bucketed(c, v, c->d_kb, c->d_bb, false);
-        else stage_sort(c, v);
-        select_heads(c->d_temp, c->temp_bytes, c->d_kb, v.nnz, c->d_seg, c->d_nseg, c->stream);
-        int32_t nseg = 0;
-        std::vector<uint32_t> keys(v.nnz), heads;
-        SP_CUDA(cudaMemcpyAsync(&nseg, c->d_nseg, 4, cudaMemcpyDeviceToHost, c->stream));
-        SP_CUDA(cudaMemcpyAsync(keys.data(), c->d_kb, v.nnz * 4, cudaMemcpyDeviceToHost, c->stream));
-        SP_CUDA(cudaStreamSynchronize(c->stream));
-        heads.resize(nseg);
-        if (nseg)
-          SP_CUDA(cudaMemcpy(heads.data(), c->d_seg, static_cast<int64_t>(nseg) * 4,
-                             cudaMemcpyDeviceToHost));
-        for (int32_t u = 0; u < nseg; ++u) {
-          const uint32_t key = keys[heads[u]];
-          const int li = static_cast<int>(
-              std::upper_bound(v.rb_end.begin(), v.rb_end.end(), key) - v.rb_end.begin());
-          uniq_dim += c->tables[v.tables[li]].dim;
-        }
+      {
+        const std::vector<uint32_t> keys = sorted_keys_host(c, v, nullptr);
+        std::vector<uint64_t> row_end;  // device-wide end row of each local table
+        for (const SortGroup& g : v.groups)
+          for (int t = g.t0; t < g.t1; ++t) row_end.push_back(g.row_base + v.rb_end[t]);
+        for (size_t p = 0; p < keys.size(); ++p)
+          if (p == 0 || keys[p] != keys[p - 1]) {
+            const int li = static_cast<int>(
+                std::upper_bound(row_end.begin(), row_end.end(), keys[p]) - row_end.begin());
+            uniq_dim += c->tables[v.tables[li]].dim;
+          }
       }
       sgd = std::max(sgd, outb + 8.0 * uniq_dim + (v.bucketed ? 12.0 : pair) * v.nnz);
+      double sort_dev = 0;
       if (v.bucketed)
-        sort = std::max(sort, 2.0 * csr + 8.0 * v.nnz + 8.0 * v.n_cnt);
+        sort_dev = 2.0 * csr + 8.0 * v.nnz + 8.0 * v.n_cnt;
       else
-        sort = std::max(sort, 2.0 * pair * v.nnz * ((v.end_bit + 7) / 8));
+        for (const SortGroup& g : v.groups)
+          sort_dev += 2.0 * pair * (g.p1 - g.p0) * ((g.end_bit + 7) / 8);
+      sort = std::max(sort, sort_dev);
     }
     out[0] = fwd;
     out[1] = a2a;

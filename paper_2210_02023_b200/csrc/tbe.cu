@@ -309,10 +309,26 @@ struct SgdShared {
   uint32_t bag[kTilePos];
   uint16_t head[kTilePos + 1];
   uint32_t rb_end[kMaxSmemTables];
+  int64_t gstart[kMaxSortGroups + 1];  // sort groups: first position
+  int32_t gt0[kMaxSortGroups + 1];     //              first local table
+  int ngroups;
   int nhead;
   int last_end;  // end (tile-relative) of the last run
   int next;      // next unclaimed run
 };
+
+// Keys are relative to their sort group; a group start always begins a run.
+__device__ __forceinline__ bool is_group_start(const SgdShared& sh, int64_t p) {
+  for (int g = 1; g < sh.ngroups; ++g)
+    if (sh.gstart[g] == p) return true;
+  return false;
+}
+
+__device__ __forceinline__ int group_of(const SgdShared& sh, int64_t p) {
+  int g = 0;
+  while (g + 1 < sh.ngroups && sh.gstart[g + 1] <= p) ++g;
+  return g;
+}
 
 __device__ __forceinline__ int table_of_key(const uint32_t* rb_end, int n_tables,
                                             uint32_t key) {
@@ -339,7 +355,7 @@ __device__ __forceinline__ uint32_t pos_bag(const SgdShared& sh, int i, int np,
 
 // One round: runs [j, j+P) of the tile's head list that belong to table m.
 template <class G, class BagT>
-__device__ __forceinline__ int sgd_round(const TableMeta& m, uint32_t rb_end,
+__device__ __forceinline__ int sgd_round(const TableMeta& m, uint32_t rb_end, int gend,
                                          int j, int jend, int np, int64_t p0,
                                          int lane, const SgdShared& sh,
                                          const BagT* __restrict__ bags,
@@ -357,8 +373,9 @@ __device__ __forceinline__ int sgd_round(const TableMeta& m, uint32_t rb_end,
     beg = sh.head[u];
     end = u + 1 < sh.nhead ? sh.head[u + 1] : sh.last_end;
     key = sh.key[beg];
-    // same table; a long run (other than the first) gets its own round
-    valid = key < rb_end && (span == 0 || end - beg < kLongRun);
+    // same table (and sort group); a long run (other than the first) gets
+    // its own round
+    valid = key < rb_end && beg < gend && (span == 0 || end - beg < kLongRun);
   }
   const unsigned bal = __ballot_sync(0xffffffffu, valid && ls == 0);
   // spans must be a contiguous prefix of valid runs
@@ -452,7 +469,8 @@ template <class BagT>
 __global__ void __launch_bounds__(kBlockThreads, SP_SGD_MIN_BLOCKS)
     sgd_kernel(const TableMeta* __restrict__ meta,
                const uint32_t* __restrict__ rb_end_g, int n_tables,
-               const uint32_t* __restrict__ keys,
+               const int64_t* __restrict__ gstart_g, const int32_t* __restrict__ gt0_g,
+               int n_groups, const uint32_t* __restrict__ keys,
                const BagT* __restrict__ bags, int64_t n,
                const float* __restrict__ grad, int64_t ldg, float lr,
                float* __restrict__ w) {
@@ -469,6 +487,11 @@ __global__ void __launch_bounds__(kBlockThreads, SP_SGD_MIN_BLOCKS)
   const bool rb_in_smem = n_tables <= kMaxSmemTables;
   if (rb_in_smem)
     for (int i = tid; i < n_tables; i += kBlockThreads) sh.rb_end[i] = rb_end_g[i];
+  if (tid <= n_groups) {
+    sh.gstart[tid] = gstart_g[tid];
+    sh.gt0[tid] = gt0_g[tid];
+  }
+  if (tid == 0) sh.ngroups = n_groups;
   const uint32_t prev = p0 > 0 ? __ldg(keys + p0 - 1) : 0xffffffffu;
   __syncthreads();
   // run heads of the tile (tile-relative positions), in order
@@ -478,7 +501,9 @@ __global__ void __launch_bounds__(kBlockThreads, SP_SGD_MIN_BLOCKS)
   for (int q = 0; q < kPosPerThread; ++q) {
     const int i = tid * kPosPerThread + q;
     const uint32_t before = i == 0 ? prev : sh.key[i - 1];
-    flags[q] = (i < np && (sh.key[i] != before || (p0 == 0 && i == 0))) ? 1 : 0;
+    flags[q] = (i < np && (sh.key[i] != before || (p0 == 0 && i == 0) ||
+                           is_group_start(sh, p0 + i)))
+                   ? 1 : 0;
     cnt += flags[q];
   }
   int first = 0, total = 0;
@@ -498,7 +523,7 @@ __global__ void __launch_bounds__(kBlockThreads, SP_SGD_MIN_BLOCKS)
       const uint32_t last_key = sh.key[np - 1];
       for (int64_t base = p0 + np;; base += 32) {
         const int64_t p = base + tid;
-        const bool diff = p >= n || __ldg(keys + p) != last_key;
+        const bool diff = p >= n || __ldg(keys + p) != last_key || is_group_start(sh, p);
         const unsigned bal = __ballot_sync(0xffffffffu, diff);
         if (bal) {
           end = static_cast<int>(base - p0) + __ffs(bal) - 1;
@@ -527,17 +552,22 @@ __global__ void __launch_bounds__(kBlockThreads, SP_SGD_MIN_BLOCKS)
       const int beg = sh.head[j];
       const int len = (j + 1 < nh ? sh.head[j + 1] : sh.last_end) - beg;
       const uint32_t key0 = sh.key[beg];
-      const int t = table_of_key(rb, n_tables, key0);
+      const int grp = group_of(sh, p0 + beg);
+      const int gt = sh.gt0[grp];
+      const int t = gt + table_of_key(rb + gt, sh.gt0[grp + 1] - gt, key0);
       const TableMeta m = meta[t];
       const uint32_t re = rb[t];
+      // runs of this round stay in the group (keys restart at a group start)
+      const int gend = sh.gstart[grp + 1] - p0 < kTilePos + 1
+                           ? static_cast<int>(sh.gstart[grp + 1] - p0) : kTilePos + 1;
       const bool lng = len >= kLongRun;
       switch (m.cls) {
 #define SP_SGD_CASE(C)                                                           \
   case C:                                                                        \
-    j += lng ? sgd_round<LongGeo<C>, BagT>(m, re, j, j + 1, np, p0, lane, sh,    \
-                                           bags, grad, ldg, lr, w)               \
-             : sgd_round<SgdGeo<C>, BagT>(m, re, j, jend, np, p0, lane, sh, bags, \
-                                          grad, ldg, lr, w);                     \
+    j += lng ? sgd_round<LongGeo<C>, BagT>(m, re, gend, j, j + 1, np, p0, lane,  \
+                                           sh, bags, grad, ldg, lr, w)           \
+             : sgd_round<SgdGeo<C>, BagT>(m, re, gend, j, jend, np, p0, lane, sh, \
+                                          bags, grad, ldg, lr, w);               \
     break;
         SP_SGD_CASE(0)
         SP_SGD_CASE(1)
@@ -725,19 +755,21 @@ size_t exclusive_scan_i32(void* temp, size_t temp_bytes, const int32_t* in,
 }
 
 void launch_sgd(const TableMeta* d_meta_canon, const uint32_t* d_rowbase_end,
-                int n_tables, const uint32_t* d_keys, const void* d_bags, bool bags16,
+                int n_tables, const int64_t* d_gstart, const int32_t* d_gt0, int n_groups,
+                const uint32_t* d_keys, const void* d_bags, bool bags16,
                 int64_t n, const float* d_grad, int64_t ldg, float lr, float* d_w,
                 cudaStream_t st) {
   if (n <= 0 || n_tables <= 0) return;
+  if (n_groups > kMaxSortGroups) raise(SP_ERR_BAD_INPUT, "too many sort groups");
   const unsigned blocks = static_cast<unsigned>((n + kTilePos - 1) / kTilePos);
   if (bags16)
     sgd_kernel<uint16_t><<<blocks, kBlockThreads, 0, st>>>(
-        d_meta_canon, d_rowbase_end, n_tables, d_keys, static_cast<const uint16_t*>(d_bags), n,
-        d_grad, ldg, lr, d_w);
+        d_meta_canon, d_rowbase_end, n_tables, d_gstart, d_gt0, n_groups, d_keys,
+        static_cast<const uint16_t*>(d_bags), n, d_grad, ldg, lr, d_w);
   else
     sgd_kernel<uint32_t><<<blocks, kBlockThreads, 0, st>>>(
-        d_meta_canon, d_rowbase_end, n_tables, d_keys, static_cast<const uint32_t*>(d_bags), n,
-        d_grad, ldg, lr, d_w);
+        d_meta_canon, d_rowbase_end, n_tables, d_gstart, d_gt0, n_groups, d_keys,
+        static_cast<const uint32_t*>(d_bags), n, d_grad, ldg, lr, d_w);
   SP_LAUNCHED();
 }
 
