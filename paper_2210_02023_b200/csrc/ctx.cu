@@ -168,6 +168,12 @@ struct sp_ctx {
   int64_t stage_cap = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // H2D of uploaded batches
+  // The backward's sort depends only on the batch, not on the gradient: with
+  // one (virtual) device it runs on `side` concurrently with the forward and
+  // the exchanges (SP_OVERLAP=0 serialises it behind K1 again).
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool overlap_sort = true;
   std::vector<cudaEvent_t> upload_events;
   ncclComm_t comm = nullptr;
   double* d_bd = nullptr;      // breakdown gather buffer
@@ -205,6 +211,10 @@ struct sp_ctx {
     for (void* p : owned) cudaFree(p);
     if (comm) sp::nccl().CommDestroy(comm);
     if (copy_stream) cudaStreamSynchronize(copy_stream);
+    if (side) cudaStreamSynchronize(side);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
     for (auto& e : upload_events) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (stream) cudaStreamDestroy(stream);
@@ -220,6 +230,7 @@ int64_t rows_per_dst(const sp_ctx* c) { return c->B / c->D; }
 void ensure_sort_capacity(sp_ctx* c, int64_t n) {
   if (n <= c->sort_cap && c->d_temp) return;
   SP_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->side) SP_CUDA(cudaStreamSynchronize(c->side));
   for (void* p : c->sort_owned) cudaFree(p);
   c->sort_owned.clear();
   const int64_t cap = std::max<int64_t>(n, 1);
@@ -290,33 +301,42 @@ void require_batch(sp_ctx* c) {
 
 enum { kProfFwd = 0, kProfKeys = 1, kProfSort = 2, kProfSgd = 3, kProfExchange = 4 };
 
-size_t prof_event(sp_ctx* c) {
+size_t prof_event(sp_ctx* c, cudaStream_t st) {
   if (c->ev_used == c->ev_pool.size()) {
     cudaEvent_t e;
     SP_CUDA(cudaEventCreate(&e));
     c->ev_pool.push_back(e);
   }
-  SP_CUDA(cudaEventRecord(c->ev_pool[c->ev_used], c->stream));
+  SP_CUDA(cudaEventRecord(c->ev_pool[c->ev_used], st));
   return c->ev_used++;
 }
 
-// Records events around a stage launch when profiling is on.
+// Records events around a stage launch (on the stream it is launched on)
+// when profiling is on.
 struct ProfScope {
   sp_ctx* c;
   int cls;
+  cudaStream_t st;
   size_t a = 0;
-  ProfScope(sp_ctx* c_, int cls_) : c(c_), cls(cls_) {
-    if (c->profiling) a = prof_event(c);
+  ProfScope(sp_ctx* c_, int cls_, cudaStream_t st_ = nullptr)
+      : c(c_), cls(cls_), st(st_ ? st_ : c_->stream) {
+    if (c->profiling) a = prof_event(c, st);
   }
   ~ProfScope() noexcept(false) {
-    if (c->profiling) c->marks.push_back({cls, a, prof_event(c)});
+    if (c->profiling) c->marks.push_back({cls, a, prof_event(c, st)});
   }
 };
 
 // ---- stages ---------------------------------------------------------------
 
+// The sort runs on the side stream, concurrently with the forward.
+bool overlap_active(const sp_ctx* c) {
+  return c->overlap_sort && c->vdevs.size() == 1 && !c->vdevs[0].bucketed &&
+         c->vdevs[0].nnz > 0;
+}
+
 void stage_forward(sp_ctx* c, VDev& v) {
-  const bool emit = c->fuse_keys && !v.bucketed && v.nnz > 0;
+  const bool emit = c->fuse_keys && !v.bucketed && v.nnz > 0 && !overlap_active(c);
   ProfScope prof(c, kProfFwd);
   launch_tbe_forward(v.d_meta_canon, v.d_tiles, v.n_tiles, c->B, v.d_off, v.d_idx,
                      c->d_w, v.d_pooled, v.W, emit ? v.d_keys : nullptr,
@@ -325,21 +345,23 @@ void stage_forward(sp_ctx* c, VDev& v) {
 }
 
 // (keys) -> stable radix sort; leaves sorted keys in d_kb, bags in d_bb.
-void stage_sort(sp_ctx* c, VDev& v) {
-  if (!v.keys_valid) {
-    ProfScope prof(c, kProfKeys);
+// rebuild: derive the keys from the CSR even if K1 emitted them (the
+// overlapped sort does not wait for K1).
+void stage_sort(sp_ctx* c, VDev& v, cudaStream_t st, bool rebuild = false) {
+  if (!v.keys_valid || rebuild) {
+    ProfScope prof(c, kProfKeys, st);
     launch_build_keys(v.d_meta_canon, static_cast<int>(v.tables.size()), c->B, v.d_off,
-                      v.d_idx, v.d_keys, v.d_bags, c->bags16, c->stream);
+                      v.d_idx, v.d_keys, v.d_bags, c->bags16, st);
     v.keys_valid = true;
   }
-  ProfScope prof(c, kProfSort);
+  ProfScope prof(c, kProfSort, st);
   const size_t bb = c->bags16 ? 2 : 4;
   for (const SortGroup& g : v.groups) {
     if (g.p1 == g.p0) continue;
     sort_pairs(c->d_temp, c->temp_bytes, v.d_keys + g.p0, c->d_kb + g.p0,
                reinterpret_cast<const char*>(v.d_bags) + g.p0 * bb,
                reinterpret_cast<char*>(c->d_bb) + g.p0 * bb, c->bags16, g.p1 - g.p0, g.end_bit,
-               c->stream);
+               st);
   }
 }
 
@@ -360,13 +382,14 @@ void stage_backward_bucketed(sp_ctx* c, VDev& v, uint32_t* sorted_keys, uint32_t
                      do_sgd, c->stream);
 }
 
-void stage_backward(sp_ctx* c, VDev& v) {
+// sorted: the overlapped sort already ran (the caller joined its stream).
+void stage_backward(sp_ctx* c, VDev& v, bool sorted = false) {
   if (v.nnz == 0) return;
   if (v.bucketed) {
     stage_backward_bucketed(c, v, nullptr, nullptr, true);
     return;
   }
-  stage_sort(c, v);
+  if (!sorted) stage_sort(c, v, c->stream);
   ProfScope prof(c, kProfSgd);
   launch_sgd(v.d_meta_canon, v.d_rb_end, static_cast<int>(v.tables.size()), v.d_gstart,
              v.d_gt0, static_cast<int>(v.groups.size()), c->d_kb, c->d_bb, c->bags16, v.nnz,
@@ -435,7 +458,20 @@ void barrier(sp_ctx* c) {
 
 bool exchange_needed(const sp_ctx* c) { return c->D > 1; }
 
+// Fork: the side stream builds the sort keys from the CSR and sorts them
+// while the main stream runs the forward and the exchanges.
+void fork_sort(sp_ctx* c) {
+  SP_CUDA(cudaEventRecord(c->ev_fork, c->stream));
+  SP_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+  stage_sort(c, c->vdevs[0], c->side, /*rebuild=*/true);
+  SP_CUDA(cudaEventRecord(c->ev_join, c->side));
+}
+
+void join_sort(sp_ctx* c) { SP_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0)); }
+
 void enqueue_iteration(sp_ctx* c) {
+  const bool ov = overlap_active(c);
+  if (ov) fork_sort(c);
   for (auto& v : c->vdevs) stage_forward(c, v);
   if (exchange_needed(c)) {
     ProfScope prof(c, kProfExchange);
@@ -447,7 +483,8 @@ void enqueue_iteration(sp_ctx* c) {
       for (auto& v : c->vdevs) a2a_bwd_emulated(c, v);
     }
   }
-  for (auto& v : c->vdevs) stage_backward(c, v);
+  if (ov) join_sort(c);
+  for (auto& v : c->vdevs) stage_backward(c, v, ov);
 }
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
@@ -470,7 +507,7 @@ std::vector<uint32_t> sorted_keys_host(sp_ctx* c, VDev& v, uint32_t* bags) {
   std::vector<uint32_t> keys(v.nnz);
   if (v.nnz == 0) return keys;
   if (v.bucketed) stage_backward_bucketed(c, v, c->d_kb, c->d_bb, false);
-  else stage_sort(c, v);
+  else stage_sort(c, v, c->stream);
   SP_CUDA(cudaMemcpyAsync(keys.data(), c->d_kb, v.nnz * 4, cudaMemcpyDeviceToHost, c->stream));
   std::vector<uint16_t> b16;
   const bool narrow = c->bags16 && !v.bucketed;  // the CUB path sorts 16-bit bags
@@ -575,6 +612,15 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
     SP_CUDA(cudaSetDevice(cuda_device));
     SP_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     SP_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    {
+      // high priority: the sort's blocks are dispatched as K1's retire
+      // instead of queueing behind all of K1's blocks
+      int lo = 0, hi = 0;
+      SP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      SP_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi));
+    }
+    SP_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    SP_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
 
     // Columns: global table order; per-device widths.
     c->gcol.resize(num_tables);
@@ -727,6 +773,7 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
     for (auto& e : c->ev_a2a) SP_CUDA(cudaEventCreate(&e));
     if (const char* f = std::getenv("SP_FUSE_KEYS")) c->fuse_keys = std::atoi(f) != 0;
     if (const char* f = std::getenv("SP_BWD")) c->use_buckets = std::string(f) == "bucket";
+    if (const char* f = std::getenv("SP_OVERLAP")) c->overlap_sort = std::atoi(f) != 0;
 
     if (world_size > 1) {
       c->plan = make_plan(tables, num_tables, num_devices, placement, batch_size, rank);
@@ -1195,9 +1242,16 @@ int sp_run_iteration(sp_ctx* ctx, sp_breakdown* out) {
     cudaStream_t st = c->stream;
     const int D = c->D;
     std::vector<double> fwd(D, 0.0), bwd(D, 0.0), cf(D, 0.0), cb(D, 0.0);
+    // the input-only backward sort overlaps stages 1-3 (its tail, if any,
+    // lands in the bwd stage, which starts by joining it)
+    const bool ov = overlap_active(c);
+    if (ov) {
+      SP_CUDA(cudaEventRecord(c->vdevs[0].ev[0], st));
+      fork_sort(c);
+    }
     // stage 1: fwd compute per (virtual) device
     for (auto& v : c->vdevs) {
-      SP_CUDA(cudaEventRecord(v.ev[0], st));
+      if (!ov) SP_CUDA(cudaEventRecord(v.ev[0], st));
       stage_forward(c, v);
       SP_CUDA(cudaEventRecord(v.ev[1], st));
     }
@@ -1229,7 +1283,8 @@ int sp_run_iteration(sp_ctx* ctx, sp_breakdown* out) {
     // stage 4: bwd compute
     for (auto& v : c->vdevs) {
       SP_CUDA(cudaEventRecord(v.ev[6], st));
-      stage_backward(c, v);
+      if (ov) join_sort(c);
+      stage_backward(c, v, ov);
       SP_CUDA(cudaEventRecord(v.ev[7], st));
     }
     SP_CUDA(cudaStreamSynchronize(st));

@@ -49,6 +49,20 @@ __device__ __forceinline__ float4 ldg_f4_policy(const float* ptr, uint64_t pol) 
   return v;
 }
 
+#ifndef SP_SGD_RED  // 1: apply the row update as red.global.add.v4.f32 (no W load)
+#define SP_SGD_RED 1
+#endif
+// Vector reduction at L2: fire-and-forget, the SM never waits for the row
+// (each unique row has exactly one update per launch, so the result is
+// deterministic: W + fp32(-lr * sum), round-to-nearest at L2). Measured on
+// B200 at cfg3: SGD 2.51 -> 2.33 ms with the old geometry, and it frees the
+// registers that held the old row for more rows/positions in flight.
+__device__ __forceinline__ void red_add_f4(float* p, float4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
 __device__ __forceinline__ float4 shfl_xor_f4(float4 v, int m) {
   v.x = __shfl_xor_sync(0xffffffffu, v.x, m);
   v.y = __shfl_xor_sync(0xffffffffu, v.y, m);
@@ -82,14 +96,16 @@ template <int CLS> struct SgdGeo;
 #include SP_GEO_HEADER
 #endif
 #ifndef SP_SGD_G0
-// (L, V, P, U) per dim class; tuned on B200 at cfg3 (profiles/r01_notes.md):
-// short runs are mostly one position, so U = 1 and registers go to V/P.
+// (L, V, P, U) per dim class; tuned on B200 at cfg3 (profiles/r01_notes.md).
+// With the L2 reduction update no register holds the old row, so lanes take
+// 64 B of a row (V = 4) for dims >= 64 and every group keeps U = 2
+// positions in flight: SGD 2.33 -> 2.09 ms.
 #define SP_SGD_G0 1, 1, 16, 2
 #define SP_SGD_G1 2, 1, 16, 1
-#define SP_SGD_G2 2, 2, 16, 1
-#define SP_SGD_G3 4, 2, 8, 1
-#define SP_SGD_G4 8, 2, 4, 1
-#define SP_SGD_G5 16, 2, 2, 1
+#define SP_SGD_G2 2, 2, 16, 2
+#define SP_SGD_G3 4, 2, 8, 2
+#define SP_SGD_G4 4, 4, 8, 2
+#define SP_SGD_G5 8, 4, 4, 2
 #endif
 #ifndef SP_SGD_INTERLEAVE  // lane float4 slices: 1 interleaved (s, s+L, ..), 0 blocked
 #define SP_SGD_INTERLEAVE 1
@@ -396,7 +412,7 @@ __device__ __forceinline__ int sgd_round(const TableMeta& m, uint32_t rb_end, in
   if (active) {
     const int64_t row = static_cast<int64_t>(key - m.rowbase);
     wrow = w + m.woff + row * m.dim + 4 * kLane * sub;
-    if (g == 0)
+    if (g == 0 && !SP_SGD_RED)
 #pragma unroll
       for (int q = 0; q < V; ++q) wold[q] = *reinterpret_cast<const float4*>(wrow + 4 * kStep * q);
     const float* gcol = grad + m.lcol + 4 * kLane * sub;
@@ -429,6 +445,11 @@ __device__ __forceinline__ int sgd_round(const TableMeta& m, uint32_t rb_end, in
 #pragma unroll
     for (int c = 0; c < V; ++c) {
       float4 r;
+      if (SP_SGD_RED) {
+        r = make_float4(-lr * acc[c].x, -lr * acc[c].y, -lr * acc[c].z, -lr * acc[c].w);
+        red_add_f4(wrow + 4 * kStep * c, r);
+        continue;
+      }
       r.x = fmaf(-lr, acc[c].x, wold[c].x);
       r.y = fmaf(-lr, acc[c].y, wold[c].y);
       r.z = fmaf(-lr, acc[c].z, wold[c].z);
