@@ -71,6 +71,8 @@ struct VDev {
   int64_t W = 0, rows_total = 0, n_tiles = 0;
   int end_bit = 1;
   int4* d_tiles = nullptr;      // K1 tiles in launch order
+  int* d_sgd_tiles = nullptr;   // K4 SGD tiles of the current batch
+  int64_t n_sgd_tiles = 0, sgd_tile_cap = 0;
   uint32_t* d_keys = nullptr;   // backward sort pairs (written by K1)
   uint32_t* d_bags = nullptr;
   bool keys_valid = false;
@@ -203,7 +205,7 @@ struct sp_ctx {
     for (auto& e : ev_pool) cudaEventDestroy(e);
     for (auto& v : vdevs)
       for (void* p : {static_cast<void*>(v.d_idx), static_cast<void*>(v.d_keys),
-                       static_cast<void*>(v.d_bags)})
+                       static_cast<void*>(v.d_bags), static_cast<void*>(v.d_sgd_tiles)})
         if (p) cudaFree(p);
     if (d_stage64) cudaFree(d_stage64);
     for (void* p : bucket_owned) cudaFree(p);
@@ -391,8 +393,7 @@ void stage_backward(sp_ctx* c, VDev& v, bool sorted = false) {
   }
   if (!sorted) stage_sort(c, v, c->stream);
   ProfScope prof(c, kProfSgd);
-  launch_sgd(v.d_meta_canon, v.d_rb_end, static_cast<int>(v.tables.size()), v.d_gstart,
-             v.d_gt0, static_cast<int>(v.groups.size()), c->d_kb, c->d_bb, c->bags16, v.nnz,
+  launch_sgd(v.d_meta_canon, v.d_sgd_tiles, v.n_sgd_tiles, c->d_kb, c->d_bb, c->bags16,
              v.d_grad, v.W, c->lr, c->d_w, c->stream);
 }
 
@@ -870,6 +871,19 @@ static void finish_batch(sp_ctx* c) {
     gs.push_back(p);
     if (v.d_gstart)
       SP_CUDA(cudaMemcpy(v.d_gstart, gs.data(), gs.size() * sizeof(int64_t),
+                         cudaMemcpyHostToDevice));
+    const std::vector<int> tl = make_sgd_tiles(v.table_nnz);
+    v.n_sgd_tiles = static_cast<int64_t>(tl.size()) / kSgdTileInts;
+    if (static_cast<int64_t>(tl.size()) > v.sgd_tile_cap) {
+      SP_CUDA(cudaStreamSynchronize(c->stream));
+      if (c->side) SP_CUDA(cudaStreamSynchronize(c->side));
+      if (v.d_sgd_tiles) cudaFree(v.d_sgd_tiles);
+      v.d_sgd_tiles = nullptr;
+      SP_CUDA(cudaMalloc(&v.d_sgd_tiles, tl.size() * sizeof(int)));
+      v.sgd_tile_cap = static_cast<int64_t>(tl.size());
+    }
+    if (!tl.empty())
+      SP_CUDA(cudaMemcpy(v.d_sgd_tiles, tl.data(), tl.size() * sizeof(int),
                          cudaMemcpyHostToDevice));
   }
   ensure_sort_capacity(c, max_nnz);

@@ -306,122 +306,82 @@ struct HeadFlag {
 };
 
 // ---------------------------------------------------------------------------
-// K4 step 3: SGD over the sorted (key, bag) pairs. A block owns the run
-// heads inside its tile of kTilePos sorted positions (a run that starts in
-// the tile is finished by the tile's block even past the tile end; a run
-// that started earlier belongs to the previous tile). Keys/bags/heads are
-// staged in shared memory; warps take contiguous slices of the tile's runs
-// and process them in rounds of up to P runs of the same table.
+// K4 step 3: row-wise SGD over the sorted (key, bag) pairs.
+//
+// The sorted array keeps every table's lookups at the table's CSR position
+// range (the key = table row base + row, tables in order), so tiles of at
+// most kTilePos positions are cut per table on the host (SgdTile) and a
+// block is specialised once on its table's dim class. A block owns the runs
+// (unique rows) whose head lies in its tile; a run that reaches the tile end
+// is finished by the same block. Prologue: the tile's rows/bags are staged in
+// shared memory and one block scan splits the heads into
+//   short runs (< kLongRun positions): packed (beg, len) in 16 bits; warps
+//     claim chunks of them dynamically and take P at a time (one span each);
+//   long runs (hot rows): every warp of the block sums a fixed slice of the
+//     run, partial sums meet in shared memory in warp order (deterministic)
+//     and one warp applies the row update.
+// The update W[row] += -lr * sum is one L2 vector reduction per 16 B
+// (red.global.add.v4.f32): each unique row has exactly one writer per
+// launch, so it is deterministic, and no SM register waits for the old row.
 
 constexpr int kTilePos = 2048;
 constexpr int kPosPerThread = kTilePos / kBlockThreads;
-constexpr int kMaxSmemTables = 512;
+constexpr int kLongRun = 32;   // runs at least this long are block-cooperative
+constexpr int kRunChunk = 16;  // short runs claimed per warp at a time (>= max P)
+constexpr int kMaxLong = kTilePos / kLongRun + 1;
 
-constexpr int kRunChunk = 16;  // runs claimed per warp at a time (>= max P)
-constexpr int kLongRun = 32;   // runs at least this long get the whole warp
-
-struct SgdShared {
-  uint32_t key[kTilePos];
-  uint32_t bag[kTilePos];
-  uint16_t head[kTilePos + 1];
-  uint32_t rb_end[kMaxSmemTables];
-  int64_t gstart[kMaxSortGroups + 1];  // sort groups: first position
-  int32_t gt0[kMaxSortGroups + 1];     //              first local table
-  int ngroups;
-  int nhead;
-  int last_end;  // end (tile-relative) of the last run
-  int next;      // next unclaimed run
+struct SgdTile {
+  int32_t t;       // canonical local table
+  int32_t p0;      // first sorted position of the tile
+  int32_t np;      // positions in the tile
+  int32_t tstart;  // first position of the table
+  int32_t pend;    // one past the table's last position
+  int32_t pad[3];
 };
 
-// Keys are relative to their sort group; a group start always begins a run.
-__device__ __forceinline__ bool is_group_start(const SgdShared& sh, int64_t p) {
-  for (int g = 1; g < sh.ngroups; ++g)
-    if (sh.gstart[g] == p) return true;
-  return false;
-}
-
-__device__ __forceinline__ int group_of(const SgdShared& sh, int64_t p) {
-  int g = 0;
-  while (g + 1 < sh.ngroups && sh.gstart[g + 1] <= p) ++g;
-  return g;
-}
-
-__device__ __forceinline__ int table_of_key(const uint32_t* rb_end, int n_tables,
-                                            uint32_t key) {
-  int lo = 0, hi = n_tables - 1;  // first t with rb_end[t] > key
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (rb_end[mid] > key) hi = mid; else lo = mid + 1;
-  }
-  return lo;
-}
-
-__device__ __forceinline__ uint32_t pos_key(const SgdShared& sh, int i, int np,
-                                            int64_t p0,
-                                            const uint32_t* __restrict__ keys) {
-  return i < np ? sh.key[i] : __ldg(keys + p0 + i);
-}
+template <class BagT>
+struct SgdShared {
+  uint32_t row[kTilePos];
+  BagT bag[kTilePos];
+  uint16_t srun[kTilePos];      // short runs: beg | len << 11
+  uint16_t lbeg[kMaxLong];      // long runs: first position (tile-relative)
+  int32_t lend[kMaxLong];       //            one past the last (may pass np)
+  alignas(16) float part[kWarpsPerBlock][128];
+  int nshort, nlong, next;
+};
 
 template <class BagT>
-__device__ __forceinline__ uint32_t pos_bag(const SgdShared& sh, int i, int np,
-                                            int64_t p0,
+__device__ __forceinline__ uint32_t sgd_bag(const SgdShared<BagT>& sh, int i, int np, int p0,
                                             const BagT* __restrict__ bags) {
-  return i < np ? sh.bag[i] : static_cast<uint32_t>(__ldg(bags + p0 + i));
+  return i < np ? static_cast<uint32_t>(sh.bag[i]) : static_cast<uint32_t>(__ldg(bags + p0 + i));
 }
 
-// One round: runs [j, j+P) of the tile's head list that belong to table m.
+// One round of up to P short runs [j, jend) of the tile (span s: run j+s).
 template <class G, class BagT>
-__device__ __forceinline__ int sgd_round(const TableMeta& m, uint32_t rb_end, int gend,
-                                         int j, int jend, int np, int64_t p0,
-                                         int lane, const SgdShared& sh,
-                                         const BagT* __restrict__ bags,
-                                         const float* __restrict__ grad,
-                                         int64_t ldg, float lr,
-                                         float* __restrict__ w) {
-  constexpr int L = G::L, V = G::V, P = G::P, U = G::U, S = G::S, GB = G::GB;
+__device__ __forceinline__ void sgd_short_round(const TableMeta& m, int j, int jend, int np,
+                                                int p0, int lane, const SgdShared<BagT>& sh,
+                                                const BagT* __restrict__ bags,
+                                                const float* __restrict__ grad, int64_t ldg,
+                                                float lr, float* __restrict__ w) {
+  constexpr int L = G::L, V = G::V, U = G::U, S = G::S, GB = G::GB;
   const int span = lane / S, ls = lane % S, g = ls / L, sub = ls % L;
-  constexpr int kLane = SP_SGD_INTERLEAVE ? 1 : V, kStep = SP_SGD_INTERLEAVE ? L : 1;
   const int u = j + span;
-  bool valid = u < jend;
-  int beg = 0, end = 0;
-  uint32_t key = 0;
-  if (valid) {
-    beg = sh.head[u];
-    end = u + 1 < sh.nhead ? sh.head[u + 1] : sh.last_end;
-    key = sh.key[beg];
-    // same table (and sort group); a long run (other than the first) gets
-    // its own round
-    valid = key < rb_end && beg < gend && (span == 0 || end - beg < kLongRun);
-  }
-  const unsigned bal = __ballot_sync(0xffffffffu, valid && ls == 0);
-  // spans must be a contiguous prefix of valid runs
-  int nvalid = 0;
+  const bool active = u < jend;
+  float4 acc[V];
 #pragma unroll
-  for (int q = 0; q < P; ++q) {
-    if (!(bal & (1u << (q * S)))) break;
-    ++nvalid;
-  }
-  const bool active = span < nvalid;
-  float4 acc[V], wold[V];
-#pragma unroll
-  for (int q = 0; q < V; ++q) {
-    acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    wold[q] = acc[q];
-  }
-  float* wrow = nullptr;
+  for (int c = 0; c < V; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  int beg = 0;
   if (active) {
-    const int64_t row = static_cast<int64_t>(key - m.rowbase);
-    wrow = w + m.woff + row * m.dim + 4 * kLane * sub;
-    if (g == 0 && !SP_SGD_RED)
-#pragma unroll
-      for (int q = 0; q < V; ++q) wold[q] = *reinterpret_cast<const float4*>(wrow + 4 * kStep * q);
-    const float* gcol = grad + m.lcol + 4 * kLane * sub;
+    const uint32_t pk = sh.srun[u];
+    beg = static_cast<int>(pk & 2047u);
+    const int end = beg + static_cast<int>(pk >> 11);
+    const float* gcol = grad + m.lcol + 4 * sub;
     for (int k = beg + g; k < end; k += GB * U) {
       uint32_t bg[U];
 #pragma unroll
       for (int q = 0; q < U; ++q) {
         const int kk = k + q * GB;
-        bg[q] = kk < end ? pos_bag(sh, kk, np, p0, bags) : 0xffffffffu;
+        bg[q] = kk < end ? sgd_bag(sh, kk, np, p0, bags) : 0xffffffffu;
       }
       float4 v[U][V];
 #pragma unroll
@@ -429,7 +389,7 @@ __device__ __forceinline__ int sgd_round(const TableMeta& m, uint32_t rb_end, in
 #pragma unroll
         for (int c = 0; c < V; ++c)
           v[q][c] = bg[q] != 0xffffffffu
-                        ? ldg_f4(gcol + static_cast<int64_t>(bg[q]) * ldg + 4 * kStep * c)
+                        ? ldg_f4(gcol + static_cast<int64_t>(bg[q]) * ldg + 4 * L * c)
                         : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int q = 0; q < U; ++q)
@@ -442,45 +402,125 @@ __device__ __forceinline__ int sgd_round(const TableMeta& m, uint32_t rb_end, in
 #pragma unroll
     for (int c = 0; c < V; ++c) acc[c] = f4_add(acc[c], shfl_xor_f4(acc[c], o));
   if (active && g == 0) {
+    float* wrow = w + m.woff + static_cast<int64_t>(sh.row[beg]) * m.dim + 4 * sub;
 #pragma unroll
-    for (int c = 0; c < V; ++c) {
-      float4 r;
-      if (SP_SGD_RED) {
-        r = make_float4(-lr * acc[c].x, -lr * acc[c].y, -lr * acc[c].z, -lr * acc[c].w);
-        red_add_f4(wrow + 4 * kStep * c, r);
-        continue;
-      }
-      r.x = fmaf(-lr, acc[c].x, wold[c].x);
-      r.y = fmaf(-lr, acc[c].y, wold[c].y);
-      r.z = fmaf(-lr, acc[c].z, wold[c].z);
-      r.w = fmaf(-lr, acc[c].w, wold[c].w);
-      *reinterpret_cast<float4*>(wrow + 4 * kStep * c) = r;
-    }
+    for (int c = 0; c < V; ++c)
+      red_add_f4(wrow + 4 * L * c, make_float4(-lr * acc[c].x, -lr * acc[c].y,
+                                               -lr * acc[c].z, -lr * acc[c].w));
   }
-  return nvalid;
 }
 
-template <class BagT>
-__device__ __forceinline__ int sgd_round_generic(
-    const TableMeta& m, int j, int np, int64_t p0, int lane, const SgdShared& sh,
-    const BagT* __restrict__ bags, const float* __restrict__ grad, int64_t ldg,
-    float lr, float* __restrict__ w) {
-  const int beg = sh.head[j];
-  const int end = j + 1 < sh.nhead ? sh.head[j + 1] : sh.last_end;
-  const int64_t row = static_cast<int64_t>(sh.key[beg] - m.rowbase);
-  for (int c0 = 0; c0 < m.dim; c0 += 32) {
-    const int c = c0 + lane;
-    float acc = 0.f;
-    for (int k = beg; k < end; ++k) {
-      const uint32_t bg = pos_bag(sh, k, np, p0, bags);
-      if (c < m.dim) acc += __ldg(grad + static_cast<int64_t>(bg) * ldg + m.lcol + c);
+// Long run [beg, end): warp `warp` sums its fixed slice into part[warp].
+template <class G, class BagT>
+__device__ __forceinline__ void sgd_long_slice(const TableMeta& m, int beg, int end, int np,
+                                               int p0, int warp, int lane,
+                                               SgdShared<BagT>& sh,
+                                               const BagT* __restrict__ bags,
+                                               const float* __restrict__ grad, int64_t ldg) {
+  constexpr int L = G::L, V = G::V, U = G::U, GB = G::GB;
+  const int g = lane / L, sub = lane % L;
+  const int len = end - beg;
+  const int per = (len + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int s0 = beg + min(len, warp * per), s1 = beg + min(len, (warp + 1) * per);
+  float4 acc[V];
+#pragma unroll
+  for (int c = 0; c < V; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float* gcol = grad + m.lcol + 4 * sub;
+  for (int k = s0 + g; k < s1; k += GB * U) {
+    uint32_t bg[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int kk = k + q * GB;
+      bg[q] = kk < s1 ? sgd_bag(sh, kk, np, p0, bags) : 0xffffffffu;
     }
-    if (c < m.dim) {
-      float* p = w + m.woff + row * m.dim + c;
-      *p = fmaf(-lr, acc, *p);
+    float4 v[U][V];
+#pragma unroll
+    for (int q = 0; q < U; ++q)
+#pragma unroll
+      for (int c = 0; c < V; ++c)
+        v[q][c] = bg[q] != 0xffffffffu
+                      ? ldg_f4(gcol + static_cast<int64_t>(bg[q]) * ldg + 4 * L * c)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < U; ++q)
+#pragma unroll
+      for (int c = 0; c < V; ++c) acc[c] = f4_add(acc[c], v[q][c]);
+  }
+#pragma unroll
+  for (int o = L; o < 32; o <<= 1)
+#pragma unroll
+    for (int c = 0; c < V; ++c) acc[c] = f4_add(acc[c], shfl_xor_f4(acc[c], o));
+  if (g == 0)
+#pragma unroll
+    for (int c = 0; c < V; ++c)
+      *reinterpret_cast<float4*>(&sh.part[warp][4 * sub + 4 * L * c]) = acc[c];
+}
+
+// Short-run (SG) and long-run (LG) geometries of one dim class.
+template <class SG, class LG, class BagT>
+__device__ __forceinline__ void sgd_tile(const TableMeta& m, const SgdTile& tile,
+                                         SgdShared<BagT>& sh,
+                                         const BagT* __restrict__ bags,
+                                         const float* __restrict__ grad, int64_t ldg,
+                                         float lr, float* __restrict__ w) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int np = tile.np, p0 = tile.p0;
+  // long runs first: all warps cooperate, two barriers per run
+  for (int r = 0; r < sh.nlong; ++r) {
+    const int beg = sh.lbeg[r], end = sh.lend[r];
+    sgd_long_slice<LG>(m, beg, end, np, p0, warp, lane, sh, bags, grad, ldg);
+    __syncthreads();
+    if (warp == 0) {
+      float* wrow = w + m.woff + static_cast<int64_t>(sh.row[beg]) * m.dim;
+      for (int c = 4 * lane; c < m.dim; c += 128) {
+        float4 s = *reinterpret_cast<const float4*>(&sh.part[0][c]);
+#pragma unroll
+        for (int q = 1; q < kWarpsPerBlock; ++q)
+          s = f4_add(s, *reinterpret_cast<const float4*>(&sh.part[q][c]));
+        red_add_f4(wrow + c, make_float4(-lr * s.x, -lr * s.y, -lr * s.z, -lr * s.w));
+      }
+    }
+    __syncthreads();
+  }
+  // short runs: dynamic chunks, P per round
+  const int ns = sh.nshort;
+  for (;;) {
+    int j0 = 0;
+    if (lane == 0) j0 = atomicAdd(&sh.next, kRunChunk);
+    j0 = __shfl_sync(0xffffffffu, j0, 0);
+    if (j0 >= ns) break;
+    const int jend = min(ns, j0 + kRunChunk);
+    for (int j = j0; j < jend; j += SG::P)
+      sgd_short_round<SG>(m, j, jend, np, p0, lane, sh, bags, grad, ldg, lr, w);
+  }
+}
+
+// Any dim (not a power of two in 4..128): a warp per run, 32 columns at a
+// time, positions in sorted order.
+template <class BagT>
+__device__ void sgd_tile_generic(const TableMeta& m, const SgdTile& tile, SgdShared<BagT>& sh,
+                                 const BagT* __restrict__ bags, const float* __restrict__ grad,
+                                 int64_t ldg, float lr, float* __restrict__ w) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nrun = sh.nshort + sh.nlong;
+  for (int r = warp; r < nrun; r += kWarpsPerBlock) {
+    int beg, end;
+    if (r < sh.nshort) {
+      beg = sh.srun[r] & 2047;
+      end = beg + (sh.srun[r] >> 11);
+    } else {
+      beg = sh.lbeg[r - sh.nshort];
+      end = sh.lend[r - sh.nshort];
+    }
+    float* wrow = w + m.woff + static_cast<int64_t>(sh.row[beg]) * m.dim;
+    for (int c = lane; c < m.dim; c += 32) {
+      float acc = 0.f;
+      for (int k = beg; k < end; ++k)
+        acc += __ldg(grad + static_cast<int64_t>(sgd_bag(sh, k, tile.np, tile.p0, bags)) * ldg +
+                     m.lcol + c);
+      atomicAdd(wrow + c, -lr * acc);
     }
   }
-  return 1;
 }
 
 #ifndef SP_SGD_MIN_BLOCKS
@@ -488,119 +528,99 @@ __device__ __forceinline__ int sgd_round_generic(
 #endif
 template <class BagT>
 __global__ void __launch_bounds__(kBlockThreads, SP_SGD_MIN_BLOCKS)
-    sgd_kernel(const TableMeta* __restrict__ meta,
-               const uint32_t* __restrict__ rb_end_g, int n_tables,
-               const int64_t* __restrict__ gstart_g, const int32_t* __restrict__ gt0_g,
-               int n_groups, const uint32_t* __restrict__ keys,
-               const BagT* __restrict__ bags, int64_t n,
+    sgd_kernel(const TableMeta* __restrict__ meta, const SgdTile* __restrict__ tiles,
+               const uint32_t* __restrict__ keys, const BagT* __restrict__ bags,
                const float* __restrict__ grad, int64_t ldg, float lr,
                float* __restrict__ w) {
-  __shared__ SgdShared sh;
+  __shared__ SgdShared<BagT> sh;
   using BlockScan = cub::BlockScan<int, kBlockThreads>;
   __shared__ typename BlockScan::TempStorage scan_tmp;
-  const int64_t p0 = static_cast<int64_t>(blockIdx.x) * kTilePos;
-  const int np = n - p0 < kTilePos ? static_cast<int>(n - p0) : kTilePos;
-  const int tid = threadIdx.x;
+  const SgdTile tile = tiles[blockIdx.x];
+  const TableMeta m = meta[tile.t];
+  const int np = tile.np, p0 = tile.p0, tid = threadIdx.x;
   for (int i = tid; i < np; i += kBlockThreads) {
-    sh.key[i] = __ldg(keys + p0 + i);
+    sh.row[i] = __ldg(keys + p0 + i) - m.rowbase;
     sh.bag[i] = __ldg(bags + p0 + i);
   }
-  const bool rb_in_smem = n_tables <= kMaxSmemTables;
-  if (rb_in_smem)
-    for (int i = tid; i < n_tables; i += kBlockThreads) sh.rb_end[i] = rb_end_g[i];
-  if (tid <= n_groups) {
-    sh.gstart[tid] = gstart_g[tid];
-    sh.gt0[tid] = gt0_g[tid];
-  }
-  if (tid == 0) sh.ngroups = n_groups;
-  const uint32_t prev = p0 > 0 ? __ldg(keys + p0 - 1) : 0xffffffffu;
+  const uint32_t prev = p0 > tile.tstart ? __ldg(keys + p0 - 1) - m.rowbase : 0xffffffffu;
   __syncthreads();
-  // run heads of the tile (tile-relative positions), in order
-  int flags[kPosPerThread];
-  int cnt = 0;
+  // heads; a run is long iff the position kLongRun-1 ahead has the same row
+  // (sorted). Ends: short runs by a short scan, long runs by binary search.
+  int sbeg[kPosPerThread], send[kPosPerThread];
+  int ns = 0, nl = 0;
 #pragma unroll
   for (int q = 0; q < kPosPerThread; ++q) {
     const int i = tid * kPosPerThread + q;
-    const uint32_t before = i == 0 ? prev : sh.key[i - 1];
-    flags[q] = (i < np && (sh.key[i] != before || (p0 == 0 && i == 0) ||
-                           is_group_start(sh, p0 + i)))
-                   ? 1 : 0;
-    cnt += flags[q];
+    sbeg[q] = -1;
+    send[q] = 0;
+    if (i >= np) continue;
+    const uint32_t r = sh.row[i];
+    if (r == (i == 0 ? prev : sh.row[i - 1])) continue;
+    const int la = i + kLongRun - 1;
+    const bool lng = la < np ? sh.row[la] == r
+                             : (p0 + la < tile.pend && __ldg(keys + p0 + la) - m.rowbase == r);
+    int e;
+    if (!lng) {
+      e = i + 1;
+      while (e < np && sh.row[e] == r) ++e;
+      if (e == np)  // the run may continue past the tile (still short)
+        while (p0 + e < tile.pend && __ldg(keys + p0 + e) - m.rowbase == r) ++e;
+      ++ns;
+    } else {
+      // first position past i + kLongRun - 1 whose row differs
+      int lo = la + 1, hi = la + 1;
+      int64_t stepw = 1;
+      auto same = [&](int x) {
+        return x < np ? sh.row[x] == r
+                      : (p0 + x < tile.pend && __ldg(keys + p0 + x) - m.rowbase == r);
+      };
+      while (same(hi)) {  // gallop
+        lo = hi + 1;
+        hi = static_cast<int>(hi + stepw < tile.pend - p0 ? hi + stepw : tile.pend - p0);
+        stepw <<= 1;
+      }
+      while (lo < hi) {  // first x in [lo, hi] with !same(x)
+        const int mid = (lo + hi) >> 1;
+        if (same(mid)) lo = mid + 1; else hi = mid;
+      }
+      e = lo;
+      ++nl;
+    }
+    sbeg[q] = lng ? -2 - i : i;  // long marked negative
+    send[q] = e;
   }
   int first = 0, total = 0;
-  BlockScan(scan_tmp).ExclusiveSum(cnt, first, total);
+  BlockScan(scan_tmp).ExclusiveSum(ns | (nl << 16), first, total);
+  int fs = first & 0xffff, fl = first >> 16;
 #pragma unroll
-  for (int q = 0; q < kPosPerThread; ++q)
-    if (flags[q]) sh.head[first++] = static_cast<uint16_t>(tid * kPosPerThread + q);
+  for (int q = 0; q < kPosPerThread; ++q) {
+    if (sbeg[q] >= 0) {
+      sh.srun[fs++] = static_cast<uint16_t>(sbeg[q] | ((send[q] - sbeg[q]) << 11));
+    } else if (sbeg[q] <= -2) {
+      sh.lbeg[fl] = static_cast<uint16_t>(-2 - sbeg[q]);
+      sh.lend[fl++] = send[q];
+    }
+  }
   if (tid == 0) {
-    sh.nhead = total;
+    sh.nshort = total & 0xffff;
+    sh.nlong = total >> 16;
     sh.next = 0;
   }
-  // end of the last run: it may continue past the tile
-  if (tid < 32) {
-    int end = np;
-    if (total > 0 && p0 + np < n) {
-      // all lanes: scan forward until the key changes
-      const uint32_t last_key = sh.key[np - 1];
-      for (int64_t base = p0 + np;; base += 32) {
-        const int64_t p = base + tid;
-        const bool diff = p >= n || __ldg(keys + p) != last_key || is_group_start(sh, p);
-        const unsigned bal = __ballot_sync(0xffffffffu, diff);
-        if (bal) {
-          end = static_cast<int>(base - p0) + __ffs(bal) - 1;
-          break;
-        }
-      }
-    }
-    if (tid == 0) sh.last_end = end;
-  }
   __syncthreads();
-  const int nh = sh.nhead;
-  if (nh == 0) return;
-  const int lane = tid & 31;
-  const uint32_t* rb = rb_in_smem ? sh.rb_end : rb_end_g;
-  // Warps claim chunks of kRunChunk runs dynamically (hot rows make run
-  // lengths very uneven). Inside a chunk: short runs go P at a time, a long
-  // run gets the whole warp (all row groups, U rows each in flight).
-  for (;;) {
-    int j0 = 0;
-    if (lane == 0) j0 = atomicAdd(&sh.next, kRunChunk);
-    j0 = __shfl_sync(0xffffffffu, j0, 0);
-    if (j0 >= nh) break;
-    const int jend = min(nh, j0 + kRunChunk);
-    int j = j0;
-    while (j < jend) {
-      const int beg = sh.head[j];
-      const int len = (j + 1 < nh ? sh.head[j + 1] : sh.last_end) - beg;
-      const uint32_t key0 = sh.key[beg];
-      const int grp = group_of(sh, p0 + beg);
-      const int gt = sh.gt0[grp];
-      const int t = gt + table_of_key(rb + gt, sh.gt0[grp + 1] - gt, key0);
-      const TableMeta m = meta[t];
-      const uint32_t re = rb[t];
-      // runs of this round stay in the group (keys restart at a group start)
-      const int gend = sh.gstart[grp + 1] - p0 < kTilePos + 1
-                           ? static_cast<int>(sh.gstart[grp + 1] - p0) : kTilePos + 1;
-      const bool lng = len >= kLongRun;
-      switch (m.cls) {
-#define SP_SGD_CASE(C)                                                           \
-  case C:                                                                        \
-    j += lng ? sgd_round<LongGeo<C>, BagT>(m, re, gend, j, j + 1, np, p0, lane,  \
-                                           sh, bags, grad, ldg, lr, w)           \
-             : sgd_round<SgdGeo<C>, BagT>(m, re, gend, j, jend, np, p0, lane, sh, \
-                                          bags, grad, ldg, lr, w);               \
+  switch (m.cls) {
+#define SP_SGD_CASE(C)                                                          \
+  case C:                                                                       \
+    sgd_tile<SgdGeo<C>, LongGeo<C>>(m, tile, sh, bags, grad, ldg, lr, w);       \
     break;
-        SP_SGD_CASE(0)
-        SP_SGD_CASE(1)
-        SP_SGD_CASE(2)
-        SP_SGD_CASE(3)
-        SP_SGD_CASE(4)
-        SP_SGD_CASE(5)
+    SP_SGD_CASE(0)
+    SP_SGD_CASE(1)
+    SP_SGD_CASE(2)
+    SP_SGD_CASE(3)
+    SP_SGD_CASE(4)
+    SP_SGD_CASE(5)
 #undef SP_SGD_CASE
-        default:
-          j += sgd_round_generic(m, j, np, p0, lane, sh, bags, grad, ldg, lr, w);
-      }
-    }
+    default:
+      sgd_tile_generic(m, tile, sh, bags, grad, ldg, lr, w);
   }
 }
 
@@ -775,22 +795,39 @@ size_t exclusive_scan_i32(void* temp, size_t temp_bytes, const int32_t* in,
   return bytes;
 }
 
-void launch_sgd(const TableMeta* d_meta_canon, const uint32_t* d_rowbase_end,
-                int n_tables, const int64_t* d_gstart, const int32_t* d_gt0, int n_groups,
-                const uint32_t* d_keys, const void* d_bags, bool bags16,
-                int64_t n, const float* d_grad, int64_t ldg, float lr, float* d_w,
-                cudaStream_t st) {
-  if (n <= 0 || n_tables <= 0) return;
-  if (n_groups > kMaxSortGroups) raise(SP_ERR_BAD_INPUT, "too many sort groups");
-  const unsigned blocks = static_cast<unsigned>((n + kTilePos - 1) / kTilePos);
+std::vector<int> make_sgd_tiles(const std::vector<int64_t>& table_nnz) {
+  std::vector<int> out;
+  int64_t p = 0;
+  for (size_t t = 0; t < table_nnz.size(); ++t) {
+    const int64_t e = p + table_nnz[t];
+    for (int64_t q = p; q < e; q += kTilePos) {
+      SgdTile tl{};
+      tl.t = static_cast<int32_t>(t);
+      tl.p0 = static_cast<int32_t>(q);
+      tl.np = static_cast<int32_t>(std::min<int64_t>(kTilePos, e - q));
+      tl.tstart = static_cast<int32_t>(p);
+      tl.pend = static_cast<int32_t>(e);
+      const int* raw = reinterpret_cast<const int*>(&tl);
+      out.insert(out.end(), raw, raw + kSgdTileInts);
+    }
+    p = e;
+  }
+  return out;
+}
+
+void launch_sgd(const TableMeta* d_meta_canon, const int* d_tiles, int64_t n_tiles,
+                const uint32_t* d_keys, const void* d_bags, bool bags16, const float* d_grad,
+                int64_t ldg, float lr, float* d_w, cudaStream_t st) {
+  if (n_tiles <= 0) return;
+  static_assert(sizeof(SgdTile) == kSgdTileInts * sizeof(int), "tile layout");
+  const SgdTile* tiles = reinterpret_cast<const SgdTile*>(d_tiles);
+  const unsigned blocks = static_cast<unsigned>(n_tiles);
   if (bags16)
     sgd_kernel<uint16_t><<<blocks, kBlockThreads, 0, st>>>(
-        d_meta_canon, d_rowbase_end, n_tables, d_gstart, d_gt0, n_groups, d_keys,
-        static_cast<const uint16_t*>(d_bags), n, d_grad, ldg, lr, d_w);
+        d_meta_canon, tiles, d_keys, static_cast<const uint16_t*>(d_bags), d_grad, ldg, lr, d_w);
   else
     sgd_kernel<uint32_t><<<blocks, kBlockThreads, 0, st>>>(
-        d_meta_canon, d_rowbase_end, n_tables, d_gstart, d_gt0, n_groups, d_keys,
-        static_cast<const uint32_t*>(d_bags), n, d_grad, ldg, lr, d_w);
+        d_meta_canon, tiles, d_keys, static_cast<const uint32_t*>(d_bags), d_grad, ldg, lr, d_w);
   SP_LAUNCHED();
 }
 

@@ -83,14 +83,16 @@ size_t sort_pairs(void* temp, size_t temp_bytes, const uint32_t* keys_in,
                   int64_t n, int end_bit, cudaStream_t st);
 // Row-wise SGD over the sorted pairs:
 // W[row] -= lr * sum_{k in run, sorted order} grad[bags[k], lcol..].
-// Keys are relative to their sort group (d_gstart[g] = first position,
-// d_gt0[g] = first local table, n_groups + 1 entries each); one launch.
+// Keys are relative to their sort group (the table's rowbase is too); the
+// sorted lookups of local table t occupy its CSR position range, so the
+// launch runs over per-table tiles (make_sgd_tiles: kSgdTileInts ints each,
+// from the per-table lookup counts in canonical order).
 constexpr int kMaxSortGroups = 32;
-void launch_sgd(const TableMeta* d_meta_canon, const uint32_t* d_rowbase_end,
-                int n_tables, const int64_t* d_gstart, const int32_t* d_gt0, int n_groups,
-                const uint32_t* d_keys, const void* d_bags, bool bags16,
-                int64_t n, const float* d_grad, int64_t ldg, float lr, float* d_w,
-                cudaStream_t st);
+constexpr int kSgdTileInts = 8;
+std::vector<int> make_sgd_tiles(const std::vector<int64_t>& table_nnz);
+void launch_sgd(const TableMeta* d_meta_canon, const int* d_tiles, int64_t n_tiles,
+                const uint32_t* d_keys, const void* d_bags, bool bags16, const float* d_grad,
+                int64_t ldg, float lr, float* d_w, cudaStream_t st);
 
 // ---- generator / layout helpers ------------------------------------------
 void launch_init_weights(float* d_w, int64_t rows, int dim, int32_t gid,
