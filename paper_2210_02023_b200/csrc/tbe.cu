@@ -98,14 +98,14 @@ template <int CLS> struct SgdGeo;
 #ifndef SP_SGD_G0
 // (L, V, P, U) per dim class; tuned on B200 at cfg3 (profiles/r01_notes.md).
 // With the L2 reduction update no register holds the old row, so lanes take
-// 64 B of a row (V = 4) for dims >= 64 and every group keeps U = 2
-// positions in flight: SGD 2.33 -> 2.09 ms.
+// 64 B of a row (V = 4) for dims >= 64; runs of >= 32 positions go to the
+// block-cooperative path, so the short rounds keep U = 1.
 #define SP_SGD_G0 1, 1, 16, 2
 #define SP_SGD_G1 2, 1, 16, 1
-#define SP_SGD_G2 2, 2, 16, 2
-#define SP_SGD_G3 4, 2, 8, 2
-#define SP_SGD_G4 4, 4, 8, 2
-#define SP_SGD_G5 8, 4, 4, 2
+#define SP_SGD_G2 2, 2, 16, 1
+#define SP_SGD_G3 4, 2, 8, 1
+#define SP_SGD_G4 4, 4, 8, 1
+#define SP_SGD_G5 8, 4, 4, 1
 #endif
 #ifndef SP_SGD_INTERLEAVE  // lane float4 slices: 1 interleaved (s, s+L, ..), 0 blocked
 #define SP_SGD_INTERLEAVE 1
@@ -116,14 +116,23 @@ template <> struct SgdGeo<2> : Geo<SP_SGD_G2> {};
 template <> struct SgdGeo<3> : Geo<SP_SGD_G3> {};
 template <> struct SgdGeo<4> : Geo<SP_SGD_G4> {};
 template <> struct SgdGeo<5> : Geo<SP_SGD_G5> {};
-// K4 SGD, long runs (hot rows): the whole warp on one run.
+// K4 SGD, long runs (hot rows): each warp of the block sums one slice of
+// the run with the whole warp.
+#ifndef SP_LONG_G0
+#define SP_LONG_G0 1, 1, 1, 4
+#define SP_LONG_G1 2, 1, 1, 4
+#define SP_LONG_G2 4, 1, 1, 4
+#define SP_LONG_G3 8, 1, 1, 4
+#define SP_LONG_G4 16, 1, 1, 8
+#define SP_LONG_G5 32, 1, 1, 8
+#endif
 template <int CLS> struct LongGeo;
-template <> struct LongGeo<0> : Geo<1, 1, 1, 4> {};
-template <> struct LongGeo<1> : Geo<2, 1, 1, 4> {};
-template <> struct LongGeo<2> : Geo<4, 1, 1, 4> {};
-template <> struct LongGeo<3> : Geo<8, 1, 1, 4> {};
-template <> struct LongGeo<4> : Geo<16, 1, 1, 8> {};
-template <> struct LongGeo<5> : Geo<32, 1, 1, 8> {};
+template <> struct LongGeo<0> : Geo<SP_LONG_G0> {};
+template <> struct LongGeo<1> : Geo<SP_LONG_G1> {};
+template <> struct LongGeo<2> : Geo<SP_LONG_G2> {};
+template <> struct LongGeo<3> : Geo<SP_LONG_G3> {};
+template <> struct LongGeo<4> : Geo<SP_LONG_G4> {};
+template <> struct LongGeo<5> : Geo<SP_LONG_G5> {};
 
 // ---------------------------------------------------------------------------
 // K1
@@ -324,9 +333,15 @@ struct HeadFlag {
 // (red.global.add.v4.f32): each unique row has exactly one writer per
 // launch, so it is deterministic, and no SM register waits for the old row.
 
-constexpr int kTilePos = 2048;
+#ifndef SP_SGD_TILE
+#define SP_SGD_TILE 2048
+#endif
+#ifndef SP_SGD_LONG
+#define SP_SGD_LONG 32
+#endif
+constexpr int kTilePos = SP_SGD_TILE;  // <= 2048 (11-bit run starts)
 constexpr int kPosPerThread = kTilePos / kBlockThreads;
-constexpr int kLongRun = 32;   // runs at least this long are block-cooperative
+constexpr int kLongRun = SP_SGD_LONG;  // runs at least this long are block-cooperative
 constexpr int kRunChunk = 16;  // short runs claimed per warp at a time (>= max P)
 constexpr int kMaxLong = kTilePos / kLongRun + 1;
 
