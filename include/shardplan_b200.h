@@ -202,6 +202,17 @@ int sp_get_sorted(sp_ctx* ctx, int32_t dev, uint32_t* keys, uint32_t* bags,
  * (oracle.hpp:206-227). Synchronizes the stream. In NCCL mode the per-device
  * arrays hold every rank's numbers (gathered), identical on all ranks. */
 int sp_run_iteration(sp_ctx* ctx, sp_breakdown* out);
+/* sp_upload_batch + sp_run_iteration in one call, pipelined: the H2D of the
+ * host LookupBatch overlaps the forward of the tables already on the device
+ * (and, with one device per context, their backward sort). The device-side
+ * part of the validation is checked at the end: on failure the tables were
+ * not updated, no batch is current, and the call returns the error
+ * sp_upload_batch would. Stage times include the upload they overlap (fwd
+ * runs from the first H2D to the last forward kernel). This is the
+ * reference-facing step with host buffers (CostOracle::evaluate_placement,
+ * oracle.hpp:187-240, over a real LookupBatch). */
+int sp_run_batch(sp_ctx* ctx, const int64_t* offsets, int64_t offsets_len,
+                 const int64_t* indices, int64_t indices_len, sp_breakdown* out);
 /* Enqueue one iteration without events or host sync (for timing loops and
  * CUDA-graph capture). */
 int sp_enqueue_iteration(sp_ctx* ctx);

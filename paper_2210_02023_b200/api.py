@@ -414,6 +414,23 @@ class EmbeddingShard:
         return CostBreakdown(list(f), list(b), list(c), bd.fwd_comm_stage_ms,
                              bd.bwd_comm_stage_ms, bd.overall_ms)
 
+    def run_batch(self, b: LookupBatch) -> CostBreakdown:
+        """upload_batch + run_iteration in one pipelined call (sp_run_batch):
+        the H2D of the host LookupBatch overlaps the forward of the tables
+        already uploaded; validation errors are raised like upload_batch and
+        leave the tables untouched."""
+        if b.num_tables != len(self.task.tables) or b.batch_size != self.B:
+            raise ShardplanError(8, "batch shape does not match the task")
+        D = self.D
+        f = (ctypes.c_double * D)()
+        bw = (ctypes.c_double * D)()
+        c = (ctypes.c_double * D)()
+        bd = SpBreakdown(f, bw, c, 0.0, 0.0, 0.0)
+        check(lib().sp_run_batch(self._h, _ptr(b.offsets), len(b.offsets), _ptr(b.indices),
+                                 len(b.indices), ctypes.byref(bd)))
+        return CostBreakdown(list(f), list(bw), list(c), bd.fwd_comm_stage_ms,
+                             bd.bwd_comm_stage_ms, bd.overall_ms)
+
     def enqueue_iteration(self):
         check(lib().sp_enqueue_iteration(self._h))
 

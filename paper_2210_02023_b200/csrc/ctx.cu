@@ -70,7 +70,10 @@ struct VDev {
   std::vector<int32_t> colmap;  // local col -> global col
   int64_t W = 0, rows_total = 0, n_tiles = 0;
   int end_bit = 1;
-  int4* d_tiles = nullptr;      // K1 tiles in launch order
+  int4* d_tiles = nullptr;      // K1 tiles in launch order (heavy tables first)
+  int4* d_tiles_canon = nullptr;  // K1 tiles in table order (pipelined upload path)
+  std::vector<int64_t> tile_start;  // first canonical tile of each local table (+ end)
+  std::vector<int> group_of_table;  // sort group of each local table
   int* d_sgd_tiles = nullptr;   // K4 SGD tiles of the current batch
   int64_t n_sgd_tiles = 0, sgd_tile_cap = 0;
   uint32_t* d_keys = nullptr;   // backward sort pairs (written by K1)
@@ -176,6 +179,7 @@ struct sp_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool overlap_sort = true;
+  int64_t upload_chunk = int64_t(8) << 20;  // indices per H2D chunk (SP_UPLOAD_CHUNK)
   std::vector<cudaEvent_t> upload_events;
   ncclComm_t comm = nullptr;
   double* d_bd = nullptr;      // breakdown gather buffer
@@ -347,6 +351,15 @@ void stage_forward(sp_ctx* c, VDev& v) {
 }
 
 // (keys) -> stable radix sort; leaves sorted keys in d_kb, bags in d_bb.
+void sort_pairs_of(sp_ctx* c, VDev& v, const SortGroup& g, cudaStream_t st) {
+  if (g.p1 == g.p0) return;
+  const size_t bb = c->bags16 ? 2 : 4;
+  sort_pairs(c->d_temp, c->temp_bytes, v.d_keys + g.p0, c->d_kb + g.p0,
+             reinterpret_cast<const char*>(v.d_bags) + g.p0 * bb,
+             reinterpret_cast<char*>(c->d_bb) + g.p0 * bb, c->bags16, g.p1 - g.p0, g.end_bit,
+             st);
+}
+
 // rebuild: derive the keys from the CSR even if K1 emitted them (the
 // overlapped sort does not wait for K1).
 void stage_sort(sp_ctx* c, VDev& v, cudaStream_t st, bool rebuild = false) {
@@ -357,14 +370,19 @@ void stage_sort(sp_ctx* c, VDev& v, cudaStream_t st, bool rebuild = false) {
     v.keys_valid = true;
   }
   ProfScope prof(c, kProfSort, st);
-  const size_t bb = c->bags16 ? 2 : 4;
-  for (const SortGroup& g : v.groups) {
-    if (g.p1 == g.p0) continue;
-    sort_pairs(c->d_temp, c->temp_bytes, v.d_keys + g.p0, c->d_kb + g.p0,
-               reinterpret_cast<const char*>(v.d_bags) + g.p0 * bb,
-               reinterpret_cast<char*>(c->d_bb) + g.p0 * bb, c->bags16, g.p1 - g.p0, g.end_bit,
-               st);
+  for (const SortGroup& g : v.groups) sort_pairs_of(c, v, g, st);
+}
+
+// Keys (from the CSR) and the stable sort of one sort group's lookups.
+void sort_group(sp_ctx* c, VDev& v, int gi, cudaStream_t st) {
+  const SortGroup& g = v.groups[gi];
+  {
+    ProfScope prof(c, kProfKeys, st);
+    launch_build_keys(v.d_meta_canon + g.t0, g.t1 - g.t0, c->B, v.d_off, v.d_idx, v.d_keys,
+                      v.d_bags, c->bags16, st);
   }
+  ProfScope prof(c, kProfSort, st);
+  sort_pairs_of(c, v, g, st);
 }
 
 // Bucketed backward (bwd.cu): partition pairs into row buckets, then one
@@ -385,7 +403,10 @@ void stage_backward_bucketed(sp_ctx* c, VDev& v, uint32_t* sorted_keys, uint32_t
 }
 
 // sorted: the overlapped sort already ran (the caller joined its stream).
-void stage_backward(sp_ctx* c, VDev& v, bool sorted = false) {
+// abort_flag (device, may be null): the SGD leaves the tables untouched
+// when *abort_flag != 0 (a batch that failed its device-side validation).
+void stage_backward(sp_ctx* c, VDev& v, bool sorted = false,
+                    const int32_t* abort_flag = nullptr) {
   if (v.nnz == 0) return;
   if (v.bucketed) {
     stage_backward_bucketed(c, v, nullptr, nullptr, true);
@@ -394,7 +415,7 @@ void stage_backward(sp_ctx* c, VDev& v, bool sorted = false) {
   if (!sorted) stage_sort(c, v, c->stream);
   ProfScope prof(c, kProfSgd);
   launch_sgd(v.d_meta_canon, v.d_sgd_tiles, v.n_sgd_tiles, c->d_kb, c->d_bb, c->bags16,
-             v.d_grad, v.W, c->lr, c->d_w, c->stream);
+             v.d_grad, v.W, c->lr, c->d_w, abort_flag, c->stream);
 }
 
 bool nccl_mode(const sp_ctx* c) { return c->world > 1; }
@@ -669,6 +690,8 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
       uint64_t dev_rows = 0;
       for (int g : v.tables) dev_rows += static_cast<uint64_t>(tables[g].hash_size);
       uint64_t group_rows = kSortGroupRows;
+      if (const char* f = std::getenv("SP_SORT_GROUP_ROWS"))  // tests: force many groups
+        group_rows = std::max<uint64_t>(1, std::strtoull(f, nullptr, 10));
       while (2 * ((dev_rows + group_rows - 1) / group_rows) > 30) group_rows *= 2;
       int64_t lcol = 0;
       uint64_t rb = 0;     // row base inside the current sort group
@@ -738,6 +761,21 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
       v.d_tiles = dalloc<int4>(tiles.size(), c->owned, c->dev_bytes);
       if (!tiles.empty())
         SP_CUDA(cudaMemcpy(v.d_tiles, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice));
+      {
+        std::vector<int> canon_order(T);
+        for (int li = 0; li < T; ++li) canon_order[li] = li;
+        const std::vector<int4> ct = make_fwd_tiles(v.meta_canon, canon_order, batch_size);
+        v.d_tiles_canon = dalloc<int4>(ct.size(), c->owned, c->dev_bytes);
+        if (!ct.empty())
+          SP_CUDA(cudaMemcpy(v.d_tiles_canon, ct.data(), ct.size() * sizeof(int4),
+                             cudaMemcpyHostToDevice));
+        v.tile_start.assign(T + 1, 0);
+        for (const int4& tl : ct) ++v.tile_start[tl.x + 1];
+        for (int li = 0; li < T; ++li) v.tile_start[li + 1] += v.tile_start[li];
+        v.group_of_table.assign(T, 0);
+        for (size_t gi = 0; gi < v.groups.size(); ++gi)
+          for (int li = v.groups[gi].t0; li < v.groups[gi].t1; ++li) v.group_of_table[li] = gi;
+      }
       v.d_meta_canon = dalloc<TableMeta>(T, c->owned, c->dev_bytes);
       v.d_rb_end = dalloc<uint32_t>(T, c->owned, c->dev_bytes);
       v.d_colmap = dalloc<int32_t>(v.W, c->owned, c->dev_bytes);
@@ -775,6 +813,8 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
     if (const char* f = std::getenv("SP_FUSE_KEYS")) c->fuse_keys = std::atoi(f) != 0;
     if (const char* f = std::getenv("SP_BWD")) c->use_buckets = std::string(f) == "bucket";
     if (const char* f = std::getenv("SP_OVERLAP")) c->overlap_sort = std::atoi(f) != 0;
+    if (const char* f = std::getenv("SP_UPLOAD_CHUNK"))
+      c->upload_chunk = std::max<int64_t>(1, std::atoll(f));
 
     if (world_size > 1) {
       c->plan = make_plan(tables, num_tables, num_devices, placement, batch_size, rank);
@@ -915,113 +955,147 @@ static void alloc_indices(sp_ctx* c, VDev& v, int64_t nnz) {
   v.keys_valid = false;
 }
 
+}  // extern "C"
+
+namespace sp {
+namespace {
+
+// validate_batch (table.hpp:167-184), O(M) parts on the host (the
+// monotonicity inside a table and the index range are checked on the device
+// while narrowing); sizes every device's CSR and the int64 staging buffer.
+void host_validate_and_size(sp_ctx* c, const int64_t* offsets, int64_t offsets_len,
+                            int64_t indices_len) {
+  const int64_t B = c->B;
+  if (offsets_len != static_cast<int64_t>(c->M) * B + 1)
+    raise(SP_ERR_MALFORMED_BATCH, "offsets length " + std::to_string(offsets_len) +
+                                      ", expected " + std::to_string(c->M * B + 1));
+  if (offsets[0] != 0) raise(SP_ERR_MALFORMED_BATCH, "offsets must start at 0");
+  if (offsets[offsets_len - 1] != indices_len)
+    raise(SP_ERR_MALFORMED_BATCH, "last offset != indices length");
+  for (int t = 0; t <= c->M; ++t) {
+    const int64_t o = offsets[t * B];
+    if (o < 0 || o > indices_len || (t > 0 && o < offsets[(t - 1) * B]))
+      raise(SP_ERR_MALFORMED_BATCH, "offsets decrease at table " + std::to_string(t));
+  }
+  c->has_batch = false;  // until the device-side checks pass
+  int64_t stage_need = 0;
+  for (auto& v : c->vdevs) {
+    v.table_nnz.clear();
+    int64_t n = 0, st = 0;
+    for (int g : v.tables) {
+      const int64_t tn = offsets[(g + 1) * B] - offsets[g * B];
+      v.table_nnz.push_back(tn);
+      n += tn;
+      st += tn + B + 1;
+    }
+    alloc_indices(c, v, n);
+    stage_need += st;  // copies run ahead of the narrows: no reuse across devices
+  }
+  if (stage_need > c->stage_cap) {
+    SP_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->d_stage64) cudaFree(c->d_stage64);
+    SP_CUDA(cudaMalloc(&c->d_stage64, std::max<int64_t>(stage_need, 1) * sizeof(int64_t)));
+    c->stage_cap = std::max<int64_t>(stage_need, 1);
+  }
+}
+
+cudaEvent_t upload_event(sp_ctx* c, size_t& n_ev) {
+  if (n_ev == c->upload_events.size()) {
+    cudaEvent_t e;
+    SP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->upload_events.push_back(e);
+  }
+  return c->upload_events[n_ev++];
+}
+
+// Coalesced, pipelined H2D of a host LookupBatch: local tables with
+// consecutive global ids are adjacent in the reference CSR, so each such run
+// is copied with two large memcpys, cut into chunks of <= kUploadChunk
+// indices (never straddling a sort group) on the copy stream while the
+// compute stream narrows the previous chunk to the int32 device CSR (and
+// flags malformed data in d_flag, clamping it so later kernels stay in
+// bounds). chunk_done(v, t0, t1) runs after the narrows of local tables
+// [t0, t1) of device v are enqueued on the compute stream.
+template <class F>
+void enqueue_upload(sp_ctx* c, const int64_t* offsets, const int64_t* indices, F&& chunk_done) {
+  const int64_t B = c->B;
+  const int64_t kUploadChunk = c->upload_chunk;
+  size_t n_ev = 0;
+  SP_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int32_t), c->stream));
+  {
+    // the staging buffer may still be read by the previous upload's narrows
+    cudaEvent_t e = upload_event(c, n_ev);
+    SP_CUDA(cudaEventRecord(e, c->stream));
+    SP_CUDA(cudaStreamWaitEvent(c->copy_stream, e, 0));
+  }
+  int64_t so = 0;  // staging offset (int64 elements), across all devices
+  for (auto& v : c->vdevs) {
+    const int T = static_cast<int>(v.tables.size());
+    int32_t base = 0;
+    int li = 0;
+    while (li < T) {
+      int run_end = li + 1;
+      while (run_end < T && v.tables[run_end] == v.tables[run_end - 1] + 1) ++run_end;
+      int c0 = li;
+      while (c0 < run_end) {
+        int c1 = c0 + 1;
+        int64_t acc = v.table_nnz[c0];
+        while (c1 < run_end && acc + v.table_nnz[c1] <= kUploadChunk &&
+               v.group_of_table[c1] == v.group_of_table[c0])
+          acc += v.table_nnz[c1++];
+        const int64_t g0 = v.tables[c0], g1 = v.tables[c1 - 1] + 1;
+        const int64_t n_off = (g1 - g0) * B + 1;
+        const int64_t i0 = offsets[g0 * B];
+        const int64_t n_idx = offsets[g1 * B] - i0;
+        int64_t* s_off = c->d_stage64 + so;
+        int64_t* s_idx = s_off + n_off;
+        SP_CUDA(cudaMemcpyAsync(s_off, offsets + g0 * B, n_off * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, c->copy_stream));
+        if (n_idx)
+          SP_CUDA(cudaMemcpyAsync(s_idx, indices + i0, n_idx * sizeof(int64_t),
+                                  cudaMemcpyHostToDevice, c->copy_stream));
+        cudaEvent_t e = upload_event(c, n_ev);
+        SP_CUDA(cudaEventRecord(e, c->copy_stream));
+        SP_CUDA(cudaStreamWaitEvent(c->stream, e, 0));
+        for (int t = c0; t < c1; ++t) {
+          const int g = v.tables[t];
+          const int64_t tn = v.table_nnz[t];
+          launch_narrow_table(s_off + (g - g0) * B, s_idx + (offsets[g * B] - i0), c->B, tn,
+                              c->tables[g].hash_size, base, v.d_off + int64_t(t) * B,
+                              v.d_idx + base, c->d_flag, c->stream);
+          base += static_cast<int32_t>(tn);
+        }
+        chunk_done(v, c0, c1);
+        so += n_off + n_idx;
+        c0 = c1;
+      }
+      li = run_end;
+    }
+    if (v.tables.empty()) SP_CUDA(cudaMemsetAsync(v.d_off, 0, sizeof(int32_t), c->stream));
+  }
+}
+
+void raise_batch_flag(int32_t flag) {
+  if (flag & 1) raise(SP_ERR_MALFORMED_BATCH, "offsets decrease inside a table");
+  if (flag & 2) raise(SP_ERR_BAD_INPUT, "lookup index outside [0, hash_size)");
+}
+
+}  // namespace
+}  // namespace sp
+
+extern "C" {
+
 int sp_upload_batch(sp_ctx* ctx, const int64_t* offsets, int64_t offsets_len,
                     const int64_t* indices, int64_t indices_len) {
   return guarded([&] {
     check_ctx(ctx);
     sp_ctx* c = ctx;
-    const int64_t B = c->B;
-    // validate_batch (table.hpp:167-184), O(1) parts on the host; the
-    // monotonicity and index range are checked on the device.
-    if (offsets_len != static_cast<int64_t>(c->M) * B + 1)
-      raise(SP_ERR_MALFORMED_BATCH, "offsets length " + std::to_string(offsets_len) +
-                                        ", expected " + std::to_string(c->M * B + 1));
-    if (offsets[0] != 0) raise(SP_ERR_MALFORMED_BATCH, "offsets must start at 0");
-    if (offsets[offsets_len - 1] != indices_len)
-      raise(SP_ERR_MALFORMED_BATCH, "last offset != indices length");
-    for (int t = 0; t <= c->M; ++t) {
-      const int64_t o = offsets[t * B];
-      if (o < 0 || o > indices_len || (t > 0 && o < offsets[(t - 1) * B]))
-        raise(SP_ERR_MALFORMED_BATCH, "offsets decrease at table " + std::to_string(t));
-    }
-    int64_t stage_need = 0;
-    for (auto& v : c->vdevs) {
-      v.table_nnz.clear();
-      int64_t n = 0, st = 0;
-      for (int g : v.tables) {
-        const int64_t tn = offsets[(g + 1) * B] - offsets[g * B];
-        v.table_nnz.push_back(tn);
-        n += tn;
-        st += tn + B + 1;
-      }
-      alloc_indices(c, v, n);
-      stage_need += st;  // copies run ahead of the narrows: no reuse across devices
-    }
-    if (stage_need > c->stage_cap) {
-      SP_CUDA(cudaStreamSynchronize(c->stream));
-      if (c->d_stage64) cudaFree(c->d_stage64);
-      SP_CUDA(cudaMalloc(&c->d_stage64, std::max<int64_t>(stage_need, 1) * sizeof(int64_t)));
-      c->stage_cap = std::max<int64_t>(stage_need, 1);
-    }
-    SP_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int32_t), c->stream));
-    // Coalesced, pipelined H2D: local tables with consecutive global ids
-    // are adjacent in the reference CSR, so each such run is copied with two
-    // large memcpys, cut into chunks of <= kUploadChunk indices on the copy
-    // stream while the compute stream narrows the previous chunk.
-    constexpr int64_t kUploadChunk = int64_t(8) << 20;
-    size_t n_ev = 0;
-    auto next_event = [&]() {
-      if (n_ev == c->upload_events.size()) {
-        cudaEvent_t e;
-        SP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        c->upload_events.push_back(e);
-      }
-      return c->upload_events[n_ev++];
-    };
-    {
-      // the staging buffer may still be read by the previous upload's narrows
-      cudaEvent_t e = next_event();
-      SP_CUDA(cudaEventRecord(e, c->stream));
-      SP_CUDA(cudaStreamWaitEvent(c->copy_stream, e, 0));
-    }
-    int64_t so = 0;  // staging offset (int64 elements), across all devices
-    for (auto& v : c->vdevs) {
-      const int T = static_cast<int>(v.tables.size());
-      int32_t base = 0;
-      int li = 0;
-      while (li < T) {
-        int run_end = li + 1;
-        while (run_end < T && v.tables[run_end] == v.tables[run_end - 1] + 1) ++run_end;
-        int c0 = li;
-        while (c0 < run_end) {
-          int c1 = c0 + 1;
-          int64_t acc = v.table_nnz[c0];
-          while (c1 < run_end && acc + v.table_nnz[c1] <= kUploadChunk) acc += v.table_nnz[c1++];
-          const int64_t g0 = v.tables[c0], g1 = v.tables[c1 - 1] + 1;
-          const int64_t n_off = (g1 - g0) * B + 1;
-          const int64_t i0 = offsets[g0 * B];
-          const int64_t n_idx = offsets[g1 * B] - i0;
-          int64_t* s_off = c->d_stage64 + so;
-          int64_t* s_idx = s_off + n_off;
-          SP_CUDA(cudaMemcpyAsync(s_off, offsets + g0 * B, n_off * sizeof(int64_t),
-                                  cudaMemcpyHostToDevice, c->copy_stream));
-          if (n_idx)
-            SP_CUDA(cudaMemcpyAsync(s_idx, indices + i0, n_idx * sizeof(int64_t),
-                                    cudaMemcpyHostToDevice, c->copy_stream));
-          cudaEvent_t e = next_event();
-          SP_CUDA(cudaEventRecord(e, c->copy_stream));
-          SP_CUDA(cudaStreamWaitEvent(c->stream, e, 0));
-          for (int t = c0; t < c1; ++t) {
-            const int g = v.tables[t];
-            const int64_t tn = v.table_nnz[t];
-            launch_narrow_table(s_off + (g - g0) * B, s_idx + (offsets[g * B] - i0), c->B, tn,
-                                c->tables[g].hash_size, base, v.d_off + int64_t(t) * B,
-                                v.d_idx + base, c->d_flag, c->stream);
-            base += static_cast<int32_t>(tn);
-          }
-          so += n_off + n_idx;
-          c0 = c1;
-        }
-        li = run_end;
-      }
-      if (v.tables.empty())
-        SP_CUDA(cudaMemsetAsync(v.d_off, 0, sizeof(int32_t), c->stream));
-    }
+    host_validate_and_size(c, offsets, offsets_len, indices_len);
+    enqueue_upload(c, offsets, indices, [](VDev&, int, int) {});
     int32_t flag = 0;
     SP_CUDA(cudaMemcpyAsync(&flag, c->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
     SP_CUDA(cudaStreamSynchronize(c->stream));
-    if (flag & 1) raise(SP_ERR_MALFORMED_BATCH, "offsets decrease inside a table");
-    if (flag & 2) raise(SP_ERR_BAD_INPUT, "lookup index outside [0, hash_size)");
+    raise_batch_flag(flag);
     finish_batch(c);
   });
 }
@@ -1248,14 +1322,108 @@ int sp_get_sorted(sp_ctx* ctx, int32_t dev, uint32_t* keys, uint32_t* bags,
   });
 }
 
+}  // extern "C"
+
+namespace sp {
+namespace {
+// Stages 2-4 with their events: exchanges (a barrier first so a rank's
+// exchange time is not its wait for the slowest rank's compute), then the
+// backward (joining the overlapped sort when ov). abort_flag: see launch_sgd.
+void timed_exchange_and_backward(sp_ctx* c, bool ov, const int32_t* abort_flag) {
+  cudaStream_t st = c->stream;
+  if (exchange_needed(c)) {
+    if (nccl_mode(c)) {
+      barrier(c);
+      SP_CUDA(cudaEventRecord(c->ev_a2a[0], st));
+      a2a_fwd_nccl(c);
+      SP_CUDA(cudaEventRecord(c->ev_a2a[1], st));
+      barrier(c);
+      SP_CUDA(cudaEventRecord(c->ev_a2a[2], st));
+      a2a_bwd_nccl(c);
+      SP_CUDA(cudaEventRecord(c->ev_a2a[3], st));
+    } else {
+      for (auto& v : c->vdevs) {
+        SP_CUDA(cudaEventRecord(v.ev[2], st));
+        a2a_fwd_emulated(c, v);
+        SP_CUDA(cudaEventRecord(v.ev[3], st));
+      }
+      for (auto& v : c->vdevs) {
+        SP_CUDA(cudaEventRecord(v.ev[4], st));
+        a2a_bwd_emulated(c, v);
+        SP_CUDA(cudaEventRecord(v.ev[5], st));
+      }
+    }
+  }
+  for (auto& v : c->vdevs) {
+    SP_CUDA(cudaEventRecord(v.ev[6], st));
+    if (ov) join_sort(c);
+    stage_backward(c, v, ov, abort_flag);
+    SP_CUDA(cudaEventRecord(v.ev[7], st));
+  }
+}
+
+// Per-stage device times of the iteration just synchronised (events ev[0..7]
+// of every (virtual) device, ev_a2a in NCCL mode), gathered over ranks and
+// composed like CostOracle::evaluate_placement (oracle.hpp:222-227).
+void collect_breakdown(sp_ctx* c, sp_breakdown* out) {
+  const int D = c->D;
+  cudaStream_t st = c->stream;
+  std::vector<double> fwd(D, 0.0), bwd(D, 0.0), cf(D, 0.0), cb(D, 0.0);
+  for (auto& v : c->vdevs) {
+    fwd[v.vid] = elapsed(v.ev[0], v.ev[1]);
+    bwd[v.vid] = elapsed(v.ev[6], v.ev[7]);
+    if (exchange_needed(c)) {
+      if (nccl_mode(c)) {
+        cf[v.vid] = elapsed(c->ev_a2a[0], c->ev_a2a[1]);
+        cb[v.vid] = elapsed(c->ev_a2a[2], c->ev_a2a[3]);
+      } else {
+        cf[v.vid] = elapsed(v.ev[2], v.ev[3]);
+        cb[v.vid] = elapsed(v.ev[4], v.ev[5]);
+      }
+    }
+  }
+  if (nccl_mode(c)) {
+    // gather every rank's four numbers
+    double mine[4] = {fwd[c->rank], bwd[c->rank], cf[c->rank], cb[c->rank]};
+    SP_CUDA(cudaMemcpyAsync(c->d_bd + 4 * c->rank, mine, sizeof(mine), cudaMemcpyHostToDevice, st));
+    SP_NCCL(nccl().AllGather(c->d_bd + 4 * c->rank, c->d_bd, 4, ncclFloat64, c->comm, st));
+    std::vector<double> all(4 * D);
+    SP_CUDA(cudaMemcpyAsync(all.data(), c->d_bd, all.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaStreamSynchronize(st));
+    for (int d = 0; d < D; ++d) {
+      fwd[d] = all[4 * d];
+      bwd[d] = all[4 * d + 1];
+      cf[d] = all[4 * d + 2];
+      cb[d] = all[4 * d + 3];
+    }
+  }
+  // composition of oracle.hpp:222-227
+  const double max_fwd = *std::max_element(fwd.begin(), fwd.end());
+  const double max_bwd = *std::max_element(bwd.begin(), bwd.end());
+  const double fstage = *std::max_element(cf.begin(), cf.end());
+  const double bstage = *std::max_element(cb.begin(), cb.end());
+  if (out) {
+    for (int d = 0; d < D; ++d) {
+      if (out->fwd_ms) out->fwd_ms[d] = fwd[d];
+      if (out->bwd_ms) out->bwd_ms[d] = bwd[d];
+      if (out->comm_ms) out->comm_ms[d] = cb[d];
+    }
+    out->fwd_comm_stage_ms = fstage;
+    out->bwd_comm_stage_ms = bstage;
+    out->overall_ms = max_fwd + fstage + bstage + max_bwd;
+  }
+}
+}  // namespace
+}  // namespace sp
+
+extern "C" {
+
 int sp_run_iteration(sp_ctx* ctx, sp_breakdown* out) {
   return guarded([&] {
     check_ctx(ctx);
     require_batch(ctx);
     sp_ctx* c = ctx;
     cudaStream_t st = c->stream;
-    const int D = c->D;
-    std::vector<double> fwd(D, 0.0), bwd(D, 0.0), cf(D, 0.0), cb(D, 0.0);
     // the input-only backward sort overlaps stages 1-3 (its tail, if any,
     // lands in the bwd stage, which starts by joining it)
     const bool ov = overlap_active(c);
@@ -1269,82 +1437,62 @@ int sp_run_iteration(sp_ctx* ctx, sp_breakdown* out) {
       stage_forward(c, v);
       SP_CUDA(cudaEventRecord(v.ev[1], st));
     }
-    // stages 2-3: exchanges (a barrier first so a rank's exchange time is
-    // not its wait for the slowest rank's compute)
-    if (exchange_needed(c)) {
-      if (nccl_mode(c)) {
-        barrier(c);
-        SP_CUDA(cudaEventRecord(c->ev_a2a[0], st));
-        a2a_fwd_nccl(c);
-        SP_CUDA(cudaEventRecord(c->ev_a2a[1], st));
-        barrier(c);
-        SP_CUDA(cudaEventRecord(c->ev_a2a[2], st));
-        a2a_bwd_nccl(c);
-        SP_CUDA(cudaEventRecord(c->ev_a2a[3], st));
-      } else {
-        for (auto& v : c->vdevs) {
-          SP_CUDA(cudaEventRecord(v.ev[2], st));
-          a2a_fwd_emulated(c, v);
-          SP_CUDA(cudaEventRecord(v.ev[3], st));
-        }
-        for (auto& v : c->vdevs) {
-          SP_CUDA(cudaEventRecord(v.ev[4], st));
-          a2a_bwd_emulated(c, v);
-          SP_CUDA(cudaEventRecord(v.ev[5], st));
-        }
-      }
-    }
-    // stage 4: bwd compute
-    for (auto& v : c->vdevs) {
-      SP_CUDA(cudaEventRecord(v.ev[6], st));
-      if (ov) join_sort(c);
-      stage_backward(c, v, ov);
-      SP_CUDA(cudaEventRecord(v.ev[7], st));
-    }
+    timed_exchange_and_backward(c, ov, nullptr);
     SP_CUDA(cudaStreamSynchronize(st));
-    for (auto& v : c->vdevs) {
-      fwd[v.vid] = elapsed(v.ev[0], v.ev[1]);
-      bwd[v.vid] = elapsed(v.ev[6], v.ev[7]);
-      if (exchange_needed(c)) {
-        if (nccl_mode(c)) {
-          cf[v.vid] = elapsed(c->ev_a2a[0], c->ev_a2a[1]);
-          cb[v.vid] = elapsed(c->ev_a2a[2], c->ev_a2a[3]);
-        } else {
-          cf[v.vid] = elapsed(v.ev[2], v.ev[3]);
-          cb[v.vid] = elapsed(v.ev[4], v.ev[5]);
-        }
+    collect_breakdown(c, out);
+  });
+}
+
+// The reference-facing step with host buffers: the LookupBatch's H2D is
+// pipelined with the forward (K1 runs on each uploaded chunk of tables while
+// the next chunk is in flight) and, with one (virtual) device, with the
+// backward sort of every completed sort group; the device-side validation
+// (offsets monotone inside a table, indices in range) is checked at the end
+// and, if it failed, the SGD never touched the tables (device-side abort
+// flag) and the call raises like sp_upload_batch.
+int sp_run_batch(sp_ctx* ctx, const int64_t* offsets, int64_t offsets_len,
+                 const int64_t* indices, int64_t indices_len, sp_breakdown* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    sp_ctx* c = ctx;
+    host_validate_and_size(c, offsets, offsets_len, indices_len);
+    finish_batch(c);  // host-side layout of this batch (sort positions, SGD tiles)
+    c->has_batch = false;
+    cudaStream_t st = c->stream;
+    const bool ov = overlap_active(c);
+    for (auto& v : c->vdevs) SP_CUDA(cudaEventRecord(v.ev[0], st));
+    enqueue_upload(c, offsets, indices, [&](VDev& v, int t0, int t1) {
+      const int64_t k0 = v.tile_start[t0], k1 = v.tile_start[t1];
+      const bool emit = !ov && c->fuse_keys && !v.bucketed;
+      {
+        ProfScope prof(c, kProfFwd);
+        launch_tbe_forward(v.d_meta_canon, v.d_tiles_canon + k0, k1 - k0, c->B, v.d_off,
+                           v.d_idx, c->d_w, v.d_pooled, v.W, emit ? v.d_keys : nullptr,
+                           emit ? v.d_bags : nullptr, c->bags16, st);
       }
-    }
-    if (nccl_mode(c)) {
-      // gather every rank's four numbers
-      double mine[4] = {fwd[c->rank], bwd[c->rank], cf[c->rank], cb[c->rank]};
-      SP_CUDA(cudaMemcpyAsync(c->d_bd + 4 * c->rank, mine, sizeof(mine), cudaMemcpyHostToDevice, st));
-      SP_NCCL(nccl().AllGather(c->d_bd + 4 * c->rank, c->d_bd, 4, ncclFloat64, c->comm, st));
-      std::vector<double> all(4 * D);
-      SP_CUDA(cudaMemcpyAsync(all.data(), c->d_bd, all.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
-      SP_CUDA(cudaStreamSynchronize(st));
-      for (int d = 0; d < D; ++d) {
-        fwd[d] = all[4 * d];
-        bwd[d] = all[4 * d + 1];
-        cf[d] = all[4 * d + 2];
-        cb[d] = all[4 * d + 3];
+      if (t1 == static_cast<int>(v.tables.size())) {
+        v.keys_valid = emit;
+        SP_CUDA(cudaEventRecord(v.ev[1], st));
       }
-    }
-    // composition of oracle.hpp:222-227
-    const double max_fwd = *std::max_element(fwd.begin(), fwd.end());
-    const double max_bwd = *std::max_element(bwd.begin(), bwd.end());
-    const double fstage = *std::max_element(cf.begin(), cf.end());
-    const double bstage = *std::max_element(cb.begin(), cb.end());
-    if (out) {
-      for (int d = 0; d < D; ++d) {
-        if (out->fwd_ms) out->fwd_ms[d] = fwd[d];
-        if (out->bwd_ms) out->bwd_ms[d] = bwd[d];
-        if (out->comm_ms) out->comm_ms[d] = cb[d];
+      const int g = v.group_of_table[t1 - 1];
+      if (ov && v.groups[g].t1 == t1) {
+        // the group's CSR is on the device: sort it on the side stream
+        SP_CUDA(cudaEventRecord(c->ev_fork, st));
+        SP_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+        sort_group(c, v, g, c->side);
+        if (g + 1 == static_cast<int>(v.groups.size()))
+          SP_CUDA(cudaEventRecord(c->ev_join, c->side));
       }
-      out->fwd_comm_stage_ms = fstage;
-      out->bwd_comm_stage_ms = bstage;
-      out->overall_ms = max_fwd + fstage + bstage + max_bwd;
-    }
+    });
+    for (auto& v : c->vdevs)
+      if (v.tables.empty()) SP_CUDA(cudaEventRecord(v.ev[1], st));
+    timed_exchange_and_backward(c, ov, c->d_flag);
+    int32_t flag = 0;
+    SP_CUDA(cudaMemcpyAsync(&flag, c->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaStreamSynchronize(st));
+    raise_batch_flag(flag);
+    c->has_batch = true;
+    collect_breakdown(c, out);
   });
 }
 

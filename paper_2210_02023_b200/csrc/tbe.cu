@@ -546,7 +546,8 @@ __global__ void __launch_bounds__(kBlockThreads, SP_SGD_MIN_BLOCKS)
     sgd_kernel(const TableMeta* __restrict__ meta, const SgdTile* __restrict__ tiles,
                const uint32_t* __restrict__ keys, const BagT* __restrict__ bags,
                const float* __restrict__ grad, int64_t ldg, float lr,
-               float* __restrict__ w) {
+               float* __restrict__ w, const int32_t* __restrict__ abort_flag) {
+  if (abort_flag != nullptr && *abort_flag != 0) return;  // invalid batch: no update
   __shared__ SgdShared<BagT> sh;
   using BlockScan = cub::BlockScan<int, kBlockThreads>;
   __shared__ typename BlockScan::TempStorage scan_tmp;
@@ -686,7 +687,9 @@ __global__ void synth_indices_kernel(const int32_t* __restrict__ gid,
   }
 }
 
-// flag bits: 1 = offsets decrease, 2 = index out of [0, rows)
+// flag bits: 1 = offsets decrease, 2 = index out of [0, rows). Bad data is
+// clamped (offsets into [0, nnz], indices to row 0) so every later kernel
+// stays in bounds even before the host has seen the flag.
 __global__ void narrow_table_kernel(const int64_t* __restrict__ off64,
                                     const int64_t* __restrict__ idx64,
                                     int batch, int64_t nnz, int64_t rows,
@@ -700,12 +703,14 @@ __global__ void narrow_table_kernel(const int64_t* __restrict__ off64,
   for (int64_t b = t0; b <= batch; b += stride) {
     const int64_t a = off64[b];
     if (b < batch && off64[b + 1] < a) bad |= 1;
-    off[b] = static_cast<int32_t>(a - o0) + base;
+    const int64_t rel = a - o0;
+    off[b] = static_cast<int32_t>(rel < 0 ? 0 : (rel > nnz ? nnz : rel)) + base;
   }
   for (int64_t p = t0; p < nnz; p += stride) {
     const int64_t r = idx64[p];
-    if (r < 0 || r >= rows) bad |= 2;
-    idx[p] = static_cast<int32_t>(r);
+    const bool out = r < 0 || r >= rows;
+    if (out) bad |= 2;
+    idx[p] = out ? 0 : static_cast<int32_t>(r);
   }
   if (bad) atomicOr(flag, bad);
 }
@@ -832,17 +837,19 @@ std::vector<int> make_sgd_tiles(const std::vector<int64_t>& table_nnz) {
 
 void launch_sgd(const TableMeta* d_meta_canon, const int* d_tiles, int64_t n_tiles,
                 const uint32_t* d_keys, const void* d_bags, bool bags16, const float* d_grad,
-                int64_t ldg, float lr, float* d_w, cudaStream_t st) {
+                int64_t ldg, float lr, float* d_w, const int32_t* d_abort, cudaStream_t st) {
   if (n_tiles <= 0) return;
   static_assert(sizeof(SgdTile) == kSgdTileInts * sizeof(int), "tile layout");
   const SgdTile* tiles = reinterpret_cast<const SgdTile*>(d_tiles);
   const unsigned blocks = static_cast<unsigned>(n_tiles);
   if (bags16)
     sgd_kernel<uint16_t><<<blocks, kBlockThreads, 0, st>>>(
-        d_meta_canon, tiles, d_keys, static_cast<const uint16_t*>(d_bags), d_grad, ldg, lr, d_w);
+        d_meta_canon, tiles, d_keys, static_cast<const uint16_t*>(d_bags), d_grad, ldg, lr, d_w,
+        d_abort);
   else
     sgd_kernel<uint32_t><<<blocks, kBlockThreads, 0, st>>>(
-        d_meta_canon, tiles, d_keys, static_cast<const uint32_t*>(d_bags), d_grad, ldg, lr, d_w);
+        d_meta_canon, tiles, d_keys, static_cast<const uint32_t*>(d_bags), d_grad, ldg, lr, d_w,
+        d_abort);
   SP_LAUNCHED();
 }
 

@@ -90,9 +90,10 @@ size_t sort_pairs(void* temp, size_t temp_bytes, const uint32_t* keys_in,
 constexpr int kMaxSortGroups = 32;
 constexpr int kSgdTileInts = 8;
 std::vector<int> make_sgd_tiles(const std::vector<int64_t>& table_nnz);
+// d_abort (may be null): when *d_abort != 0 the launch leaves W untouched.
 void launch_sgd(const TableMeta* d_meta_canon, const int* d_tiles, int64_t n_tiles,
                 const uint32_t* d_keys, const void* d_bags, bool bags16, const float* d_grad,
-                int64_t ldg, float lr, float* d_w, cudaStream_t st);
+                int64_t ldg, float lr, float* d_w, const int32_t* d_abort, cudaStream_t st);
 
 // ---- generator / layout helpers ------------------------------------------
 void launch_init_weights(float* d_w, int64_t rows, int dim, int32_t gid,

@@ -1,0 +1,98 @@
+"""sp_run_batch — the pipelined upload + iteration with host buffers (the e2e
+path of bench.py) — against the CPU oracle and against the unpipelined
+upload_batch + run_iteration, including many upload chunks and sort groups
+(SP_UPLOAD_CHUNK / SP_SORT_GROUP_ROWS), and its deferred validation: a bad
+batch raises like upload_batch and leaves every table untouched."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import lookup as orc
+from paper_2210_02023_b200.api import EmbeddingShard, LookupBatch, ShardplanError
+from tests.helpers import as_dicts, random_task, random_weights
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-5
+
+
+@pytest.fixture(params=["default", "chunked"])
+def chunking(request, monkeypatch):
+    if request.param == "chunked":
+        monkeypatch.setenv("SP_UPLOAD_CHUNK", "700")
+        monkeypatch.setenv("SP_SORT_GROUP_ROWS", "3000")
+    return request.param
+
+
+def _shard(task, placement, weights, lr):
+    sh = EmbeddingShard(task, placement, lr=lr)
+    for i, w in enumerate(weights):
+        sh.set_table(i, w)
+    return sh
+
+
+@pytest.mark.parametrize("D", [1, 3])
+@pytest.mark.parametrize("overlap", ["1", "0"])
+def test_run_batch_matches_oracle(D, overlap, chunking, monkeypatch):
+    monkeypatch.setenv("SP_OVERLAP", overlap)
+    B = 96
+    dims = [16, 32, 64, 128, 16, 64, 12, 4]
+    task, placement = random_task(31 + D, dims, D, B)
+    weights = random_weights(13, task.tables)
+    off, idx = orc.synth_batch(as_dicts(task.tables), B, seed=9)
+    W = sum(dims)
+    grad = np.random.default_rng(4).uniform(-1, 1, size=(B, W)).astype(np.float32)
+    lr = 0.02
+    sh = _shard(task, placement, weights, lr)
+    sh.set_grad(grad)
+    bd = sh.run_batch(LookupBatch(idx, off, len(dims), B))
+    assert bd.overall_ms > 0 and len(bd.fwd_ms) == D
+    rows = [t.hash_size for t in task.tables]
+    np.testing.assert_allclose(sh.pooled(), orc.tbe_forward(dims, rows, weights, off, idx, B),
+                               rtol=RTOL, atol=1e-5)
+    want = orc.tbe_backward_sgd(dims, rows, weights, off, idx, B, grad, lr,
+                                list(range(len(dims))))
+    got = [sh.get_table(i) for i in range(len(dims))]
+    for i in range(len(dims)):
+        np.testing.assert_allclose(got[i], want[i], rtol=RTOL, atol=1e-5)
+    # identical to the unpipelined path on a fresh shard (same kernels, same order)
+    ref = _shard(task, placement, weights, lr)
+    ref.set_grad(grad)
+    ref.upload_batch(LookupBatch(idx, off, len(dims), B))
+    ref.run_iteration()
+    for i in range(len(dims)):
+        np.testing.assert_array_equal(got[i], ref.get_table(i))
+    # the batch stays current: a plain iteration on it works
+    sh.run_iteration()
+    sh.close()
+    ref.close()
+
+
+def test_run_batch_rejects_bad_batch_without_update(chunking):
+    B = 64
+    dims = [16, 64, 32]
+    task, placement = random_task(5, dims, 1, B)
+    weights = random_weights(3, task.tables)
+    off, idx = orc.synth_batch(as_dicts(task.tables), B, seed=2)
+    sh = _shard(task, placement, weights, 0.1)
+    sh.set_grad(np.ones((B, sum(dims)), dtype=np.float32))
+    bad = idx.copy()
+    bad[len(bad) // 2] = task.tables[1].hash_size + 5  # out of range in table 1
+    with pytest.raises(ShardplanError) as e:
+        sh.run_batch(LookupBatch(bad, off, 3, B))
+    assert e.value.kind == "bad_input"
+    for i in range(3):
+        np.testing.assert_array_equal(sh.get_table(i), weights[i])
+    with pytest.raises(ShardplanError):  # no batch is current after the failure
+        sh.run_iteration()
+    bad_off = off.copy()
+    bad_off[5] = bad_off[7] + 1  # decreases inside table 0
+    with pytest.raises(ShardplanError) as e:
+        sh.run_batch(LookupBatch(idx, bad_off, 3, B))
+    assert e.value.kind == "malformed_batch"
+    for i in range(3):
+        np.testing.assert_array_equal(sh.get_table(i), weights[i])
+    # a good batch afterwards works
+    sh.run_batch(LookupBatch(idx, off, 3, B))
+    sh.close()
