@@ -220,6 +220,12 @@ int sp_enqueue_iteration(sp_ctx* ctx);
  * times; 0 iters only builds the graph. Reports kernel nodes per graph. */
 int sp_graph_replay(sp_ctx* ctx, int32_t iters, int32_t* kernels_per_iter);
 
+/* The backward's key build + radix sort reads only the batch: by default
+ * (one device per context) it runs on a high-priority side stream,
+ * concurrently with the forward and the exchanges. on = 0 serialises it
+ * behind K1 (per-kernel timing in isolation). */
+int sp_ctx_set_overlap(sp_ctx* ctx, int32_t on);
+
 /* Per-kernel CUDA-event timing of the hot-path launches enqueued while
  * enabled (on the context stream): sp_ctx_kernel_ms returns the summed ms
  * and launch counts of [0]=K1 forward, [1]=key build, [2]=radix sort,

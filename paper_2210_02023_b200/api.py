@@ -439,6 +439,11 @@ class EmbeddingShard:
         check(lib().sp_graph_replay(self._h, iters, ctypes.byref(k)))
         return k.value
 
+    def set_overlap(self, on: bool):
+        """Backward sort on the side stream concurrently with the forward
+        (default) or serialised behind it (sp_ctx_set_overlap)."""
+        check(lib().sp_ctx_set_overlap(self._h, 1 if on else 0))
+
     def set_profiling(self, on: bool):
         check(lib().sp_ctx_set_profiling(self._h, 1 if on else 0))
 

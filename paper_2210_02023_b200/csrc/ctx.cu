@@ -179,6 +179,11 @@ struct sp_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool overlap_sort = true;
+  // 1: keys rebuilt from the CSR + the whole sort on the side stream under K1;
+  // 2 (SP_OVERLAP=2): K1 per sort group emitting the keys, each group's sort
+  // under K1 of the next groups (measured slower at cfg3: 4.81 vs 4.43 ms,
+  // the last group's sort is left exposed)
+  int overlap_mode = 1;
   int64_t upload_chunk = int64_t(8) << 20;  // indices per H2D chunk (SP_UPLOAD_CHUNK)
   std::vector<cudaEvent_t> upload_events;
   ncclComm_t comm = nullptr;
@@ -491,10 +496,43 @@ void fork_sort(sp_ctx* c) {
 
 void join_sort(sp_ctx* c) { SP_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0)); }
 
-void enqueue_iteration(sp_ctx* c) {
-  const bool ov = overlap_active(c);
+// Overlap mode 2: K1 runs sort group by sort group (canonical tile order),
+// emitting the group's sort pairs; each group's radix sort then runs on the
+// side stream under K1 of the next groups.
+void forward_pipelined(sp_ctx* c) {
+  VDev& v = c->vdevs[0];
+  for (size_t gi = 0; gi < v.groups.size(); ++gi) {
+    const SortGroup& g = v.groups[gi];
+    const int64_t k0 = v.tile_start[g.t0], k1 = v.tile_start[g.t1];
+    {
+      ProfScope prof(c, kProfFwd);
+      launch_tbe_forward(v.d_meta_canon, v.d_tiles_canon + k0, k1 - k0, c->B, v.d_off,
+                         v.d_idx, c->d_w, v.d_pooled, v.W, v.d_keys, v.d_bags, c->bags16,
+                         c->stream);
+    }
+    SP_CUDA(cudaEventRecord(c->ev_fork, c->stream));
+    SP_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    ProfScope prof(c, kProfSort, c->side);
+    sort_pairs_of(c, v, g, c->side);
+  }
+  v.keys_valid = true;
+  SP_CUDA(cudaEventRecord(c->ev_join, c->side));
+}
+
+// Stage 1 of an iteration: the forward, with the backward sort forked onto
+// the side stream when the overlap is active.
+void forward_stage(sp_ctx* c, bool ov) {
+  if (ov && c->overlap_mode == 2) {
+    forward_pipelined(c);
+    return;
+  }
   if (ov) fork_sort(c);
   for (auto& v : c->vdevs) stage_forward(c, v);
+}
+
+void enqueue_iteration(sp_ctx* c) {
+  const bool ov = overlap_active(c);
+  forward_stage(c, ov);
   if (exchange_needed(c)) {
     ProfScope prof(c, kProfExchange);
     if (nccl_mode(c)) {
@@ -812,7 +850,10 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
     for (auto& e : c->ev_a2a) SP_CUDA(cudaEventCreate(&e));
     if (const char* f = std::getenv("SP_FUSE_KEYS")) c->fuse_keys = std::atoi(f) != 0;
     if (const char* f = std::getenv("SP_BWD")) c->use_buckets = std::string(f) == "bucket";
-    if (const char* f = std::getenv("SP_OVERLAP")) c->overlap_sort = std::atoi(f) != 0;
+    if (const char* f = std::getenv("SP_OVERLAP")) {
+      c->overlap_sort = std::atoi(f) != 0;
+      if (std::atoi(f) == 1 || std::atoi(f) == 2) c->overlap_mode = std::atoi(f);
+    }
     if (const char* f = std::getenv("SP_UPLOAD_CHUNK"))
       c->upload_chunk = std::max<int64_t>(1, std::atoll(f));
 
@@ -1429,13 +1470,15 @@ int sp_run_iteration(sp_ctx* ctx, sp_breakdown* out) {
     const bool ov = overlap_active(c);
     if (ov) {
       SP_CUDA(cudaEventRecord(c->vdevs[0].ev[0], st));
-      fork_sort(c);
-    }
-    // stage 1: fwd compute per (virtual) device
-    for (auto& v : c->vdevs) {
-      if (!ov) SP_CUDA(cudaEventRecord(v.ev[0], st));
-      stage_forward(c, v);
-      SP_CUDA(cudaEventRecord(v.ev[1], st));
+      forward_stage(c, ov);
+      SP_CUDA(cudaEventRecord(c->vdevs[0].ev[1], st));
+    } else {
+      // stage 1: fwd compute per (virtual) device
+      for (auto& v : c->vdevs) {
+        SP_CUDA(cudaEventRecord(v.ev[0], st));
+        stage_forward(c, v);
+        SP_CUDA(cudaEventRecord(v.ev[1], st));
+      }
     }
     timed_exchange_and_backward(c, ov, nullptr);
     SP_CUDA(cudaStreamSynchronize(st));
@@ -1463,7 +1506,7 @@ int sp_run_batch(sp_ctx* ctx, const int64_t* offsets, int64_t offsets_len,
     for (auto& v : c->vdevs) SP_CUDA(cudaEventRecord(v.ev[0], st));
     enqueue_upload(c, offsets, indices, [&](VDev& v, int t0, int t1) {
       const int64_t k0 = v.tile_start[t0], k1 = v.tile_start[t1];
-      const bool emit = !ov && c->fuse_keys && !v.bucketed;
+      const bool emit = ov ? c->overlap_mode == 2 : (c->fuse_keys && !v.bucketed);
       {
         ProfScope prof(c, kProfFwd);
         launch_tbe_forward(v.d_meta_canon, v.d_tiles_canon + k0, k1 - k0, c->B, v.d_off,
@@ -1479,7 +1522,12 @@ int sp_run_batch(sp_ctx* ctx, const int64_t* offsets, int64_t offsets_len,
         // the group's CSR is on the device: sort it on the side stream
         SP_CUDA(cudaEventRecord(c->ev_fork, st));
         SP_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-        sort_group(c, v, g, c->side);
+        if (c->overlap_mode == 2) {
+          ProfScope prof(c, kProfSort, c->side);
+          sort_pairs_of(c, v, v.groups[g], c->side);
+        } else {
+          sort_group(c, v, g, c->side);
+        }
         if (g + 1 == static_cast<int>(v.groups.size()))
           SP_CUDA(cudaEventRecord(c->ev_join, c->side));
       }
@@ -1565,6 +1613,19 @@ int sp_exchange_plan(const sp_table_spec* tables, int32_t num_tables, int32_t nu
   });
 }
 
+int sp_ctx_set_overlap(sp_ctx* ctx, int32_t on) {
+  return guarded([&] {
+    check_ctx(ctx);
+    SP_CUDA(cudaStreamSynchronize(ctx->stream));
+    SP_CUDA(cudaStreamSynchronize(ctx->side));
+    ctx->overlap_sort = on != 0;
+    if (ctx->graph_exec) {
+      cudaGraphExecDestroy(ctx->graph_exec);
+      ctx->graph_exec = nullptr;
+    }
+  });
+}
+
 int sp_ctx_set_profiling(sp_ctx* ctx, int32_t on) {
   return guarded([&] {
     check_ctx(ctx);
@@ -1613,7 +1674,7 @@ int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]) {
       const double offs = 4.0 * (static_cast<double>(T) * c->B + 1);
       const double csr = offs + 4.0 * v.nnz;
       const double outb = 4.0 * c->B * v.W;
-      const bool emit = c->fuse_keys && !v.bucketed;
+      const bool emit = overlap_active(c) ? c->overlap_mode == 2 : (c->fuse_keys && !v.bucketed);
       const double pair = c->bags16 ? 6.0 : 8.0;  // sort key + bag payload bytes
       fwd = std::max(fwd, csr + rows_bytes + outb + (emit ? pair * v.nnz : 0.0));
       a2a = std::max(a2a, 4.0 * c->B * v.W * (c->D - 1) / c->D);
