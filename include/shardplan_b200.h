@@ -42,6 +42,7 @@ extern "C" {
 #define SP_NUM_BINS 17      /* table.hpp:26 kNumBins */
 #define SP_NUM_FEATURES 21  /* table.hpp:28 kNumFeatures */
 #define SP_NCCL_ID_BYTES 128
+#define SP_IPC_BYTES 128    /* two cudaIpcMemHandle_t: receive + gradient buffers */
 
 /* Status codes: ErrorKind (error.hpp:11-22) + 1. */
 enum sp_status {
@@ -111,7 +112,8 @@ int sp_nccl_unique_id(uint8_t out_id[SP_NCCL_ID_BYTES]);
 /* Creates rank `rank`'s shard of `placement` (length num_tables, entries in
  * [0, num_devices), oracle.hpp:75-76).
  *  - world_size == num_devices: one process per GPU, all-to-all over NCCL
- *    (nccl_id from sp_nccl_unique_id, NULL when num_devices == 1);
+ *    (nccl_id from sp_nccl_unique_id, NULL when num_devices == 1) or over
+ *    peer memory (sp_ipc_import; nccl_id NULL = host-driven stages);
  *  - world_size == 1 < num_devices: emulation — all num_devices virtual
  *    devices live on this GPU and run back to back; their per-device
  *    compute is measured for real, the exchange is a device-local copy of
@@ -139,6 +141,24 @@ int sp_ctx_local_tables(sp_ctx* ctx, int32_t* ids, int32_t* n_out);
 int sp_init_tables(sp_ctx* ctx, uint64_t seed);
 int sp_set_table(sp_ctx* ctx, int32_t table_id, const float* rows);
 int sp_get_table(sp_ctx* ctx, int32_t table_id, float* rows);
+
+/* Peer-memory exchange (one process per GPU on one NVLink/NVSwitch node, or
+ * several processes sharing a GPU): every rank exports the CUDA IPC handles
+ * of its receive and gradient buffers, the host all-gathers them (rank
+ * order, world_size * SP_IPC_BYTES) and every rank imports them. From then on
+ * K1 stores each batch slice's pooled rows straight into the receiving
+ * rank's buffer (the forward all-to-all is fused into the lookup kernel:
+ * stores to mapped peer addresses + a system-scope fence) and the backward
+ * exchange pulls this rank's gradient slices from the peers. Replaces the
+ * NCCL exchange of device_comm (oracle.hpp:178-185). With an NCCL id the
+ * whole iteration stays on the device (NCCL barriers between the stages);
+ * a context created without one (nccl_id = NULL, world_size > 1) is driven
+ * stage by stage from the host: sp_forward; sp_ctx_synchronize + host rank
+ * barrier; sp_a2a_backward; sp_ctx_synchronize + barrier; sp_backward_sgd. */
+int sp_ipc_export(sp_ctx* ctx, uint8_t out[SP_IPC_BYTES]);
+int sp_ipc_import(sp_ctx* ctx, const uint8_t* all_handles);
+/* Wait for all work enqueued on the context's streams. */
+int sp_ctx_synchronize(sp_ctx* ctx);
 
 /* Lookup batch in the reference layout, shardplan::LookupBatch
  * (table.hpp:158-165): offsets[num_tables*B + 1], indices[offsets.back()],

@@ -56,6 +56,9 @@ SIGNATURES = {
     "sp_ctx_algorithmic_bytes": (c_i32, [c_vp, P(c_f64)]),
     "sp_ctx_set_profiling": (c_i32, [c_vp, c_i32]),
     "sp_ctx_set_overlap": (c_i32, [c_vp, c_i32]),
+    "sp_ipc_export": (c_i32, [c_vp, c_vp]),
+    "sp_ipc_import": (c_i32, [c_vp, c_vp]),
+    "sp_ctx_synchronize": (c_i32, [c_vp]),
     "sp_ctx_kernel_ms": (c_i32, [c_vp, P(c_f64), P(c_i64)]),
     "sp_host_alloc": (c_i32, [c_u64, P(c_vp)]),
     "sp_host_free": (None, [c_vp]),

@@ -439,6 +439,27 @@ class EmbeddingShard:
         check(lib().sp_graph_replay(self._h, iters, ctypes.byref(k)))
         return k.value
 
+    IPC_BYTES = 128
+
+    def ipc_export(self) -> bytes:
+        """CUDA IPC handles of this rank's receive and gradient buffers
+        (sp_ipc_export), to be all-gathered by the host in rank order."""
+        buf = (ctypes.c_uint8 * self.IPC_BYTES)()
+        check(lib().sp_ipc_export(self._h, buf))
+        return bytes(buf)
+
+    def ipc_import(self, handles: list):
+        """Map every rank's buffers (sp_ipc_import): K1 then stores pooled
+        rows at their receivers and the backward pulls gradients from peers."""
+        if len(handles) != self.world:
+            raise ShardplanError(8, "one handle blob per rank expected")
+        blob = b"".join(handles)
+        buf = (ctypes.c_uint8 * len(blob)).from_buffer_copy(blob)
+        check(lib().sp_ipc_import(self._h, buf))
+
+    def synchronize(self):
+        check(lib().sp_ctx_synchronize(self._h))
+
     def set_overlap(self, on: bool):
         """Backward sort on the side stream concurrently with the forward
         (default) or serialised behind it (sp_ctx_set_overlap)."""

@@ -187,6 +187,13 @@ struct sp_ctx {
   int64_t upload_chunk = int64_t(8) << 20;  // indices per H2D chunk (SP_UPLOAD_CHUNK)
   std::vector<cudaEvent_t> upload_events;
   ncclComm_t comm = nullptr;
+  // Peer-memory exchange (sp_ipc_import): every rank's receive and gradient
+  // buffers mapped here. K1 stores pooled rows straight into the receivers'
+  // slots; the backward pulls this rank's gradient slices from the peers.
+  bool peer = false;
+  float* peer_recv[sp::kMaxPeers] = {};
+  float* peer_gin[sp::kMaxPeers] = {};
+  std::vector<void*> ipc_opened;
   double* d_bd = nullptr;      // breakdown gather buffer
   int32_t* d_barrier = nullptr;
   cudaEvent_t ev_a2a[4] = {};
@@ -221,6 +228,7 @@ struct sp_ctx {
     for (void* p : sort_owned) cudaFree(p);
     for (void* p : owned) cudaFree(p);
     if (comm) sp::nccl().CommDestroy(comm);
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (copy_stream) cudaStreamSynchronize(copy_stream);
     if (side) cudaStreamSynchronize(side);
     if (ev_fork) cudaEventDestroy(ev_fork);
@@ -346,11 +354,25 @@ bool overlap_active(const sp_ctx* c) {
          c->vdevs[0].nnz > 0;
 }
 
+// Where K1 writes: the local pooled [B, W_v], or — with peer memory — batch
+// slice j straight into rank j's receive slot for this rank (the fused
+// forward all-to-all).
+RowMap fwd_rows(const sp_ctx* c, const VDev& v) {
+  if (!c->peer) return local_rows(v.d_pooled, c->B);
+  RowMap r{};
+  const int64_t R = c->B / c->D;
+  for (int j = 0; j < c->D; ++j) r.base[j] = c->peer_recv[j] + R * c->cumW[c->rank];
+  r.rows_per_part = R;
+  r.parts = c->D;
+  r.fence = 1;
+  return r;
+}
+
 void stage_forward(sp_ctx* c, VDev& v) {
   const bool emit = c->fuse_keys && !v.bucketed && v.nnz > 0 && !overlap_active(c);
   ProfScope prof(c, kProfFwd);
   launch_tbe_forward(v.d_meta_canon, v.d_tiles, v.n_tiles, c->B, v.d_off, v.d_idx,
-                     c->d_w, v.d_pooled, v.W, emit ? v.d_keys : nullptr,
+                     c->d_w, fwd_rows(c, v), v.W, emit ? v.d_keys : nullptr,
                      emit ? v.d_bags : nullptr, c->bags16, c->stream);
   if (emit) v.keys_valid = true;
 }
@@ -423,7 +445,10 @@ void stage_backward(sp_ctx* c, VDev& v, bool sorted = false,
              v.d_grad, v.W, c->lr, c->d_w, abort_flag, c->stream);
 }
 
-bool nccl_mode(const sp_ctx* c) { return c->world > 1; }
+// One process per rank (world > 1); the exchange goes through peer memory
+// (sp_ipc_import) or NCCL.
+bool multi_rank(const sp_ctx* c) { return c->world > 1; }
+bool nccl_mode(const sp_ctx* c) { return c->world > 1 && c->comm != nullptr; }
 
 void d2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   if (bytes) SP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
@@ -477,6 +502,43 @@ void a2a_bwd_nccl(sp_ctx* c) {
   SP_NCCL(nccl().GroupEnd());
 }
 
+// Backward exchange over peer memory: this rank's gradient slice of every
+// receiver j ([B/D, W_r] at j's slot for this rank) is pulled into grad_v.
+void a2a_bwd_peer(sp_ctx* c) {
+  VDev& v = c->vdevs[0];
+  const int64_t R = c->B / c->D;
+  for (int j = 0; j < c->D; ++j)
+    d2d(v.d_grad + j * R * v.W, c->peer_gin[j] + R * c->cumW[c->rank], R * v.W * sizeof(float),
+        c->stream);
+}
+
+void a2a_fwd_rank(sp_ctx* c) {
+  if (c->peer) return;  // K1 already stored every slice at its receiver
+  if (!c->comm) raise(SP_ERR_BAD_INPUT, "multi-rank context without NCCL or peer memory");
+  a2a_fwd_nccl(c);
+}
+
+void a2a_bwd_rank(sp_ctx* c) {
+  if (c->peer) {
+    a2a_bwd_peer(c);
+    return;
+  }
+  if (!c->comm) raise(SP_ERR_BAD_INPUT, "multi-rank context without NCCL or peer memory");
+  a2a_bwd_nccl(c);
+}
+
+// A whole iteration on one stream needs device-side rank barriers (NCCL); a
+// peer-only context (no NCCL id) is driven stage by stage from the host,
+// which synchronises the ranks in between.
+void require_device_sync(const sp_ctx* c) {
+  if (multi_rank(c) && c->comm == nullptr)
+    raise(SP_ERR_BAD_INPUT,
+          "peer-only context (no NCCL id): run the stages from the host with a rank "
+          "barrier between sp_forward, sp_a2a_backward and sp_backward_sgd");
+}
+
+// Device-side rank barrier (NCCL); a peer-only context (no NCCL id) relies on
+// the host to synchronise the ranks between stages.
 void barrier(sp_ctx* c) {
   if (nccl_mode(c))
     SP_NCCL(nccl().AllReduce(c->d_barrier, c->d_barrier, 1, ncclInt32, ncclSum,
@@ -507,7 +569,7 @@ void forward_pipelined(sp_ctx* c) {
     {
       ProfScope prof(c, kProfFwd);
       launch_tbe_forward(v.d_meta_canon, v.d_tiles_canon + k0, k1 - k0, c->B, v.d_off,
-                         v.d_idx, c->d_w, v.d_pooled, v.W, v.d_keys, v.d_bags, c->bags16,
+                         v.d_idx, c->d_w, fwd_rows(c, v), v.W, v.d_keys, v.d_bags, c->bags16,
                          c->stream);
     }
     SP_CUDA(cudaEventRecord(c->ev_fork, c->stream));
@@ -535,9 +597,13 @@ void enqueue_iteration(sp_ctx* c) {
   forward_stage(c, ov);
   if (exchange_needed(c)) {
     ProfScope prof(c, kProfExchange);
-    if (nccl_mode(c)) {
-      a2a_fwd_nccl(c);
-      a2a_bwd_nccl(c);
+    if (multi_rank(c)) {
+      require_device_sync(c);
+      if (c->peer) barrier(c);  // every rank's K1 peer stores have landed
+      a2a_fwd_rank(c);
+      if (c->peer) barrier(c);  // every rank's gradients are ready
+      a2a_bwd_rank(c);
+      if (c->peer) barrier(c);  // pulls done before the peers reuse their buffers
     } else {
       for (auto& v : c->vdevs) a2a_fwd_emulated(c, v);
       for (auto& v : c->vdevs) a2a_bwd_emulated(c, v);
@@ -631,8 +697,8 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
     if (!(world_size == 1 || world_size == num_devices))
       raise(SP_ERR_BAD_INPUT, "world_size must be 1 (emulation) or num_devices");
     if (rank < 0 || rank >= world_size) raise(SP_ERR_BAD_INPUT, "rank out of range");
-    if (world_size > 1 && nccl_id == nullptr)
-      raise(SP_ERR_BAD_INPUT, "multi-rank context needs an NCCL unique id");
+    // world_size > 1 without an NCCL id: a peer-only context, whose exchange
+    // must go through peer memory (sp_ipc_import) with host-driven stages
 
     // Placement legality, as evaluate_placement (oracle.hpp:190-204).
     std::vector<double> mem(num_devices, 0.0);
@@ -859,15 +925,70 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
 
     if (world_size > 1) {
       c->plan = make_plan(tables, num_tables, num_devices, placement, batch_size, rank);
-      ncclUniqueId id;
-      std::memcpy(id.internal, nccl_id, SP_NCCL_ID_BYTES);
-      SP_NCCL(nccl().CommInitRank(&c->comm, world_size, id, rank));
+      if (nccl_id != nullptr) {
+        ncclUniqueId id;
+        std::memcpy(id.internal, nccl_id, SP_NCCL_ID_BYTES);
+        SP_NCCL(nccl().CommInitRank(&c->comm, world_size, id, rank));
+      }
     }
     *out = c.release();
   });
 }
 
 void sp_ctx_destroy(sp_ctx* ctx) { delete ctx; }
+
+int sp_ipc_export(sp_ctx* ctx, uint8_t out[SP_IPC_BYTES]) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (out == nullptr) raise(SP_ERR_BAD_INPUT, "null output");
+    if (ctx->world < 2) raise(SP_ERR_BAD_INPUT, "peer memory needs a multi-rank context");
+    cudaIpcMemHandle_t h[2];
+    SP_CUDA(cudaIpcGetMemHandle(&h[0], ctx->d_recv));
+    SP_CUDA(cudaIpcGetMemHandle(&h[1], ctx->d_gin));
+    static_assert(2 * sizeof(cudaIpcMemHandle_t) == SP_IPC_BYTES, "IPC handle size");
+    std::memcpy(out, h, sizeof(h));
+  });
+}
+
+int sp_ipc_import(sp_ctx* ctx, const uint8_t* all) {
+  return guarded([&] {
+    check_ctx(ctx);
+    sp_ctx* c = ctx;
+    if (all == nullptr) raise(SP_ERR_BAD_INPUT, "null handles");
+    if (c->world < 2 || c->world > kMaxPeers)
+      raise(SP_ERR_BAD_INPUT, "peer memory supports 2.." + std::to_string(kMaxPeers) + " ranks");
+    if (c->peer) raise(SP_ERR_BAD_INPUT, "peer memory already imported");
+    SP_CUDA(cudaStreamSynchronize(c->stream));
+    for (int j = 0; j < c->world; ++j) {
+      if (j == c->rank) {
+        c->peer_recv[j] = c->d_recv;
+        c->peer_gin[j] = c->d_gin;
+        continue;
+      }
+      cudaIpcMemHandle_t h[2];
+      std::memcpy(h, all + static_cast<size_t>(j) * SP_IPC_BYTES, sizeof(h));
+      for (int k = 0; k < 2; ++k) {
+        void* p = nullptr;
+        SP_CUDA(cudaIpcOpenMemHandle(&p, h[k], cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_opened.push_back(p);
+        (k == 0 ? c->peer_recv : c->peer_gin)[j] = static_cast<float*>(p);
+      }
+    }
+    c->peer = true;
+    if (c->graph_exec) {
+      cudaGraphExecDestroy(c->graph_exec);
+      c->graph_exec = nullptr;
+    }
+  });
+}
+
+int sp_ctx_synchronize(sp_ctx* ctx) {
+  return guarded([&] {
+    check_ctx(ctx);
+    SP_CUDA(cudaStreamSynchronize(ctx->stream));
+    SP_CUDA(cudaStreamSynchronize(ctx->side));
+  });
+}
 
 int sp_ctx_stream(sp_ctx* ctx, void** stream) {
   return guarded([&] {
@@ -1227,7 +1348,7 @@ int sp_a2a_forward(sp_ctx* ctx) {
   return guarded([&] {
     check_ctx(ctx);
     if (!exchange_needed(ctx)) return;
-    if (nccl_mode(ctx)) a2a_fwd_nccl(ctx);
+    if (multi_rank(ctx)) a2a_fwd_rank(ctx);
     else for (auto& v : ctx->vdevs) a2a_fwd_emulated(ctx, v);
   });
 }
@@ -1236,7 +1357,7 @@ int sp_a2a_backward(sp_ctx* ctx) {
   return guarded([&] {
     check_ctx(ctx);
     if (!exchange_needed(ctx)) return;
-    if (nccl_mode(ctx)) a2a_bwd_nccl(ctx);
+    if (multi_rank(ctx)) a2a_bwd_rank(ctx);
     else for (auto& v : ctx->vdevs) a2a_bwd_emulated(ctx, v);
   });
 }
@@ -1337,6 +1458,9 @@ int sp_get_pooled(sp_ctx* ctx, float* pooled) {
 int sp_get_local_pooled(sp_ctx* ctx, int32_t dev, float* pooled) {
   return guarded([&] {
     check_ctx(ctx);
+    if (ctx->peer)
+      raise(SP_ERR_BAD_INPUT, "peer memory: K1 stores the pooled rows at their receivers "
+                              "(read them with sp_get_pooled on each rank)");
     VDev& v = vdev_for(ctx, dev);
     SP_CUDA(cudaMemcpyAsync(pooled, v.d_pooled, static_cast<int64_t>(ctx->B) * v.W * sizeof(float),
                             cudaMemcpyDeviceToHost, ctx->stream));
@@ -1373,14 +1497,16 @@ namespace {
 void timed_exchange_and_backward(sp_ctx* c, bool ov, const int32_t* abort_flag) {
   cudaStream_t st = c->stream;
   if (exchange_needed(c)) {
-    if (nccl_mode(c)) {
+    if (multi_rank(c)) {
+      require_device_sync(c);
       barrier(c);
       SP_CUDA(cudaEventRecord(c->ev_a2a[0], st));
-      a2a_fwd_nccl(c);
+      a2a_fwd_rank(c);  // peer memory: already done by K1 (the barrier is its completion)
       SP_CUDA(cudaEventRecord(c->ev_a2a[1], st));
       barrier(c);
       SP_CUDA(cudaEventRecord(c->ev_a2a[2], st));
-      a2a_bwd_nccl(c);
+      a2a_bwd_rank(c);
+      if (c->peer) barrier(c);
       SP_CUDA(cudaEventRecord(c->ev_a2a[3], st));
     } else {
       for (auto& v : c->vdevs) {
@@ -1414,7 +1540,7 @@ void collect_breakdown(sp_ctx* c, sp_breakdown* out) {
     fwd[v.vid] = elapsed(v.ev[0], v.ev[1]);
     bwd[v.vid] = elapsed(v.ev[6], v.ev[7]);
     if (exchange_needed(c)) {
-      if (nccl_mode(c)) {
+      if (multi_rank(c)) {
         cf[v.vid] = elapsed(c->ev_a2a[0], c->ev_a2a[1]);
         cb[v.vid] = elapsed(c->ev_a2a[2], c->ev_a2a[3]);
       } else {
@@ -1510,7 +1636,7 @@ int sp_run_batch(sp_ctx* ctx, const int64_t* offsets, int64_t offsets_len,
       {
         ProfScope prof(c, kProfFwd);
         launch_tbe_forward(v.d_meta_canon, v.d_tiles_canon + k0, k1 - k0, c->B, v.d_off,
-                           v.d_idx, c->d_w, v.d_pooled, v.W, emit ? v.d_keys : nullptr,
+                           v.d_idx, c->d_w, fwd_rows(c, v), v.W, emit ? v.d_keys : nullptr,
                            emit ? v.d_bags : nullptr, c->bags16, st);
       }
       if (t1 == static_cast<int>(v.tables.size())) {

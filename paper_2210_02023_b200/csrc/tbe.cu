@@ -147,6 +147,12 @@ struct FwdTile {
 constexpr int kTileBags = 256;
 constexpr int kIdxCap = 4096;  // staged indices per tile (16 KB)
 
+__device__ __forceinline__ float* out_row(const RowMap& rm, int64_t b, int64_t ld) {
+  if (rm.parts == 1) return rm.base[0] + b * ld;
+  const int64_t j = b / rm.rows_per_part;
+  return rm.base[j] + (b - j * rm.rows_per_part) * ld;
+}
+
 template <class G>
 __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb,
                                               int p0, int warp, int lane,
@@ -154,7 +160,7 @@ __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb
                                               const int32_t* s_idx,
                                               const int32_t* __restrict__ idx,
                                               const float* __restrict__ w,
-                                              float* __restrict__ out,
+                                              const RowMap& out,
                                               int64_t ldo) {
   constexpr int L = G::L, V = G::V, P = G::P, U = G::U, S = G::S, GB = G::GB;
   const int span = lane / S, ls = lane % S, g = ls / L, s = ls % L;
@@ -195,7 +201,7 @@ __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb
 #pragma unroll
       for (int j = 0; j < V; ++j) acc[j] = f4_add(acc[j], shfl_xor_f4(acc[j], o));
     if (ok && g == 0) {
-      float* o = out + static_cast<int64_t>(b0 + bag) * ldo + m.lcol + 4 * s;
+      float* o = out_row(out, b0 + bag, ldo) + m.lcol + 4 * s;
 #pragma unroll
       for (int j = 0; j < V; ++j) __stcs(reinterpret_cast<float4*>(o + 4 * L * j), acc[j]);
     }
@@ -206,7 +212,7 @@ __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb
 __device__ __forceinline__ void fwd_tile_warp_generic(
     const TableMeta& m, int b0, int nb, int p0, int warp, int lane,
     const int32_t* s_off, const int32_t* s_idx, const int32_t* __restrict__ idx,
-    const float* __restrict__ w, float* __restrict__ out, int64_t ldo) {
+    const float* __restrict__ w, const RowMap& out, int64_t ldo) {
   for (int bag = warp; bag < nb; bag += kWarpsPerBlock) {
     const int beg = s_off[bag] - p0, end = s_off[bag + 1] - p0;
     for (int c0 = 0; c0 < m.dim; c0 += 32) {
@@ -216,7 +222,7 @@ __device__ __forceinline__ void fwd_tile_warp_generic(
         const int r = k < kIdxCap ? s_idx[k] : __ldg(idx + p0 + k);
         if (c < m.dim) acc += __ldg(w + m.woff + static_cast<int64_t>(r) * m.dim + c);
       }
-      if (c < m.dim) out[static_cast<int64_t>(b0 + bag) * ldo + m.lcol + c] = acc;
+      if (c < m.dim) out_row(out, b0 + bag, ldo)[m.lcol + c] = acc;
     }
   }
 }
@@ -229,7 +235,7 @@ __global__ void __launch_bounds__(kBlockThreads)
                        const FwdTile* __restrict__ tiles, int batch,
                        const int32_t* __restrict__ off,
                        const int32_t* __restrict__ idx,
-                       const float* __restrict__ w, float* __restrict__ out,
+                       const float* __restrict__ w, const RowMap out,
                        int64_t ldo, uint32_t* __restrict__ keys,
                        BagT* __restrict__ bags) {
   __shared__ int32_t s_off[kTileBags + 1];
@@ -274,6 +280,10 @@ __global__ void __launch_bounds__(kBlockThreads)
       fwd_tile_warp_generic(m, tile.b0, tile.nb, p0, warp, lane, s_off, s_idx, idx,
                             w, out, ldo);
   }
+  // peer stores (the fused forward all-to-all) are made visible system-wide
+  // before the block retires; the host/NCCL barrier after K1 orders them
+  // against the receivers' reads
+  if (out.fence) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------
@@ -749,22 +759,23 @@ std::vector<int4> make_fwd_tiles(const std::vector<TableMeta>& canon,
 
 void launch_tbe_forward(const TableMeta* d_meta_canon, const int4* d_tiles,
                         int64_t n_tiles, int batch, const int32_t* d_off,
-                        const int32_t* d_idx, const float* d_w, float* d_out,
+                        const int32_t* d_idx, const float* d_w, const RowMap& out,
                         int64_t ldo, uint32_t* d_keys, void* d_bags, bool bags16,
                         cudaStream_t st) {
   if (n_tiles <= 0) return;
+  if (out.parts < 1 || out.parts > kMaxPeers) raise(SP_ERR_BAD_INPUT, "bad K1 row map");
   const FwdTile* tiles = reinterpret_cast<const FwdTile*>(d_tiles);
   const unsigned g = static_cast<unsigned>(n_tiles);
   if (!d_keys)
     tbe_forward_kernel<false, uint32_t><<<g, kBlockThreads, 0, st>>>(
-        d_meta_canon, tiles, batch, d_off, d_idx, d_w, d_out, ldo, nullptr, nullptr);
+        d_meta_canon, tiles, batch, d_off, d_idx, d_w, out, ldo, nullptr, nullptr);
   else if (bags16)
     tbe_forward_kernel<true, uint16_t><<<g, kBlockThreads, 0, st>>>(
-        d_meta_canon, tiles, batch, d_off, d_idx, d_w, d_out, ldo, d_keys,
+        d_meta_canon, tiles, batch, d_off, d_idx, d_w, out, ldo, d_keys,
         static_cast<uint16_t*>(d_bags));
   else
     tbe_forward_kernel<true, uint32_t><<<g, kBlockThreads, 0, st>>>(
-        d_meta_canon, tiles, batch, d_off, d_idx, d_w, d_out, ldo, d_keys,
+        d_meta_canon, tiles, batch, d_off, d_idx, d_w, out, ldo, d_keys,
         static_cast<uint32_t*>(d_bags));
   SP_LAUNCHED();
 }

@@ -81,8 +81,11 @@ def test_ctx_argument_errors_before_gpu():
         EmbeddingShard(PlacementTask(tables, 2, cap, 64), [0, 0, 1])
     assert e.value.kind == "memory_violation" and e.value.exit_code == 2
     with pytest.raises(ShardplanError) as e:
-        EmbeddingShard(PlacementTask(tables, 2, 0.0, 64), [0, 1, 1], rank=1, world_size=2)
-    assert e.value.kind == "bad_input"           # multi-rank needs an NCCL id
+        EmbeddingShard(PlacementTask(tables, 2, 0.0, 64), [0, 1, 1], rank=1, world_size=3)
+    assert e.value.kind == "bad_input"           # world_size is 1 (emulation) or D
+    with pytest.raises(ShardplanError) as e:
+        EmbeddingShard(PlacementTask(tables, 2, 0.0, 64), [0, 1, 1], rank=2, world_size=2)
+    assert e.value.kind == "bad_input"           # rank out of range
 
 
 def test_ingest_argument_errors_before_gpu():
