@@ -193,6 +193,7 @@ struct sp_ctx {
   bool peer = false;
   float* peer_recv[sp::kMaxPeers] = {};
   float* peer_gin[sp::kMaxPeers] = {};
+  sp::RowMap* d_rowmap = nullptr;  // K1's peer row map (device), null = local
   std::vector<void*> ipc_opened;
   double* d_bd = nullptr;      // breakdown gather buffer
   int32_t* d_barrier = nullptr;
@@ -354,25 +355,11 @@ bool overlap_active(const sp_ctx* c) {
          c->vdevs[0].nnz > 0;
 }
 
-// Where K1 writes: the local pooled [B, W_v], or — with peer memory — batch
-// slice j straight into rank j's receive slot for this rank (the fused
-// forward all-to-all).
-RowMap fwd_rows(const sp_ctx* c, const VDev& v) {
-  if (!c->peer) return local_rows(v.d_pooled, c->B);
-  RowMap r{};
-  const int64_t R = c->B / c->D;
-  for (int j = 0; j < c->D; ++j) r.base[j] = c->peer_recv[j] + R * c->cumW[c->rank];
-  r.rows_per_part = R;
-  r.parts = c->D;
-  r.fence = 1;
-  return r;
-}
-
 void stage_forward(sp_ctx* c, VDev& v) {
   const bool emit = c->fuse_keys && !v.bucketed && v.nnz > 0 && !overlap_active(c);
   ProfScope prof(c, kProfFwd);
   launch_tbe_forward(v.d_meta_canon, v.d_tiles, v.n_tiles, c->B, v.d_off, v.d_idx,
-                     c->d_w, fwd_rows(c, v), v.W, emit ? v.d_keys : nullptr,
+                     c->d_w, v.d_pooled, c->d_rowmap, v.W, emit ? v.d_keys : nullptr,
                      emit ? v.d_bags : nullptr, c->bags16, c->stream);
   if (emit) v.keys_valid = true;
 }
@@ -569,7 +556,7 @@ void forward_pipelined(sp_ctx* c) {
     {
       ProfScope prof(c, kProfFwd);
       launch_tbe_forward(v.d_meta_canon, v.d_tiles_canon + k0, k1 - k0, c->B, v.d_off,
-                         v.d_idx, c->d_w, fwd_rows(c, v), v.W, v.d_keys, v.d_bags, c->bags16,
+                         v.d_idx, c->d_w, v.d_pooled, c->d_rowmap, v.W, v.d_keys, v.d_bags, c->bags16,
                          c->stream);
     }
     SP_CUDA(cudaEventRecord(c->ev_fork, c->stream));
@@ -974,6 +961,14 @@ int sp_ipc_import(sp_ctx* ctx, const uint8_t* all) {
         (k == 0 ? c->peer_recv : c->peer_gin)[j] = static_cast<float*>(p);
       }
     }
+    // K1's row map: batch slice j -> rank j's receive slot for this rank
+    RowMap rm{};
+    const int64_t R = c->B / c->D;
+    for (int j = 0; j < c->D; ++j) rm.base[j] = c->peer_recv[j] + R * c->cumW[c->rank];
+    rm.rows_per_part = R;
+    rm.parts = c->D;
+    c->d_rowmap = dalloc<RowMap>(1, c->owned, c->dev_bytes);
+    SP_CUDA(cudaMemcpy(c->d_rowmap, &rm, sizeof(rm), cudaMemcpyHostToDevice));
     c->peer = true;
     if (c->graph_exec) {
       cudaGraphExecDestroy(c->graph_exec);
@@ -1636,7 +1631,7 @@ int sp_run_batch(sp_ctx* ctx, const int64_t* offsets, int64_t offsets_len,
       {
         ProfScope prof(c, kProfFwd);
         launch_tbe_forward(v.d_meta_canon, v.d_tiles_canon + k0, k1 - k0, c->B, v.d_off,
-                           v.d_idx, c->d_w, fwd_rows(c, v), v.W, emit ? v.d_keys : nullptr,
+                           v.d_idx, c->d_w, v.d_pooled, c->d_rowmap, v.W, emit ? v.d_keys : nullptr,
                            emit ? v.d_bags : nullptr, c->bags16, st);
       }
       if (t1 == static_cast<int>(v.tables.size())) {

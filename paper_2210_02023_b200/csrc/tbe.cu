@@ -18,6 +18,8 @@
 // sums combine with a fixed xor-shuffle tree: bitwise reproducible.
 #include <cub/cub.cuh>
 
+#include <type_traits>
+
 #include "common.h"
 #include "synth.cuh"
 #include "tbe.h"
@@ -81,20 +83,28 @@ struct Geo {
   static constexpr int S = 32 / P, GB = S / L;
   static_assert(S % L == 0 && GB >= 1, "bad geometry");
 };
-// K1: bags are ~2*pf long; GB*U rows of a bag in flight.
-template <int CLS> struct FwdGeo;
-template <> struct FwdGeo<0> : Geo<1, 1, 8, 4> {};
-template <> struct FwdGeo<1> : Geo<2, 1, 8, 4> {};
-template <> struct FwdGeo<2> : Geo<4, 1, 4, 4> {};
-template <> struct FwdGeo<3> : Geo<8, 1, 2, 4> {};
-template <> struct FwdGeo<4> : Geo<16, 1, 2, 8> {};
-template <> struct FwdGeo<5> : Geo<32, 1, 1, 8> {};
-// K4 SGD: most runs hold 1-2 positions, so more runs per warp (P) matter
-// more than rows per run; lanes move up to 64 B of a row.
-template <int CLS> struct SgdGeo;
 #ifdef SP_GEO_HEADER  // A/B builds: -DSP_GEO_HEADER=\"geo.h\" overriding the knobs below
 #include SP_GEO_HEADER
 #endif
+// K1: bags are ~2*pf long; GB*U rows of a bag in flight.
+#ifndef SP_FWD_G0
+#define SP_FWD_G0 1, 1, 8, 4
+#define SP_FWD_G1 2, 1, 8, 4
+#define SP_FWD_G2 4, 1, 4, 4
+#define SP_FWD_G3 8, 1, 2, 4
+#define SP_FWD_G4 16, 1, 2, 8
+#define SP_FWD_G5 32, 1, 1, 8
+#endif
+template <int CLS> struct FwdGeo;
+template <> struct FwdGeo<0> : Geo<SP_FWD_G0> {};
+template <> struct FwdGeo<1> : Geo<SP_FWD_G1> {};
+template <> struct FwdGeo<2> : Geo<SP_FWD_G2> {};
+template <> struct FwdGeo<3> : Geo<SP_FWD_G3> {};
+template <> struct FwdGeo<4> : Geo<SP_FWD_G4> {};
+template <> struct FwdGeo<5> : Geo<SP_FWD_G5> {};
+// K4 SGD: most runs hold 1-2 positions, so more runs per warp (P) matter
+// more than rows per run; lanes move up to 64 B of a row.
+template <int CLS> struct SgdGeo;
 #ifndef SP_SGD_G0
 // (L, V, P, U) per dim class; tuned on B200 at cfg3 (profiles/r01_notes.md).
 // With the L2 reduction update no register holds the old row, so lanes take
@@ -147,20 +157,26 @@ struct FwdTile {
 constexpr int kTileBags = 256;
 constexpr int kIdxCap = 4096;  // staged indices per tile (16 KB)
 
-__device__ __forceinline__ float* out_row(const RowMap& rm, int64_t b, int64_t ld) {
-  if (rm.parts == 1) return rm.base[0] + b * ld;
-  const int64_t j = b / rm.rows_per_part;
-  return rm.base[j] + (b - j * rm.rows_per_part) * ld;
+// kPeer: a compile-time path, so the local store path stays exactly the
+// plain `out + b * ld` (a runtime branch on a by-value row-map parameter cost
+// K1 6% at cfg3). The peer map lives in device memory.
+template <bool kPeer>
+__device__ __forceinline__ float* out_row(float* out, const RowMap* __restrict__ peer,
+                                          int64_t b, int64_t ld) {
+  if (!kPeer) return out + b * ld;
+  const int64_t j = b / peer->rows_per_part;
+  return peer->base[j] + (b - j * peer->rows_per_part) * ld;
 }
 
-template <class G>
+template <class G, bool kPeer>
 __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb,
                                               int p0, int warp, int lane,
                                               const int32_t* s_off,
                                               const int32_t* s_idx,
                                               const int32_t* __restrict__ idx,
                                               const float* __restrict__ w,
-                                              const RowMap& out,
+                                              float* __restrict__ out,
+                                              const RowMap* __restrict__ peer,
                                               int64_t ldo) {
   constexpr int L = G::L, V = G::V, P = G::P, U = G::U, S = G::S, GB = G::GB;
   const int span = lane / S, ls = lane % S, g = ls / L, s = ls % L;
@@ -201,7 +217,7 @@ __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb
 #pragma unroll
       for (int j = 0; j < V; ++j) acc[j] = f4_add(acc[j], shfl_xor_f4(acc[j], o));
     if (ok && g == 0) {
-      float* o = out_row(out, b0 + bag, ldo) + m.lcol + 4 * s;
+      float* o = out_row<kPeer>(out, peer, b0 + bag, ldo) + m.lcol + 4 * s;
 #pragma unroll
       for (int j = 0; j < V; ++j) __stcs(reinterpret_cast<float4*>(o + 4 * L * j), acc[j]);
     }
@@ -209,10 +225,12 @@ __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb
 }
 
 // Any dim: one warp per bag, 32 scalar columns at a time.
+template <bool kPeer>
 __device__ __forceinline__ void fwd_tile_warp_generic(
     const TableMeta& m, int b0, int nb, int p0, int warp, int lane,
     const int32_t* s_off, const int32_t* s_idx, const int32_t* __restrict__ idx,
-    const float* __restrict__ w, const RowMap& out, int64_t ldo) {
+    const float* __restrict__ w, float* __restrict__ out, const RowMap* __restrict__ peer,
+    int64_t ldo) {
   for (int bag = warp; bag < nb; bag += kWarpsPerBlock) {
     const int beg = s_off[bag] - p0, end = s_off[bag + 1] - p0;
     for (int c0 = 0; c0 < m.dim; c0 += 32) {
@@ -222,20 +240,26 @@ __device__ __forceinline__ void fwd_tile_warp_generic(
         const int r = k < kIdxCap ? s_idx[k] : __ldg(idx + p0 + k);
         if (c < m.dim) acc += __ldg(w + m.woff + static_cast<int64_t>(r) * m.dim + c);
       }
-      if (c < m.dim) out_row(out, b0 + bag, ldo)[m.lcol + c] = acc;
+      if (c < m.dim) out_row<kPeer>(out, peer, b0 + bag, ldo)[m.lcol + c] = acc;
     }
   }
 }
 
 // BagT: the sort payload — uint16_t when the batch fits 16 bits (6-byte
 // pairs through the radix sort instead of 8), else uint32_t.
-template <bool kEmitKeys, class BagT>
-__global__ void __launch_bounds__(kBlockThreads)
+#ifdef SP_FWD_MIN_BLOCKS  // A/B builds; default: ptxas' own choice (32 registers)
+#define SP_FWD_BOUNDS __launch_bounds__(kBlockThreads, SP_FWD_MIN_BLOCKS)
+#else
+#define SP_FWD_BOUNDS __launch_bounds__(kBlockThreads)
+#endif
+template <bool kEmitKeys, class BagT, bool kPeer>
+__global__ void SP_FWD_BOUNDS
     tbe_forward_kernel(const TableMeta* __restrict__ meta,
                        const FwdTile* __restrict__ tiles, int batch,
                        const int32_t* __restrict__ off,
                        const int32_t* __restrict__ idx,
-                       const float* __restrict__ w, const RowMap out,
+                       const float* __restrict__ w, float* __restrict__ out,
+                       const RowMap* __restrict__ peer,
                        int64_t ldo, uint32_t* __restrict__ keys,
                        BagT* __restrict__ bags) {
   __shared__ int32_t s_off[kTileBags + 1];
@@ -266,8 +290,8 @@ __global__ void __launch_bounds__(kBlockThreads)
   switch (m.cls) {
 #define SP_FWD_CASE(C)                                                         \
   case C:                                                                      \
-    fwd_tile_warp<FwdGeo<C>>(m, tile.b0, tile.nb, p0, warp, lane, s_off, s_idx, \
-                             idx, w, out, ldo);                                \
+    fwd_tile_warp<FwdGeo<C>, kPeer>(m, tile.b0, tile.nb, p0, warp, lane, s_off, s_idx, \
+                             idx, w, out, peer, ldo);                          \
     break;
     SP_FWD_CASE(0)
     SP_FWD_CASE(1)
@@ -277,13 +301,13 @@ __global__ void __launch_bounds__(kBlockThreads)
     SP_FWD_CASE(5)
 #undef SP_FWD_CASE
     default:
-      fwd_tile_warp_generic(m, tile.b0, tile.nb, p0, warp, lane, s_off, s_idx, idx,
-                            w, out, ldo);
+      fwd_tile_warp_generic<kPeer>(m, tile.b0, tile.nb, p0, warp, lane, s_off, s_idx, idx,
+                                   w, out, peer, ldo);
   }
   // peer stores (the fused forward all-to-all) are made visible system-wide
   // before the block retires; the host/NCCL barrier after K1 orders them
   // against the receivers' reads
-  if (out.fence) __threadfence_system();
+  if (kPeer) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------
@@ -759,24 +783,28 @@ std::vector<int4> make_fwd_tiles(const std::vector<TableMeta>& canon,
 
 void launch_tbe_forward(const TableMeta* d_meta_canon, const int4* d_tiles,
                         int64_t n_tiles, int batch, const int32_t* d_off,
-                        const int32_t* d_idx, const float* d_w, const RowMap& out,
-                        int64_t ldo, uint32_t* d_keys, void* d_bags, bool bags16,
-                        cudaStream_t st) {
+                        const int32_t* d_idx, const float* d_w, float* d_out,
+                        const RowMap* d_peer, int64_t ldo, uint32_t* d_keys, void* d_bags,
+                        bool bags16, cudaStream_t st) {
   if (n_tiles <= 0) return;
-  if (out.parts < 1 || out.parts > kMaxPeers) raise(SP_ERR_BAD_INPUT, "bad K1 row map");
   const FwdTile* tiles = reinterpret_cast<const FwdTile*>(d_tiles);
   const unsigned g = static_cast<unsigned>(n_tiles);
-  if (!d_keys)
-    tbe_forward_kernel<false, uint32_t><<<g, kBlockThreads, 0, st>>>(
-        d_meta_canon, tiles, batch, d_off, d_idx, d_w, out, ldo, nullptr, nullptr);
-  else if (bags16)
-    tbe_forward_kernel<true, uint16_t><<<g, kBlockThreads, 0, st>>>(
-        d_meta_canon, tiles, batch, d_off, d_idx, d_w, out, ldo, d_keys,
-        static_cast<uint16_t*>(d_bags));
-  else
-    tbe_forward_kernel<true, uint32_t><<<g, kBlockThreads, 0, st>>>(
-        d_meta_canon, tiles, batch, d_off, d_idx, d_w, out, ldo, d_keys,
-        static_cast<uint32_t*>(d_bags));
+  auto go = [&](auto peer) {
+    constexpr bool kPeer = decltype(peer)::value;
+    if (!d_keys)
+      tbe_forward_kernel<false, uint32_t, kPeer><<<g, kBlockThreads, 0, st>>>(
+          d_meta_canon, tiles, batch, d_off, d_idx, d_w, d_out, d_peer, ldo, nullptr, nullptr);
+    else if (bags16)
+      tbe_forward_kernel<true, uint16_t, kPeer><<<g, kBlockThreads, 0, st>>>(
+          d_meta_canon, tiles, batch, d_off, d_idx, d_w, d_out, d_peer, ldo, d_keys,
+          static_cast<uint16_t*>(d_bags));
+    else
+      tbe_forward_kernel<true, uint32_t, kPeer><<<g, kBlockThreads, 0, st>>>(
+          d_meta_canon, tiles, batch, d_off, d_idx, d_w, d_out, d_peer, ldo, d_keys,
+          static_cast<uint32_t*>(d_bags));
+  };
+  if (d_peer) go(std::true_type{});
+  else go(std::false_type{});
   SP_LAUNCHED();
 }
 

@@ -61,32 +61,25 @@ constexpr int kBlockThreads = 32 * kWarpsPerBlock;
 // keys[p] = rowbase_i + idx[p], bags[p] = b.
 // Tiles (x = canonical table, y = first bag, z = bag count) in launch order.
 //
-// Where the pooled rows go: batch rows [j*rows_per_part, (j+1)*rows_per_part)
-// are written to base[j] with row stride ldo. parts = 1 is the local pooled
-// buffer; with peer memory (D ranks, CUDA IPC / NVLink) base[j] is rank j's
-// receive slot for this rank, so K1 itself performs the forward all-to-all
-// (stores to mapped peer addresses) and fences them system-wide (fence = 1).
+// Where the pooled rows go: d_peer == nullptr -> the local pooled buffer
+// d_out [B, ldo]; otherwise (peer memory, D ranks over CUDA IPC / NVLink, a
+// device-resident map) batch rows [j*rows_per_part, (j+1)*rows_per_part) go
+// to base[j], rank j's receive slot for this rank: K1 itself performs the
+// forward all-to-all (stores to mapped peer addresses, fenced system-wide).
 constexpr int kMaxPeers = 8;
 struct RowMap {
   float* base[kMaxPeers];
   int64_t rows_per_part;
   int32_t parts;
-  int32_t fence;
+  int32_t pad;
 };
-inline RowMap local_rows(float* p, int64_t batch) {
-  RowMap r{};
-  r.base[0] = p;
-  r.rows_per_part = batch;
-  r.parts = 1;
-  return r;
-}
 std::vector<int4> make_fwd_tiles(const std::vector<TableMeta>& canon,
                                  const std::vector<int>& order, int batch);
 void launch_tbe_forward(const TableMeta* d_meta_canon, const int4* d_tiles,
                         int64_t n_tiles, int batch, const int32_t* d_off,
-                        const int32_t* d_idx, const float* d_w, const RowMap& out,
-                        int64_t ldo, uint32_t* d_keys, void* d_bags, bool bags16,
-                        cudaStream_t st);
+                        const int32_t* d_idx, const float* d_w, float* d_out,
+                        const RowMap* d_peer, int64_t ldo, uint32_t* d_keys, void* d_bags,
+                        bool bags16, cudaStream_t st);
 
 // ---- K4: backward = keys -> stable radix sort -> runs -> SGD -------------
 void launch_build_keys(const TableMeta* d_meta_canon, int n_tables, int batch,
