@@ -150,8 +150,9 @@ struct sp_ctx {
   int64_t W_total = 0;
   std::vector<sp::VDev> vdevs;
   sp::ExchangePlan plan;       // NCCL mode: this rank's exchange
-  std::vector<int64_t> woff;   // per global table (-1 if not local)
-  float* d_w = nullptr;
+  std::vector<int64_t> woff;   // per global table: element offset (-1 if not local)
+  void* d_w = nullptr;         // weight slab, elements of type wt
+  sp::WeightType wt = sp::WeightType::kF32;
   float* d_recv = nullptr;     // rows_per_dst * W_total per destination
   float* d_gin = nullptr;
   int n_dst = 1;               // destinations held here (D in emulation)
@@ -246,6 +247,11 @@ namespace {
 
 int64_t rows_per_dst(const sp_ctx* c) { return c->B / c->D; }
 
+// Row 0 of global table g in the weight slab.
+void* wptr(const sp_ctx* c, int g) {
+  return static_cast<uint8_t*>(c->d_w) + c->woff[g] * elem_bytes(c->wt);
+}
+
 // Frees and re-allocates the shared sort scratch for n positions.
 void ensure_sort_capacity(sp_ctx* c, int64_t n) {
   if (n <= c->sort_cap && c->d_temp) return;
@@ -277,7 +283,7 @@ void ensure_sort_capacity(sp_ctx* c, int64_t n) {
 void plan_buckets(sp_ctx* c) {
   int64_t need = 0;
   for (auto& v : c->vdevs) {
-    v.bucketed = c->use_buckets && !v.tables.empty() &&
+    v.bucketed = c->use_buckets && c->wt == WeightType::kF32 && !v.tables.empty() &&
                  bucket_plan(v.meta_canon, v.table_nnz, c->B, v.bmeta, v.n_cnt, v.n_btiles,
                              v.n_buckets);
     if (!v.bucketed) continue;
@@ -359,7 +365,7 @@ void stage_forward(sp_ctx* c, VDev& v) {
   const bool emit = c->fuse_keys && !v.bucketed && v.nnz > 0 && !overlap_active(c);
   ProfScope prof(c, kProfFwd);
   launch_tbe_forward(v.d_meta_canon, v.d_tiles, v.n_tiles, c->B, v.d_off, v.d_idx,
-                     c->d_w, v.d_pooled, c->d_rowmap, v.W, emit ? v.d_keys : nullptr,
+                     c->d_w, c->wt, v.d_pooled, c->d_rowmap, v.W, emit ? v.d_keys : nullptr,
                      emit ? v.d_bags : nullptr, c->bags16, c->stream);
   if (emit) v.keys_valid = true;
 }
@@ -412,7 +418,8 @@ void stage_backward_bucketed(sp_ctx* c, VDev& v, uint32_t* sorted_keys, uint32_t
   }
   ProfScope prof(c, kProfSgd);
   launch_bwd_buckets(v.d_meta_canon, v.d_bm, T, v.n_buckets, c->d_cpos, v.nnz, c->d_prow,
-                     c->d_pbag, c->d_scr, v.d_grad, v.W, c->lr, c->d_w, sorted_keys, sorted_bags,
+                     c->d_pbag, c->d_scr, v.d_grad, v.W, c->lr, static_cast<float*>(c->d_w),
+                     sorted_keys, sorted_bags,
                      do_sgd, c->stream);
 }
 
@@ -429,7 +436,7 @@ void stage_backward(sp_ctx* c, VDev& v, bool sorted = false,
   if (!sorted) stage_sort(c, v, c->stream);
   ProfScope prof(c, kProfSgd);
   launch_sgd(v.d_meta_canon, v.d_sgd_tiles, v.n_sgd_tiles, c->d_kb, c->d_bb, c->bags16,
-             v.d_grad, v.W, c->lr, c->d_w, abort_flag, c->stream);
+             v.d_grad, v.W, c->lr, c->d_w, c->wt, abort_flag, c->stream);
 }
 
 // One process per rank (world > 1); the exchange goes through peer memory
@@ -556,7 +563,7 @@ void forward_pipelined(sp_ctx* c) {
     {
       ProfScope prof(c, kProfFwd);
       launch_tbe_forward(v.d_meta_canon, v.d_tiles_canon + k0, k1 - k0, c->B, v.d_off,
-                         v.d_idx, c->d_w, v.d_pooled, c->d_rowmap, v.W, v.d_keys, v.d_bags, c->bags16,
+                         v.d_idx, c->d_w, c->wt, v.d_pooled, c->d_rowmap, v.W, v.d_keys, v.d_bags, c->bags16,
                          c->stream);
     }
     SP_CUDA(cudaEventRecord(c->ev_fork, c->stream));
@@ -755,7 +762,31 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
     else
       held.push_back(rank);
 
+    // Storage type from the tables' own sizing: table_size_gb =
+    // rows * dim * bytes_per_param / 2^30 (table_memory_gb, table.hpp:55-63):
+    // 2 B/param (the reference's default, the paper's fp16 tables) -> fp16,
+    // 4 B/param -> fp32; one type per context.
+    {
+      int bpp_all = 0;
+      for (int i = 0; i < num_tables; ++i) {
+        const sp_table_spec& t = tables[i];
+        if (!(t.table_size_gb > 0.0)) continue;  // unsized: fp32
+        const double bpp = t.table_size_gb * 1073741824.0 /
+                           (static_cast<double>(t.hash_size) * static_cast<double>(t.dim));
+        const int b = std::fabs(bpp - 2.0) < 0.5 ? 2 : (std::fabs(bpp - 4.0) < 1.0 ? 4 : 0);
+        if (b == 0)
+          raise(SP_ERR_BAD_INPUT, "table " + std::to_string(i) + " is sized at " +
+                                      std::to_string(bpp) +
+                                      " bytes/param: only 2 (fp16) or 4 (fp32) are stored");
+        if (bpp_all != 0 && b != bpp_all)
+          raise(SP_ERR_BAD_INPUT, "tables mix 2 and 4 bytes/param");
+        bpp_all = b;
+      }
+      c->wt = bpp_all == 2 ? WeightType::kF16 : WeightType::kF32;
+    }
     // Weight slab.
+    const int64_t eb = elem_bytes(c->wt);
+    const int64_t align = 256 / eb;  // elements per 256 bytes
     c->woff.assign(num_tables, -1);
     int64_t slab = 0;
     for (int d : held)
@@ -766,9 +797,9 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
           // 256-byte aligned table bases: with dim a multiple of 16, every
           // row starts on a 64-byte DRAM burst (a 16-byte aligned base can
           // make each 64-byte row straddle two bursts)
-          slab = (slab + 63) & ~int64_t(63);
+          slab = (slab + align - 1) / align * align;
         }
-    c->d_w = dalloc<float>(slab, c->owned, c->dev_bytes);
+    c->d_w = dalloc<uint8_t>(slab * eb, c->owned, c->dev_bytes);
 
     const int64_t R = static_cast<int64_t>(batch_size) / num_devices;
     for (int d : held) {
@@ -812,7 +843,7 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
         m.dim = t.dim;
         m.lcol = static_cast<int32_t>(lcol);
         m.rowbase = static_cast<uint32_t>(rb);
-        m.cls = dim_class(t.dim);
+        m.cls = row_class(t.dim, c->wt);
         m.local = li;
         m.gid = g;
         v.meta_canon.push_back(m);
@@ -1021,7 +1052,7 @@ int sp_init_tables(sp_ctx* ctx, uint64_t seed) {
     check_ctx(ctx);
     for (auto& v : ctx->vdevs)
       for (int g : v.tables)
-        launch_init_weights(ctx->d_w + ctx->woff[g], ctx->tables[g].hash_size,
+        launch_init_weights(wptr(ctx, g), ctx->wt, ctx->tables[g].hash_size,
                             ctx->tables[g].dim, g, seed, ctx->stream);
     SP_CUDA(cudaStreamSynchronize(ctx->stream));
   });
@@ -1033,9 +1064,18 @@ int sp_set_table(sp_ctx* ctx, int32_t table_id, const float* rows) {
     if (table_id < 0 || table_id >= ctx->M || ctx->woff[table_id] < 0)
       raise(SP_ERR_UNKNOWN_TABLE, "table id " + std::to_string(table_id) + " is not local");
     const auto& t = ctx->tables[table_id];
-    SP_CUDA(cudaMemcpyAsync(ctx->d_w + ctx->woff[table_id], rows,
-                            t.hash_size * t.dim * sizeof(float),
-                            cudaMemcpyHostToDevice, ctx->stream));
+    const int64_t n = t.hash_size * t.dim;
+    if (ctx->wt == WeightType::kF32) {
+      SP_CUDA(cudaMemcpyAsync(wptr(ctx, table_id), rows, n * sizeof(float),
+                              cudaMemcpyHostToDevice, ctx->stream));
+    } else {
+      float* tmp = nullptr;
+      SP_CUDA(cudaMalloc(&tmp, std::max<int64_t>(n, 1) * sizeof(float)));
+      SP_CUDA(cudaMemcpyAsync(tmp, rows, n * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+      launch_f32_to_weights(tmp, wptr(ctx, table_id), ctx->wt, n, ctx->stream);
+      SP_CUDA(cudaStreamSynchronize(ctx->stream));
+      cudaFree(tmp);
+    }
     SP_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -1046,9 +1086,18 @@ int sp_get_table(sp_ctx* ctx, int32_t table_id, float* rows) {
     if (table_id < 0 || table_id >= ctx->M || ctx->woff[table_id] < 0)
       raise(SP_ERR_UNKNOWN_TABLE, "table id " + std::to_string(table_id) + " is not local");
     const auto& t = ctx->tables[table_id];
-    SP_CUDA(cudaMemcpyAsync(rows, ctx->d_w + ctx->woff[table_id],
-                            t.hash_size * t.dim * sizeof(float),
-                            cudaMemcpyDeviceToHost, ctx->stream));
+    const int64_t n = t.hash_size * t.dim;
+    if (ctx->wt == WeightType::kF32) {
+      SP_CUDA(cudaMemcpyAsync(rows, wptr(ctx, table_id), n * sizeof(float),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    } else {
+      float* tmp = nullptr;
+      SP_CUDA(cudaMalloc(&tmp, std::max<int64_t>(n, 1) * sizeof(float)));
+      launch_weights_to_f32(wptr(ctx, table_id), ctx->wt, tmp, n, ctx->stream);
+      SP_CUDA(cudaMemcpyAsync(rows, tmp, n * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+      SP_CUDA(cudaStreamSynchronize(ctx->stream));
+      cudaFree(tmp);
+    }
     SP_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -1631,7 +1680,7 @@ int sp_run_batch(sp_ctx* ctx, const int64_t* offsets, int64_t offsets_len,
       {
         ProfScope prof(c, kProfFwd);
         launch_tbe_forward(v.d_meta_canon, v.d_tiles_canon + k0, k1 - k0, c->B, v.d_off,
-                           v.d_idx, c->d_w, v.d_pooled, c->d_rowmap, v.W, emit ? v.d_keys : nullptr,
+                           v.d_idx, c->d_w, c->wt, v.d_pooled, c->d_rowmap, v.W, emit ? v.d_keys : nullptr,
                            emit ? v.d_bags : nullptr, c->bags16, st);
       }
       if (t1 == static_cast<int>(v.tables.size())) {
@@ -1786,12 +1835,14 @@ int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]) {
     //      kernel also re-reads rows for its histogram: +4 B)
     //  [3] sort / partition: CUB 16 B/lookup/pass; bucketed: ids twice +
     //      pair write (8+8 B/lookup) + offsets
+    // (row bytes use the storage type: 2 B/param for fp16 tables)
     double fwd = 0, a2a = 0, sgd = 0, sort = 0;
+    const double eb = elem_bytes(c->wt);
     for (auto& v : c->vdevs) {
       const int T = static_cast<int>(v.tables.size());
       double rows_bytes = 0;
       for (int li = 0; li < T; ++li)
-        rows_bytes += 4.0 * static_cast<double>(v.table_nnz[li]) * c->tables[v.tables[li]].dim;
+        rows_bytes += eb * static_cast<double>(v.table_nnz[li]) * c->tables[v.tables[li]].dim;
       const double offs = 4.0 * (static_cast<double>(T) * c->B + 1);
       const double csr = offs + 4.0 * v.nnz;
       const double outb = 4.0 * c->B * v.W;
@@ -1812,7 +1863,7 @@ int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]) {
             uniq_dim += c->tables[v.tables[li]].dim;
           }
       }
-      sgd = std::max(sgd, outb + 8.0 * uniq_dim + (v.bucketed ? 12.0 : pair) * v.nnz);
+      sgd = std::max(sgd, outb + 2.0 * eb * uniq_dim + (v.bucketed ? 12.0 : pair) * v.nnz);
       double sort_dev = 0;
       if (v.bucketed)
         sort_dev = 2.0 * csr + 8.0 * v.nnz + 8.0 * v.n_cnt;

@@ -143,6 +143,35 @@ template <> struct LongGeo<2> : Geo<SP_LONG_G2> {};
 template <> struct LongGeo<3> : Geo<SP_LONG_G3> {};
 template <> struct LongGeo<4> : Geo<SP_LONG_G4> {};
 template <> struct LongGeo<5> : Geo<SP_LONG_G5> {};
+// fp16 rows: a 16-byte slice widens to 8 fp32 values (twice the registers of
+// an fp32 slice), so fewer slices per lane / rows in flight per class.
+template <int CLS> struct FwdGeoH;
+template <> struct FwdGeoH<0> : Geo<1, 1, 8, 2> {};
+template <> struct FwdGeoH<1> : Geo<2, 1, 8, 2> {};
+template <> struct FwdGeoH<2> : Geo<4, 1, 4, 2> {};
+template <> struct FwdGeoH<3> : Geo<8, 1, 2, 2> {};
+template <> struct FwdGeoH<4> : Geo<16, 1, 2, 4> {};
+template <> struct FwdGeoH<5> : Geo<32, 1, 1, 4> {};
+template <int CLS> struct SgdGeoH;
+template <> struct SgdGeoH<0> : Geo<1, 1, 16, 1> {};
+template <> struct SgdGeoH<1> : Geo<2, 1, 16, 1> {};
+template <> struct SgdGeoH<2> : Geo<4, 1, 8, 1> {};
+template <> struct SgdGeoH<3> : Geo<8, 1, 4, 1> {};
+template <> struct SgdGeoH<4> : Geo<8, 2, 4, 1> {};
+template <> struct SgdGeoH<5> : Geo<16, 2, 2, 1> {};
+template <int CLS> struct LongGeoH;
+template <> struct LongGeoH<0> : Geo<1, 1, 1, 2> {};
+template <> struct LongGeoH<1> : Geo<2, 1, 1, 2> {};
+template <> struct LongGeoH<2> : Geo<4, 1, 1, 2> {};
+template <> struct LongGeoH<3> : Geo<8, 1, 1, 2> {};
+template <> struct LongGeoH<4> : Geo<16, 1, 1, 4> {};
+template <> struct LongGeoH<5> : Geo<32, 1, 1, 4> {};
+template <int C, class T>
+using FwdG = std::conditional_t<std::is_same<T, float>::value, FwdGeo<C>, FwdGeoH<C>>;
+template <int C, class T>
+using SgdG = std::conditional_t<std::is_same<T, float>::value, SgdGeo<C>, SgdGeoH<C>>;
+template <int C, class T>
+using LongG = std::conditional_t<std::is_same<T, float>::value, LongGeo<C>, LongGeoH<C>>;
 
 // ---------------------------------------------------------------------------
 // K1
@@ -157,6 +186,56 @@ struct FwdTile {
 constexpr int kTileBags = 256;
 constexpr int kIdxCap = 4096;  // staged indices per tile (16 KB)
 
+// 16-byte slices of a table row of element type T, widened to fp32 (K1) and
+// the matching L2 vector reduction for the row update (K4): fp32 tables
+// (the bench's 4 B/param pools) and fp16 tables (the paper's, PAPER.md:709,
+// and the reference's default 2 B/param sizing, table.hpp:30).
+template <class T> struct TypeTag { using type = T; };
+template <class T> struct Slice;
+template <> struct Slice<float> {
+  static constexpr int E = 4;
+  __device__ static __forceinline__ void load(const float* p, float (&v)[4]) {
+    const float4 x = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  }
+  __device__ static __forceinline__ void red_add(float* p, const float (&d)[4]) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(d[0]),
+                 "f"(d[1]), "f"(d[2]), "f"(d[3])
+                 : "memory");
+  }
+  __device__ static __forceinline__ float to_f(float x) { return x; }
+  __device__ static __forceinline__ void red_add1(float* p, float d) { atomicAdd(p, d); }
+};
+template <> struct Slice<__half> {
+  static constexpr int E = 8;
+  __device__ static __forceinline__ void load(const __half* p, float (&v)[8]) {
+    const uint4 x = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[k]));
+      v[2 * k] = f.x;
+      v[2 * k + 1] = f.y;
+    }
+  }
+  // W += fp16(d), round-to-nearest at L2 (REDG.ADD.F16x8)
+  __device__ static __forceinline__ void red_add(__half* p, const float (&d)[8]) {
+    uint32_t u[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const __half2 h = __floats2half2_rn(d[2 * k], d[2 * k + 1]);
+      u[k] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    asm volatile("red.global.add.noftz.v4.f16x2 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(u[0]),
+                 "r"(u[1]), "r"(u[2]), "r"(u[3])
+                 : "memory");
+  }
+  __device__ static __forceinline__ float to_f(__half x) { return __half2float(x); }
+  __device__ static __forceinline__ void red_add1(__half* p, float d) {
+    atomicAdd(p, __float2half_rn(d));
+  }
+};
+
 // kPeer: a compile-time path, so the local store path stays exactly the
 // plain `out + b * ld` (a runtime branch on a by-value row-map parameter cost
 // K1 6% at cfg3). The peer map lives in device memory.
@@ -168,19 +247,20 @@ __device__ __forceinline__ float* out_row(float* out, const RowMap* __restrict__
   return peer->base[j] + (b - j * peer->rows_per_part) * ld;
 }
 
-template <class G, bool kPeer>
+template <class G, bool kPeer, class T>
 __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb,
                                               int p0, int warp, int lane,
                                               const int32_t* s_off,
                                               const int32_t* s_idx,
                                               const int32_t* __restrict__ idx,
-                                              const float* __restrict__ w,
+                                              const T* __restrict__ w,
                                               float* __restrict__ out,
                                               const RowMap* __restrict__ peer,
                                               int64_t ldo) {
   constexpr int L = G::L, V = G::V, P = G::P, U = G::U, S = G::S, GB = G::GB;
+  constexpr int E = Slice<T>::E;
   const int span = lane / S, ls = lane % S, g = ls / L, s = ls % L;
-  const float* wt = w + m.woff + 4 * s;  // lane s moves float4 s, s+L, s+2L, ... (coalesced)
+  const T* wt = w + m.woff + E * s;  // lane s moves slices s, s+L, s+2L, ... (coalesced)
   const int dim = m.dim;
   for (int bg = warp * P; bg < nb; bg += kWarpsPerBlock * P) {
     const int bag = bg + span;
@@ -190,9 +270,11 @@ __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb
       beg = s_off[bag] - p0;
       end = s_off[bag + 1] - p0;
     }
-    float4 acc[V];
+    float acc[V][E];
 #pragma unroll
-    for (int j = 0; j < V; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < V; ++j)
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[j][e] = 0.f;
     for (int k = beg + g; k < end; k += GB * U) {
       int r[U];
 #pragma unroll
@@ -200,36 +282,49 @@ __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb
         const int kk = k + u * GB;
         r[u] = kk < end ? (kk < kIdxCap ? s_idx[kk] : __ldg(idx + p0 + kk)) : -1;
       }
-      float4 v[U][V];
+      float v[U][V][E];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          if (r[u] >= 0) {
+            Slice<T>::load(wt + static_cast<int64_t>(r[u]) * dim + E * L * j, v[u][j]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[u][j][e] = 0.f;
+          }
+        }
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int j = 0; j < V; ++j)
-          v[u][j] = r[u] >= 0 ? ldg_f4(wt + static_cast<int64_t>(r[u]) * dim + 4 * L * j)
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int j = 0; j < V; ++j) acc[j] = f4_add(acc[j], v[u][j]);
+          for (int e = 0; e < E; ++e) acc[j][e] += v[u][j][e];
     }
 #pragma unroll
     for (int o = L; o < S; o <<= 1)
 #pragma unroll
-      for (int j = 0; j < V; ++j) acc[j] = f4_add(acc[j], shfl_xor_f4(acc[j], o));
-    if (ok && g == 0) {
-      float* o = out_row<kPeer>(out, peer, b0 + bag, ldo) + m.lcol + 4 * s;
+      for (int j = 0; j < V; ++j)
 #pragma unroll
-      for (int j = 0; j < V; ++j) __stcs(reinterpret_cast<float4*>(o + 4 * L * j), acc[j]);
+        for (int e = 0; e < E; ++e) acc[j][e] += __shfl_xor_sync(0xffffffffu, acc[j][e], o);
+    if (ok && g == 0) {
+      float* o = out_row<kPeer>(out, peer, b0 + bag, ldo) + m.lcol + E * s;
+#pragma unroll
+      for (int j = 0; j < V; ++j)
+#pragma unroll
+        for (int e = 0; e < E; e += 4)
+          __stcs(reinterpret_cast<float4*>(o + E * L * j + e),
+                 make_float4(acc[j][e], acc[j][e + 1], acc[j][e + 2], acc[j][e + 3]));
     }
   }
 }
 
 // Any dim: one warp per bag, 32 scalar columns at a time.
-template <bool kPeer>
+template <bool kPeer, class T>
 __device__ __forceinline__ void fwd_tile_warp_generic(
     const TableMeta& m, int b0, int nb, int p0, int warp, int lane,
     const int32_t* s_off, const int32_t* s_idx, const int32_t* __restrict__ idx,
-    const float* __restrict__ w, float* __restrict__ out, const RowMap* __restrict__ peer,
+    const T* __restrict__ w, float* __restrict__ out, const RowMap* __restrict__ peer,
     int64_t ldo) {
   for (int bag = warp; bag < nb; bag += kWarpsPerBlock) {
     const int beg = s_off[bag] - p0, end = s_off[bag + 1] - p0;
@@ -238,7 +333,7 @@ __device__ __forceinline__ void fwd_tile_warp_generic(
       float acc = 0.f;
       for (int k = beg; k < end; ++k) {
         const int r = k < kIdxCap ? s_idx[k] : __ldg(idx + p0 + k);
-        if (c < m.dim) acc += __ldg(w + m.woff + static_cast<int64_t>(r) * m.dim + c);
+        if (c < m.dim) acc += Slice<T>::to_f(w[m.woff + static_cast<int64_t>(r) * m.dim + c]);
       }
       if (c < m.dim) out_row<kPeer>(out, peer, b0 + bag, ldo)[m.lcol + c] = acc;
     }
@@ -252,13 +347,13 @@ __device__ __forceinline__ void fwd_tile_warp_generic(
 #else
 #define SP_FWD_BOUNDS __launch_bounds__(kBlockThreads)
 #endif
-template <bool kEmitKeys, class BagT, bool kPeer>
+template <bool kEmitKeys, class BagT, bool kPeer, class T>
 __global__ void SP_FWD_BOUNDS
     tbe_forward_kernel(const TableMeta* __restrict__ meta,
                        const FwdTile* __restrict__ tiles, int batch,
                        const int32_t* __restrict__ off,
                        const int32_t* __restrict__ idx,
-                       const float* __restrict__ w, float* __restrict__ out,
+                       const T* __restrict__ w, float* __restrict__ out,
                        const RowMap* __restrict__ peer,
                        int64_t ldo, uint32_t* __restrict__ keys,
                        BagT* __restrict__ bags) {
@@ -290,7 +385,7 @@ __global__ void SP_FWD_BOUNDS
   switch (m.cls) {
 #define SP_FWD_CASE(C)                                                         \
   case C:                                                                      \
-    fwd_tile_warp<FwdGeo<C>, kPeer>(m, tile.b0, tile.nb, p0, warp, lane, s_off, s_idx, \
+    fwd_tile_warp<FwdG<C, T>, kPeer, T>(m, tile.b0, tile.nb, p0, warp, lane, s_off, s_idx, \
                              idx, w, out, peer, ldo);                          \
     break;
     SP_FWD_CASE(0)
@@ -301,7 +396,7 @@ __global__ void SP_FWD_BOUNDS
     SP_FWD_CASE(5)
 #undef SP_FWD_CASE
     default:
-      fwd_tile_warp_generic<kPeer>(m, tile.b0, tile.nb, p0, warp, lane, s_off, s_idx, idx,
+      fwd_tile_warp_generic<kPeer, T>(m, tile.b0, tile.nb, p0, warp, lane, s_off, s_idx, idx,
                                    w, out, peer, ldo);
   }
   // peer stores (the fused forward all-to-all) are made visible system-wide
@@ -395,7 +490,7 @@ struct SgdShared {
   uint16_t srun[kTilePos];      // short runs: beg | len << 11
   uint16_t lbeg[kMaxLong];      // long runs: first position (tile-relative)
   int32_t lend[kMaxLong];       //            one past the last (may pass np)
-  alignas(16) float part[kWarpsPerBlock][128];
+  alignas(16) float part[kWarpsPerBlock][256];  // one row: <= 512 B of fp32 or fp16
   int nshort, nlong, next;
 };
 
@@ -405,26 +500,39 @@ __device__ __forceinline__ uint32_t sgd_bag(const SgdShared<BagT>& sh, int i, in
   return i < np ? static_cast<uint32_t>(sh.bag[i]) : static_cast<uint32_t>(__ldg(bags + p0 + i));
 }
 
+// Gradient columns of one 16-byte weight slice (E fp32 values, E/4 float4).
+template <int E>
+__device__ __forceinline__ void load_grad(const float* p, float (&v)[E]) {
+#pragma unroll
+  for (int e = 0; e < E; e += 4) {
+    const float4 x = ldg_f4(p + e);
+    v[e] = x.x; v[e + 1] = x.y; v[e + 2] = x.z; v[e + 3] = x.w;
+  }
+}
+
 // One round of up to P short runs [j, jend) of the tile (span s: run j+s).
-template <class G, class BagT>
+template <class G, class BagT, class T>
 __device__ __forceinline__ void sgd_short_round(const TableMeta& m, int j, int jend, int np,
                                                 int p0, int lane, const SgdShared<BagT>& sh,
                                                 const BagT* __restrict__ bags,
                                                 const float* __restrict__ grad, int64_t ldg,
-                                                float lr, float* __restrict__ w) {
+                                                float lr, T* __restrict__ w) {
   constexpr int L = G::L, V = G::V, U = G::U, S = G::S, GB = G::GB;
+  constexpr int E = Slice<T>::E;
   const int span = lane / S, ls = lane % S, g = ls / L, sub = ls % L;
   const int u = j + span;
   const bool active = u < jend;
-  float4 acc[V];
+  float acc[V][E];
 #pragma unroll
-  for (int c = 0; c < V; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int c = 0; c < V; ++c)
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[c][e] = 0.f;
   int beg = 0;
   if (active) {
     const uint32_t pk = sh.srun[u];
     beg = static_cast<int>(pk & 2047u);
     const int end = beg + static_cast<int>(pk >> 11);
-    const float* gcol = grad + m.lcol + 4 * sub;
+    const float* gcol = grad + m.lcol + E * sub;
     for (int k = beg + g; k < end; k += GB * U) {
       uint32_t bg[U];
 #pragma unroll
@@ -432,49 +540,63 @@ __device__ __forceinline__ void sgd_short_round(const TableMeta& m, int j, int j
         const int kk = k + q * GB;
         bg[q] = kk < end ? sgd_bag(sh, kk, np, p0, bags) : 0xffffffffu;
       }
-      float4 v[U][V];
+      float v[U][V][E];
+#pragma unroll
+      for (int q = 0; q < U; ++q)
+#pragma unroll
+        for (int c = 0; c < V; ++c) {
+          if (bg[q] != 0xffffffffu) {
+            load_grad<E>(gcol + static_cast<int64_t>(bg[q]) * ldg + E * L * c, v[q][c]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[q][c][e] = 0.f;
+          }
+        }
 #pragma unroll
       for (int q = 0; q < U; ++q)
 #pragma unroll
         for (int c = 0; c < V; ++c)
-          v[q][c] = bg[q] != 0xffffffffu
-                        ? ldg_f4(gcol + static_cast<int64_t>(bg[q]) * ldg + 4 * L * c)
-                        : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int q = 0; q < U; ++q)
-#pragma unroll
-        for (int c = 0; c < V; ++c) acc[c] = f4_add(acc[c], v[q][c]);
+          for (int e = 0; e < E; ++e) acc[c][e] += v[q][c][e];
     }
   }
 #pragma unroll
   for (int o = L; o < S; o <<= 1)
 #pragma unroll
-    for (int c = 0; c < V; ++c) acc[c] = f4_add(acc[c], shfl_xor_f4(acc[c], o));
-  if (active && g == 0) {
-    float* wrow = w + m.woff + static_cast<int64_t>(sh.row[beg]) * m.dim + 4 * sub;
-#pragma unroll
     for (int c = 0; c < V; ++c)
-      red_add_f4(wrow + 4 * L * c, make_float4(-lr * acc[c].x, -lr * acc[c].y,
-                                               -lr * acc[c].z, -lr * acc[c].w));
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[c][e] += __shfl_xor_sync(0xffffffffu, acc[c][e], o);
+  if (active && g == 0) {
+    T* wrow = w + m.woff + static_cast<int64_t>(sh.row[beg]) * m.dim + E * sub;
+#pragma unroll
+    for (int c = 0; c < V; ++c) {
+      float d[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) d[e] = -lr * acc[c][e];
+      Slice<T>::red_add(wrow + E * L * c, d);
+    }
   }
 }
 
 // Long run [beg, end): warp `warp` sums its fixed slice into part[warp].
-template <class G, class BagT>
+template <class G, class BagT, class T>
 __device__ __forceinline__ void sgd_long_slice(const TableMeta& m, int beg, int end, int np,
                                                int p0, int warp, int lane,
                                                SgdShared<BagT>& sh,
                                                const BagT* __restrict__ bags,
                                                const float* __restrict__ grad, int64_t ldg) {
   constexpr int L = G::L, V = G::V, U = G::U, GB = G::GB;
+  constexpr int E = Slice<T>::E;
   const int g = lane / L, sub = lane % L;
   const int len = end - beg;
   const int per = (len + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int s0 = beg + min(len, warp * per), s1 = beg + min(len, (warp + 1) * per);
-  float4 acc[V];
+  float acc[V][E];
 #pragma unroll
-  for (int c = 0; c < V; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-  const float* gcol = grad + m.lcol + 4 * sub;
+  for (int c = 0; c < V; ++c)
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[c][e] = 0.f;
+  const float* gcol = grad + m.lcol + E * sub;
   for (int k = s0 + g; k < s1; k += GB * U) {
     uint32_t bg[U];
 #pragma unroll
@@ -482,51 +604,71 @@ __device__ __forceinline__ void sgd_long_slice(const TableMeta& m, int beg, int 
       const int kk = k + q * GB;
       bg[q] = kk < s1 ? sgd_bag(sh, kk, np, p0, bags) : 0xffffffffu;
     }
-    float4 v[U][V];
+    float v[U][V][E];
+#pragma unroll
+    for (int q = 0; q < U; ++q)
+#pragma unroll
+      for (int c = 0; c < V; ++c) {
+        if (bg[q] != 0xffffffffu) {
+          load_grad<E>(gcol + static_cast<int64_t>(bg[q]) * ldg + E * L * c, v[q][c]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e) v[q][c][e] = 0.f;
+        }
+      }
 #pragma unroll
     for (int q = 0; q < U; ++q)
 #pragma unroll
       for (int c = 0; c < V; ++c)
-        v[q][c] = bg[q] != 0xffffffffu
-                      ? ldg_f4(gcol + static_cast<int64_t>(bg[q]) * ldg + 4 * L * c)
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int q = 0; q < U; ++q)
-#pragma unroll
-      for (int c = 0; c < V; ++c) acc[c] = f4_add(acc[c], v[q][c]);
+        for (int e = 0; e < E; ++e) acc[c][e] += v[q][c][e];
   }
 #pragma unroll
   for (int o = L; o < 32; o <<= 1)
 #pragma unroll
-    for (int c = 0; c < V; ++c) acc[c] = f4_add(acc[c], shfl_xor_f4(acc[c], o));
+    for (int c = 0; c < V; ++c)
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[c][e] += __shfl_xor_sync(0xffffffffu, acc[c][e], o);
   if (g == 0)
 #pragma unroll
     for (int c = 0; c < V; ++c)
-      *reinterpret_cast<float4*>(&sh.part[warp][4 * sub + 4 * L * c]) = acc[c];
+#pragma unroll
+      for (int e = 0; e < E; e += 4)
+        *reinterpret_cast<float4*>(&sh.part[warp][E * sub + E * L * c + e]) =
+            make_float4(acc[c][e], acc[c][e + 1], acc[c][e + 2], acc[c][e + 3]);
 }
 
-// Short-run (SG) and long-run (LG) geometries of one dim class.
-template <class SG, class LG, class BagT>
+// Short-run (SG) and long-run (LG) geometries of one row class.
+template <class SG, class LG, class BagT, class T>
 __device__ __forceinline__ void sgd_tile(const TableMeta& m, const SgdTile& tile,
                                          SgdShared<BagT>& sh,
                                          const BagT* __restrict__ bags,
                                          const float* __restrict__ grad, int64_t ldg,
-                                         float lr, float* __restrict__ w) {
+                                         float lr, T* __restrict__ w) {
+  constexpr int E = Slice<T>::E;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int np = tile.np, p0 = tile.p0;
   // long runs first: all warps cooperate, two barriers per run
   for (int r = 0; r < sh.nlong; ++r) {
     const int beg = sh.lbeg[r], end = sh.lend[r];
-    sgd_long_slice<LG>(m, beg, end, np, p0, warp, lane, sh, bags, grad, ldg);
+    sgd_long_slice<LG, BagT, T>(m, beg, end, np, p0, warp, lane, sh, bags, grad, ldg);
     __syncthreads();
     if (warp == 0) {
-      float* wrow = w + m.woff + static_cast<int64_t>(sh.row[beg]) * m.dim;
-      for (int c = 4 * lane; c < m.dim; c += 128) {
-        float4 s = *reinterpret_cast<const float4*>(&sh.part[0][c]);
+      T* wrow = w + m.woff + static_cast<int64_t>(sh.row[beg]) * m.dim;
+      for (int c = E * lane; c < m.dim; c += 32 * E) {
+        float d[E];
 #pragma unroll
-        for (int q = 1; q < kWarpsPerBlock; ++q)
-          s = f4_add(s, *reinterpret_cast<const float4*>(&sh.part[q][c]));
-        red_add_f4(wrow + c, make_float4(-lr * s.x, -lr * s.y, -lr * s.z, -lr * s.w));
+        for (int e = 0; e < E; e += 4) {
+          float4 sum = *reinterpret_cast<const float4*>(&sh.part[0][c + e]);
+#pragma unroll
+          for (int q = 1; q < kWarpsPerBlock; ++q)
+            sum = f4_add(sum, *reinterpret_cast<const float4*>(&sh.part[q][c + e]));
+          d[e] = -lr * sum.x;
+          d[e + 1] = -lr * sum.y;
+          d[e + 2] = -lr * sum.z;
+          d[e + 3] = -lr * sum.w;
+        }
+        Slice<T>::red_add(wrow + c, d);
       }
     }
     __syncthreads();
@@ -540,16 +682,16 @@ __device__ __forceinline__ void sgd_tile(const TableMeta& m, const SgdTile& tile
     if (j0 >= ns) break;
     const int jend = min(ns, j0 + kRunChunk);
     for (int j = j0; j < jend; j += SG::P)
-      sgd_short_round<SG>(m, j, jend, np, p0, lane, sh, bags, grad, ldg, lr, w);
+      sgd_short_round<SG, BagT, T>(m, j, jend, np, p0, lane, sh, bags, grad, ldg, lr, w);
   }
 }
 
-// Any dim (not a power of two in 4..128): a warp per run, 32 columns at a
-// time, positions in sorted order.
-template <class BagT>
+// Any other row size: a warp per run, 32 columns at a time, positions in
+// sorted order.
+template <class BagT, class T>
 __device__ void sgd_tile_generic(const TableMeta& m, const SgdTile& tile, SgdShared<BagT>& sh,
                                  const BagT* __restrict__ bags, const float* __restrict__ grad,
-                                 int64_t ldg, float lr, float* __restrict__ w) {
+                                 int64_t ldg, float lr, T* __restrict__ w) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nrun = sh.nshort + sh.nlong;
   for (int r = warp; r < nrun; r += kWarpsPerBlock) {
@@ -561,13 +703,13 @@ __device__ void sgd_tile_generic(const TableMeta& m, const SgdTile& tile, SgdSha
       beg = sh.lbeg[r - sh.nshort];
       end = sh.lend[r - sh.nshort];
     }
-    float* wrow = w + m.woff + static_cast<int64_t>(sh.row[beg]) * m.dim;
+    T* wrow = w + m.woff + static_cast<int64_t>(sh.row[beg]) * m.dim;
     for (int c = lane; c < m.dim; c += 32) {
       float acc = 0.f;
       for (int k = beg; k < end; ++k)
         acc += __ldg(grad + static_cast<int64_t>(sgd_bag(sh, k, tile.np, tile.p0, bags)) * ldg +
                      m.lcol + c);
-      atomicAdd(wrow + c, -lr * acc);
+      Slice<T>::red_add1(wrow + c, -lr * acc);
     }
   }
 }
@@ -575,12 +717,12 @@ __device__ void sgd_tile_generic(const TableMeta& m, const SgdTile& tile, SgdSha
 #ifndef SP_SGD_MIN_BLOCKS
 #define SP_SGD_MIN_BLOCKS 4  // 4 x 256 threads per SM: <= 64 registers
 #endif
-template <class BagT>
+template <class BagT, class T>
 __global__ void __launch_bounds__(kBlockThreads, SP_SGD_MIN_BLOCKS)
     sgd_kernel(const TableMeta* __restrict__ meta, const SgdTile* __restrict__ tiles,
                const uint32_t* __restrict__ keys, const BagT* __restrict__ bags,
                const float* __restrict__ grad, int64_t ldg, float lr,
-               float* __restrict__ w, const int32_t* __restrict__ abort_flag) {
+               T* __restrict__ w, const int32_t* __restrict__ abort_flag) {
   if (abort_flag != nullptr && *abort_flag != 0) return;  // invalid batch: no update
   __shared__ SgdShared<BagT> sh;
   using BlockScan = cub::BlockScan<int, kBlockThreads>;
@@ -660,7 +802,7 @@ __global__ void __launch_bounds__(kBlockThreads, SP_SGD_MIN_BLOCKS)
   switch (m.cls) {
 #define SP_SGD_CASE(C)                                                          \
   case C:                                                                       \
-    sgd_tile<SgdGeo<C>, LongGeo<C>>(m, tile, sh, bags, grad, ldg, lr, w);       \
+    sgd_tile<SgdG<C, T>, LongG<C, T>, BagT, T>(m, tile, sh, bags, grad, ldg, lr, w); \
     break;
     SP_SGD_CASE(0)
     SP_SGD_CASE(1)
@@ -670,23 +812,41 @@ __global__ void __launch_bounds__(kBlockThreads, SP_SGD_MIN_BLOCKS)
     SP_SGD_CASE(5)
 #undef SP_SGD_CASE
     default:
-      sgd_tile_generic(m, tile, sh, bags, grad, ldg, lr, w);
+      sgd_tile_generic<BagT, T>(m, tile, sh, bags, grad, ldg, lr, w);
   }
 }
 
 // ---------------------------------------------------------------------------
 // Generator / layout kernels
 
-__global__ void init_weights_kernel(float* __restrict__ w, int64_t rows,
+__device__ __forceinline__ void store_w(float* p, float v) { *p = v; }
+__device__ __forceinline__ void store_w(__half* p, float v) { *p = __float2half_rn(v); }
+
+template <class T>
+__global__ void init_weights_kernel(T* __restrict__ w, int64_t rows,
                                     int dim, int32_t gid, uint64_t seed) {
   const int64_t n = rows * dim;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
        e < n; e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t r = e / dim;
     const int c = static_cast<int>(e - r * dim);
-    w[e] = weight_from_base(
-        h3(seed, kTagW, static_cast<uint64_t>(gid), static_cast<uint64_t>(r)), c);
+    store_w(w + e, weight_from_base(
+                       h3(seed, kTagW, static_cast<uint64_t>(gid), static_cast<uint64_t>(r)), c));
   }
+}
+
+// fp32 host rows <-> fp16 device rows (set_table / get_table)
+__global__ void f32_to_f16_kernel(const float* __restrict__ src, __half* __restrict__ dst,
+                                  int64_t n) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[e] = __float2half_rn(src[e]);
+}
+__global__ void f16_to_f32_kernel(const __half* __restrict__ src, float* __restrict__ dst,
+                                  int64_t n) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[e] = __half2float(src[e]);
 }
 
 __global__ void synth_lengths_kernel(const int32_t* __restrict__ gid,
@@ -783,28 +943,37 @@ std::vector<int4> make_fwd_tiles(const std::vector<TableMeta>& canon,
 
 void launch_tbe_forward(const TableMeta* d_meta_canon, const int4* d_tiles,
                         int64_t n_tiles, int batch, const int32_t* d_off,
-                        const int32_t* d_idx, const float* d_w, float* d_out,
+                        const int32_t* d_idx, const void* d_w, WeightType wt, float* d_out,
                         const RowMap* d_peer, int64_t ldo, uint32_t* d_keys, void* d_bags,
                         bool bags16, cudaStream_t st) {
   if (n_tiles <= 0) return;
   const FwdTile* tiles = reinterpret_cast<const FwdTile*>(d_tiles);
   const unsigned g = static_cast<unsigned>(n_tiles);
-  auto go = [&](auto peer) {
+  auto go = [&](auto peer, auto elem) {
     constexpr bool kPeer = decltype(peer)::value;
+    using T = typename decltype(elem)::type;
+    const T* w = static_cast<const T*>(d_w);
     if (!d_keys)
-      tbe_forward_kernel<false, uint32_t, kPeer><<<g, kBlockThreads, 0, st>>>(
-          d_meta_canon, tiles, batch, d_off, d_idx, d_w, d_out, d_peer, ldo, nullptr, nullptr);
+      tbe_forward_kernel<false, uint32_t, kPeer, T><<<g, kBlockThreads, 0, st>>>(
+          d_meta_canon, tiles, batch, d_off, d_idx, w, d_out, d_peer, ldo, nullptr, nullptr);
     else if (bags16)
-      tbe_forward_kernel<true, uint16_t, kPeer><<<g, kBlockThreads, 0, st>>>(
-          d_meta_canon, tiles, batch, d_off, d_idx, d_w, d_out, d_peer, ldo, d_keys,
+      tbe_forward_kernel<true, uint16_t, kPeer, T><<<g, kBlockThreads, 0, st>>>(
+          d_meta_canon, tiles, batch, d_off, d_idx, w, d_out, d_peer, ldo, d_keys,
           static_cast<uint16_t*>(d_bags));
     else
-      tbe_forward_kernel<true, uint32_t, kPeer><<<g, kBlockThreads, 0, st>>>(
-          d_meta_canon, tiles, batch, d_off, d_idx, d_w, d_out, d_peer, ldo, d_keys,
+      tbe_forward_kernel<true, uint32_t, kPeer, T><<<g, kBlockThreads, 0, st>>>(
+          d_meta_canon, tiles, batch, d_off, d_idx, w, d_out, d_peer, ldo, d_keys,
           static_cast<uint32_t*>(d_bags));
   };
-  if (d_peer) go(std::true_type{});
-  else go(std::false_type{});
+  using F32 = TypeTag<float>;
+  using F16 = TypeTag<__half>;
+  if (wt == WeightType::kF16) {
+    if (d_peer) go(std::true_type{}, F16{});
+    else go(std::false_type{}, F16{});
+  } else {
+    if (d_peer) go(std::true_type{}, F32{});
+    else go(std::false_type{}, F32{});
+  }
   SP_LAUNCHED();
 }
 
@@ -876,27 +1045,61 @@ std::vector<int> make_sgd_tiles(const std::vector<int64_t>& table_nnz) {
 
 void launch_sgd(const TableMeta* d_meta_canon, const int* d_tiles, int64_t n_tiles,
                 const uint32_t* d_keys, const void* d_bags, bool bags16, const float* d_grad,
-                int64_t ldg, float lr, float* d_w, const int32_t* d_abort, cudaStream_t st) {
+                int64_t ldg, float lr, void* d_w, WeightType wt, const int32_t* d_abort,
+                cudaStream_t st) {
   if (n_tiles <= 0) return;
   static_assert(sizeof(SgdTile) == kSgdTileInts * sizeof(int), "tile layout");
   const SgdTile* tiles = reinterpret_cast<const SgdTile*>(d_tiles);
   const unsigned blocks = static_cast<unsigned>(n_tiles);
-  if (bags16)
-    sgd_kernel<uint16_t><<<blocks, kBlockThreads, 0, st>>>(
-        d_meta_canon, tiles, d_keys, static_cast<const uint16_t*>(d_bags), d_grad, ldg, lr, d_w,
-        d_abort);
-  else
-    sgd_kernel<uint32_t><<<blocks, kBlockThreads, 0, st>>>(
-        d_meta_canon, tiles, d_keys, static_cast<const uint32_t*>(d_bags), d_grad, ldg, lr, d_w,
-        d_abort);
+  auto go = [&](auto elem) {
+    using T = typename decltype(elem)::type;
+    T* w = static_cast<T*>(d_w);
+    if (bags16)
+      sgd_kernel<uint16_t, T><<<blocks, kBlockThreads, 0, st>>>(
+          d_meta_canon, tiles, d_keys, static_cast<const uint16_t*>(d_bags), d_grad, ldg, lr, w,
+          d_abort);
+    else
+      sgd_kernel<uint32_t, T><<<blocks, kBlockThreads, 0, st>>>(
+          d_meta_canon, tiles, d_keys, static_cast<const uint32_t*>(d_bags), d_grad, ldg, lr, w,
+          d_abort);
+  };
+  if (wt == WeightType::kF16) go(TypeTag<__half>{});
+  else go(TypeTag<float>{});
   SP_LAUNCHED();
 }
 
-void launch_init_weights(float* d_w, int64_t rows, int dim, int32_t gid,
+void launch_init_weights(void* d_w, WeightType wt, int64_t rows, int dim, int32_t gid,
                          uint64_t seed, cudaStream_t st) {
-  init_weights_kernel<<<grid_for(rows * dim, 256), 256, 0, st>>>(d_w, rows, dim,
-                                                                  gid, seed);
+  if (wt == WeightType::kF16)
+    init_weights_kernel<__half><<<grid_for(rows * dim, 256), 256, 0, st>>>(
+        static_cast<__half*>(d_w), rows, dim, gid, seed);
+  else
+    init_weights_kernel<float><<<grid_for(rows * dim, 256), 256, 0, st>>>(
+        static_cast<float*>(d_w), rows, dim, gid, seed);
   SP_LAUNCHED();
+}
+
+void launch_f32_to_weights(const float* d_src, void* d_dst, WeightType wt, int64_t n,
+                           cudaStream_t st) {
+  if (n <= 0) return;
+  if (wt == WeightType::kF16) {
+    f32_to_f16_kernel<<<grid_for(n, 256), 256, 0, st>>>(d_src, static_cast<__half*>(d_dst), n);
+    SP_LAUNCHED();
+  } else {
+    SP_CUDA(cudaMemcpyAsync(d_dst, d_src, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  }
+}
+
+void launch_weights_to_f32(const void* d_src, WeightType wt, float* d_dst, int64_t n,
+                           cudaStream_t st) {
+  if (n <= 0) return;
+  if (wt == WeightType::kF16) {
+    f16_to_f32_kernel<<<grid_for(n, 256), 256, 0, st>>>(static_cast<const __half*>(d_src),
+                                                        d_dst, n);
+    SP_LAUNCHED();
+  } else {
+    SP_CUDA(cudaMemcpyAsync(d_dst, d_src, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  }
 }
 
 void launch_synth_lengths(const int32_t* d_gid, const int64_t* d_lmax,

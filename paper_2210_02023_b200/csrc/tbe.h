@@ -2,6 +2,7 @@
 // the launchers of the hot kernels (K1 forward, K4 backward).
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -11,7 +12,7 @@ namespace sp {
 
 // One local table of a (virtual) device, in kernel order.
 struct TableMeta {
-  int64_t woff;         // float offset of row 0 in the weight slab
+  int64_t woff;         // element offset of row 0 in the weight slab
   int64_t rows;         // hash_size
   int64_t reserved;
   int32_t dim;
@@ -22,18 +23,26 @@ struct TableMeta {
   int32_t gid;          // global table id
 };
 
-// Dim class: 0..5 for dim = 4,8,16,32,64,128 (float4 row slices), -1 else.
-inline int dim_class(int dim) {
-  switch (dim) {
-    case 4: return 0;
-    case 8: return 1;
-    case 16: return 2;
-    case 32: return 3;
-    case 64: return 4;
-    case 128: return 5;
+// Storage type of the embedding rows: fp32 (4 B/param) or fp16 (2 B/param,
+// the paper's tables, and table_memory_gb's default,
+// table.hpp:30). Pooled outputs, gradients and all sums stay fp32.
+enum class WeightType : int32_t { kF32 = 0, kF16 = 1 };
+inline int elem_bytes(WeightType t) { return t == WeightType::kF16 ? 2 : 4; }
+
+// Row class by row bytes: 0..5 for 16, 32, ..., 512-byte rows (whole 16-byte
+// slices: fp32 dims 4..128, fp16 dims 8..256), -1 = the generic path.
+inline int row_class(int dim, WeightType t) {
+  switch (dim * elem_bytes(t)) {
+    case 16: return 0;
+    case 32: return 1;
+    case 64: return 2;
+    case 128: return 3;
+    case 256: return 4;
+    case 512: return 5;
     default: return -1;
   }
 }
+inline int dim_class(int dim) { return row_class(dim, WeightType::kF32); }
 
 // Bags (K1) or unique rows (K4) per warp for each dim class: the warp is
 // split into P spans of 32/P lanes; a span sums one bag / one row's
@@ -77,7 +86,7 @@ std::vector<int4> make_fwd_tiles(const std::vector<TableMeta>& canon,
                                  const std::vector<int>& order, int batch);
 void launch_tbe_forward(const TableMeta* d_meta_canon, const int4* d_tiles,
                         int64_t n_tiles, int batch, const int32_t* d_off,
-                        const int32_t* d_idx, const float* d_w, float* d_out,
+                        const int32_t* d_idx, const void* d_w, WeightType wt, float* d_out,
                         const RowMap* d_peer, int64_t ldo, uint32_t* d_keys, void* d_bags,
                         bool bags16, cudaStream_t st);
 
@@ -106,11 +115,17 @@ std::vector<int> make_sgd_tiles(const std::vector<int64_t>& table_nnz);
 // d_abort (may be null): when *d_abort != 0 the launch leaves W untouched.
 void launch_sgd(const TableMeta* d_meta_canon, const int* d_tiles, int64_t n_tiles,
                 const uint32_t* d_keys, const void* d_bags, bool bags16, const float* d_grad,
-                int64_t ldg, float lr, float* d_w, const int32_t* d_abort, cudaStream_t st);
+                int64_t ldg, float lr, void* d_w, WeightType wt, const int32_t* d_abort,
+                cudaStream_t st);
 
 // ---- generator / layout helpers ------------------------------------------
-void launch_init_weights(float* d_w, int64_t rows, int dim, int32_t gid,
+void launch_init_weights(void* d_w, WeightType wt, int64_t rows, int dim, int32_t gid,
                          uint64_t seed, cudaStream_t st);
+// fp32 rows -> table storage type and back (device to device).
+void launch_f32_to_weights(const float* d_src, void* d_dst, WeightType wt, int64_t n,
+                           cudaStream_t st);
+void launch_weights_to_f32(const void* d_src, WeightType wt, float* d_dst, int64_t n,
+                           cudaStream_t st);
 // lengths of the bags of local tables (gid, lmax per table) into d_len[i*B+b]
 void launch_synth_lengths(const int32_t* d_gid, const int64_t* d_lmax,
                           int n_tables, int batch, uint64_t seed,
