@@ -221,6 +221,51 @@ def config_dict(args, task):
             "parallelism": f"table-wise model parallel x{task.num_devices}"}
 
 
+def bench_fp16(args, task, placement, device: int):
+    """The same iteration with the tables stored in fp16 (2 B/param): device
+    ms/iter over the timed loop and each hot kernel in isolation."""
+    import torch
+    from paper_2210_02023_b200 import api
+    tables = [api.TableDesc(t.id, t.dim, t.hash_size, t.pooling_factor,
+                            api.table_memory_gb(t.hash_size, t.dim, 2), t.dist)
+              for t in task.tables]
+    t16 = api.PlacementTask(tables, task.num_devices, task.mem_cap_gb / 2, task.batch_size)
+    sh = api.EmbeddingShard(t16, placement, lr=0.01, device=device)
+    sh.init_tables(SEED)
+    sh.synth_batch(SEED)
+    sh.synth_grad(SEED)
+    stream = torch.cuda.ExternalStream(sh.stream, device=device)
+    for _ in range(args.warmup):
+        sh.enqueue_iteration()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    steps = max(3, min(args.steps, 100))
+    e0.record(stream)
+    for _ in range(steps):
+        sh.enqueue_iteration()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    sh.set_overlap(False)
+    sh.set_profiling(True)
+    for _ in range(3):
+        sh.enqueue_iteration()
+    sh.kernel_ms()
+    for _ in range(steps):
+        sh.enqueue_iteration()
+    kms = sh.kernel_ms()
+    sh.set_profiling(False)
+    ab = sh.algorithmic_bytes()
+    sh.close()
+    out = {"ms_per_iter": round(ms, 4), "weights": "fp16 (2 B/param), fp32 sums/pooled/grad"}
+    for k, a in (("fwd", ab["fwd"]), ("sort", ab["sort"]), ("sgd", ab["bwd"])):
+        t = kms[k][0] / kms[k][1] if kms[k][1] else 0.0
+        out[k] = {"ms": round(t, 4), "alg_bytes": a,
+                  "alg_gbs": round(a / (t * 1e6), 1) if t > 0 else None}
+    return out
+
+
 def bench_evaluator(args, device: int, n: int = 4096):
     """Batched cost-net scoring and policy rollouts (K6/K7) of one task."""
     import torch
@@ -403,6 +448,12 @@ def run_ours(args, world, rank, local):
         }
         esh.close()
 
+    # fp16 tables (the paper's storage; 2 B/param like the
+    # reference's default table_memory_gb): same tables, batch and placement
+    fp16 = None
+    if world == 1 and not args.no_fp16:
+        fp16 = bench_fp16(args, task, placement, local)
+
     # K6/K7 evaluator throughput (SURVEY cfg5 shape): 4096 candidate
     # placements of this task at D = 8, scored and rolled out on this GPU
     evaluator = None
@@ -440,6 +491,7 @@ def run_ours(args, world, rank, local):
                                             "into our library, K4 SGD)"},
             "clocks": clk.summary(),
             "emulated_d8": emulated,
+            "fp16_tables": fp16,
             "evaluator": evaluator,
         }
         print(json.dumps(line), flush=True)
@@ -459,6 +511,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-emulation", action="store_true")
     ap.add_argument("--no-evaluator", action="store_true")
+    ap.add_argument("--no-fp16", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
