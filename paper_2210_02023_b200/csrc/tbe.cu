@@ -183,7 +183,11 @@ struct FwdTile {
   int32_t pad;
 };
 
-constexpr int kTileBags = 256;
+constexpr int kTileBags = 256;  // build_keys block (bags per block)
+#ifndef SP_FWD_TILE_BAGS
+#define SP_FWD_TILE_BAGS 128  // 256: 1.634 ms, 128: 1.607, 64: 1.630 (K1 at cfg3)
+#endif
+constexpr int kFwdTileBags = SP_FWD_TILE_BAGS;  // K1 tile (bags per block)
 constexpr int kIdxCap = 4096;  // staged indices per tile (16 KB)
 
 // 16-byte slices of a table row of element type T, widened to fp32 (K1) and
@@ -357,7 +361,7 @@ __global__ void SP_FWD_BOUNDS
                        const RowMap* __restrict__ peer,
                        int64_t ldo, uint32_t* __restrict__ keys,
                        BagT* __restrict__ bags) {
-  __shared__ int32_t s_off[kTileBags + 1];
+  __shared__ int32_t s_off[kFwdTileBags + 1];
   __shared__ int32_t s_idx[kIdxCap];
   const FwdTile tile = tiles[blockIdx.x];
   const TableMeta m = meta[tile.t];
@@ -936,8 +940,8 @@ std::vector<int4> make_fwd_tiles(const std::vector<TableMeta>& canon,
                                  const std::vector<int>& order, int batch) {
   std::vector<int4> tiles;
   for (int li : order)
-    for (int b0 = 0; b0 < batch; b0 += kTileBags)
-      tiles.push_back(make_int4(canon[li].local, b0, std::min(kTileBags, batch - b0), 0));
+    for (int b0 = 0; b0 < batch; b0 += kFwdTileBags)
+      tiles.push_back(make_int4(canon[li].local, b0, std::min(kFwdTileBags, batch - b0), 0));
   return tiles;
 }
 

@@ -47,3 +47,41 @@ def test_provider_measures_on_gpu():
         r = subprocess.run([exe, "gpu"], capture_output=True, text=True)
         assert r.returncode == 0, r.stderr
         assert "ok (gpu)" in r.stdout
+
+
+TRAIN_BIN = os.path.join(ROOT, "tests", "cpp", "_bin", "measured_train_test")
+
+
+def _build_train(exe):
+    cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+    cmd = [cxx, "-std=c++20", "-O2", "-DSHARDPLAN_B200_WITH_REFERENCE", "-I", REF,
+           "-I", _json_include(),
+           "-include", os.path.join(ROOT, "tests", "cpp", "ref_shim.hpp"),
+           "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "tests", "cpp", "measured_train_test.cpp"), "-o", exe,
+           os.path.join(LIBDIR, "_shardplan_b200.so"), f"-Wl,-rpath,{LIBDIR}"]
+    subprocess.run(cmd, check=True, capture_output=True)
+
+
+@pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "shardplan")),
+                    reason="reference headers not present")
+def test_training_loop_on_provider_reproduces_reference_train():
+    """train_on_provider with OracleCostProvider == the reference's train()."""
+    with tempfile.TemporaryDirectory() as d:
+        exe = os.path.join(d, "t")
+        _build_train(exe)
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr
+        assert "ok (oracle" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(TRAIN_BIN),
+                    reason="built by __graft_entry__.build() where the reference headers exist")
+def test_training_loop_on_measured_costs():
+    """The reference's training loop with the collect phase on B200-measured
+    costs (MeasuredCostProvider): finite costs and losses, one
+    measured cost vector per table per collected episode."""
+    r = subprocess.run([TRAIN_BIN, "gpu"], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr
+    assert "ok (gpu" in r.stdout, r.stdout
