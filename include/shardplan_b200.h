@@ -233,6 +233,16 @@ int sp_run_iteration(sp_ctx* ctx, sp_breakdown* out);
  * oracle.hpp:187-240, over a real LookupBatch). */
 int sp_run_batch(sp_ctx* ctx, const int64_t* offsets, int64_t offsets_len,
                  const int64_t* indices, int64_t indices_len, sp_breakdown* out);
+/* n consecutive host-buffer steps (a training segment fed by a data loader;
+ * batch s = offsets[s][offsets_len[s]], indices[s][indices_len[s]], host
+ * buffers valid until the call returns): step s's H2D overlaps step s-1's
+ * compute (two staging slots); step s's forward still follows step s-1's SGD.
+ * step_ms[s] (may be NULL) = device time from the end of step s-1 (s = 0:
+ * the start of its upload) to the end of step s. Raises for the first step
+ * whose device-side validation failed (that step updated nothing). */
+int sp_run_batches(sp_ctx* ctx, int32_t n, const int64_t* const* offsets,
+                   const int64_t* offsets_len, const int64_t* const* indices,
+                   const int64_t* indices_len, double* step_ms);
 /* Enqueue one iteration without events or host sync (for timing loops and
  * CUDA-graph capture). */
 int sp_enqueue_iteration(sp_ctx* ctx);

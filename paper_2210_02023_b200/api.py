@@ -431,6 +431,21 @@ class EmbeddingShard:
         return CostBreakdown(list(f), list(bw), list(c), bd.fwd_comm_stage_ms,
                              bd.bwd_comm_stage_ms, bd.overall_ms)
 
+    def run_batches(self, batches: list) -> list:
+        """n consecutive host-buffer steps (sp_run_batches): step s's H2D
+        overlaps step s-1's compute. Returns per-step device ms."""
+        n = len(batches)
+        for b in batches:
+            if b.num_tables != len(self.task.tables) or b.batch_size != self.B:
+                raise ShardplanError(8, "batch shape does not match the task")
+        offs = (ctypes.c_void_p * n)(*[b.offsets.ctypes.data for b in batches])
+        idxs = (ctypes.c_void_p * n)(*[b.indices.ctypes.data for b in batches])
+        olen = (ctypes.c_int64 * n)(*[len(b.offsets) for b in batches])
+        ilen = (ctypes.c_int64 * n)(*[len(b.indices) for b in batches])
+        ms = (ctypes.c_double * n)()
+        check(lib().sp_run_batches(self._h, n, offs, olen, idxs, ilen, ms))
+        return list(ms)
+
     def enqueue_iteration(self):
         check(lib().sp_enqueue_iteration(self._h))
 

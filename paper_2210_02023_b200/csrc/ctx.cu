@@ -62,8 +62,6 @@ struct SortGroup {
 struct VDev {
   int vid = 0;
   std::vector<SortGroup> groups;
-  int64_t* d_gstart = nullptr;  // [groups + 1] first position (last = nnz)
-  int32_t* d_gt0 = nullptr;     // [groups + 1] first local table (last = T)
   std::vector<int> tables;  // global ids, ascending
   std::vector<TableMeta> meta_canon;
   std::vector<uint32_t> rb_end;
@@ -74,8 +72,12 @@ struct VDev {
   int4* d_tiles_canon = nullptr;  // K1 tiles in table order (pipelined upload path)
   std::vector<int64_t> tile_start;  // first canonical tile of each local table (+ end)
   std::vector<int> group_of_table;  // sort group of each local table
-  int* d_sgd_tiles = nullptr;   // K4 SGD tiles of the current batch
-  int64_t n_sgd_tiles = 0, sgd_tile_cap = 0;
+  // K4 SGD tiles of the current batch, one buffer per staging slot (a step's
+  // tiles upload while the previous step's SGD may still read its own)
+  int* d_sgd_tiles[2] = {};
+  int64_t sgd_tile_cap[2] = {};
+  int64_t n_sgd_tiles = 0;
+  int cur = 0;  // slot of the current batch
   uint32_t* d_keys = nullptr;   // backward sort pairs (written by K1)
   uint32_t* d_bags = nullptr;
   bool keys_valid = false;
@@ -170,8 +172,20 @@ struct sp_ctx {
   int64_t sort_cap = 0;
   void* d_temp = nullptr;
   size_t temp_bytes = 0;
-  int64_t* d_stage64 = nullptr;
+  int64_t* d_stage64 = nullptr;      // int64 staging of an uploaded LookupBatch
+  int64_t* d_stage64_alt = nullptr;  // second slot (sp_run_batches: next step's H2D)
   int64_t stage_cap = 0;
+  cudaEvent_t stage_free[2] = {};    // recorded after the narrows that read a slot
+  bool stage_used[2] = {};
+  int32_t* d_step_flags = nullptr;   // per-step validation flags (sp_run_batches)
+  int64_t step_flags_cap = 0;
+  // pinned host copies of a batch's layout metadata (SGD tiles, sort group
+  // starts), one per staging slot: a pageable H2D would wait for the stream
+  uint8_t* meta_host[2] = {};
+  size_t meta_cap[2] = {};
+  cudaEvent_t slot_done[2] = {};     // after the SGD of the last step that used a slot
+  bool slot_done_used[2] = {};
+  cudaEvent_t meta_ready = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // H2D of uploaded batches
   // The backward's sort depends only on the batch, not on the gradient: with
@@ -223,9 +237,19 @@ struct sp_ctx {
     for (auto& e : ev_pool) cudaEventDestroy(e);
     for (auto& v : vdevs)
       for (void* p : {static_cast<void*>(v.d_idx), static_cast<void*>(v.d_keys),
-                       static_cast<void*>(v.d_bags), static_cast<void*>(v.d_sgd_tiles)})
+                       static_cast<void*>(v.d_bags), static_cast<void*>(v.d_sgd_tiles[0]),
+                       static_cast<void*>(v.d_sgd_tiles[1])})
         if (p) cudaFree(p);
     if (d_stage64) cudaFree(d_stage64);
+    if (d_stage64_alt) cudaFree(d_stage64_alt);
+    if (d_step_flags) cudaFree(d_step_flags);
+    for (auto* p : meta_host)
+      if (p) cudaFreeHost(p);
+    for (auto& e : stage_free)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : slot_done)
+      if (e) cudaEventDestroy(e);
+    if (meta_ready) cudaEventDestroy(meta_ready);
     for (void* p : bucket_owned) cudaFree(p);
     for (void* p : sort_owned) cudaFree(p);
     for (void* p : owned) cudaFree(p);
@@ -435,7 +459,7 @@ void stage_backward(sp_ctx* c, VDev& v, bool sorted = false,
   }
   if (!sorted) stage_sort(c, v, c->stream);
   ProfScope prof(c, kProfSgd);
-  launch_sgd(v.d_meta_canon, v.d_sgd_tiles, v.n_sgd_tiles, c->d_kb, c->d_bb, c->bags16,
+  launch_sgd(v.d_meta_canon, v.d_sgd_tiles[v.cur], v.n_sgd_tiles, c->d_kb, c->d_bb, c->bags16,
              v.d_grad, v.W, c->lr, c->d_w, c->wt, abort_flag, c->stream);
 }
 
@@ -741,6 +765,9 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
     }
     SP_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     SP_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    for (auto& e : c->stage_free) SP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : c->slot_done) SP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    SP_CUDA(cudaEventCreateWithFlags(&c->meta_ready, cudaEventDisableTiming));
 
     // Columns: global table order; per-device widths.
     c->gcol.resize(num_tables);
@@ -855,16 +882,6 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
         v.rb_end.push_back(static_cast<uint32_t>(rb));
       }
       if (T > 0) close_group(T);
-      {
-        std::vector<int32_t> gt0;
-        for (const SortGroup& sg : v.groups) gt0.push_back(sg.t0);
-        gt0.push_back(T);
-        v.d_gt0 = dalloc<int32_t>(gt0.size(), c->owned, c->dev_bytes);
-        v.d_gstart = dalloc<int64_t>(gt0.size(), c->owned, c->dev_bytes);
-        SP_CUDA(cudaMemcpy(v.d_gt0, gt0.data(), gt0.size() * sizeof(int32_t),
-                           cudaMemcpyHostToDevice));
-        SP_CUDA(cudaMemset(v.d_gstart, 0, gt0.size() * sizeof(int64_t)));
-      }
       v.W = lcol;
       v.rows_total = gbase;
       v.end_bit = 1;
@@ -1102,36 +1119,69 @@ int sp_get_table(sp_ctx* ctx, int32_t table_id, float* rows) {
   });
 }
 
-static void finish_batch(sp_ctx* c) {
+// Layout metadata of the current batch (sort-group positions on the host,
+// SGD tiles on the device). The tiles go through the pinned buffer of `slot`
+// on the copy stream, ahead of the batch's H2D and into the slot's own
+// device buffer, so a step's upload never queues behind the previous step's
+// compute (a pageable or compute-stream copy would).
+// pipelined: the caller orders this step after the slot's previous user
+// (sp_run_batches, steps >= 1); otherwise the upload waits for all work
+// already enqueued on the compute stream.
+static void finish_batch(sp_ctx* c, int slot = 0, bool pipelined = false) {
   int64_t max_nnz = 0;
+  std::vector<std::vector<int>> tiles;
+  size_t need = 0;
   for (auto& v : c->vdevs) {
+    tiles.push_back(make_sgd_tiles(v.table_nnz));
+    need += tiles.back().size() * sizeof(int) + 16;
+  }
+  if (c->stage_used[slot]) SP_CUDA(cudaEventSynchronize(c->stage_free[slot]));
+  if (need > c->meta_cap[slot]) {
+    if (c->meta_host[slot]) cudaFreeHost(c->meta_host[slot]);
+    c->meta_host[slot] = nullptr;
+    SP_CUDA(cudaMallocHost(&c->meta_host[slot], need));
+    c->meta_cap[slot] = need;
+  }
+  // the previous SGD that read this slot's tiles must be done
+  if (!pipelined) {
+    SP_CUDA(cudaEventRecord(c->meta_ready, c->stream));
+    SP_CUDA(cudaStreamWaitEvent(c->copy_stream, c->meta_ready, 0));
+  } else if (c->slot_done_used[slot]) {
+    SP_CUDA(cudaStreamWaitEvent(c->copy_stream, c->slot_done[slot], 0));
+  }
+  size_t mo = 0;  // offset into the pinned buffer
+  for (size_t vi = 0; vi < c->vdevs.size(); ++vi) {
+    VDev& v = c->vdevs[vi];
     max_nnz = std::max(max_nnz, v.nnz);
     int64_t p = 0;  // positions of each sort group in the device CSR
-    std::vector<int64_t> gs;
     for (SortGroup& g : v.groups) {
       g.p0 = p;
-      gs.push_back(p);
       for (int t = g.t0; t < g.t1; ++t) p += v.table_nnz[t];
       g.p1 = p;
     }
-    gs.push_back(p);
-    if (v.d_gstart)
-      SP_CUDA(cudaMemcpy(v.d_gstart, gs.data(), gs.size() * sizeof(int64_t),
-                         cudaMemcpyHostToDevice));
-    const std::vector<int> tl = make_sgd_tiles(v.table_nnz);
+    const std::vector<int>& tl = tiles[vi];
     v.n_sgd_tiles = static_cast<int64_t>(tl.size()) / kSgdTileInts;
-    if (static_cast<int64_t>(tl.size()) > v.sgd_tile_cap) {
+    if (static_cast<int64_t>(tl.size()) > v.sgd_tile_cap[slot]) {
       SP_CUDA(cudaStreamSynchronize(c->stream));
-      if (c->side) SP_CUDA(cudaStreamSynchronize(c->side));
-      if (v.d_sgd_tiles) cudaFree(v.d_sgd_tiles);
-      v.d_sgd_tiles = nullptr;
-      SP_CUDA(cudaMalloc(&v.d_sgd_tiles, tl.size() * sizeof(int)));
-      v.sgd_tile_cap = static_cast<int64_t>(tl.size());
+      SP_CUDA(cudaStreamSynchronize(c->side));
+      SP_CUDA(cudaStreamSynchronize(c->copy_stream));
+      if (v.d_sgd_tiles[slot]) cudaFree(v.d_sgd_tiles[slot]);
+      v.d_sgd_tiles[slot] = nullptr;
+      SP_CUDA(cudaMalloc(&v.d_sgd_tiles[slot], tl.size() * sizeof(int)));
+      v.sgd_tile_cap[slot] = static_cast<int64_t>(tl.size());
     }
-    if (!tl.empty())
-      SP_CUDA(cudaMemcpy(v.d_sgd_tiles, tl.data(), tl.size() * sizeof(int),
-                         cudaMemcpyHostToDevice));
+    if (!tl.empty()) {
+      std::memcpy(c->meta_host[slot] + mo, tl.data(), tl.size() * sizeof(int));
+      SP_CUDA(cudaMemcpyAsync(v.d_sgd_tiles[slot], c->meta_host[slot] + mo,
+                              tl.size() * sizeof(int), cudaMemcpyHostToDevice,
+                              c->copy_stream));
+      mo += (tl.size() * sizeof(int) + 15) & ~size_t(15);
+    }
+    v.cur = slot;
   }
+  // the compute stream reads the tiles only after this point
+  SP_CUDA(cudaEventRecord(c->meta_ready, c->copy_stream));
+  SP_CUDA(cudaStreamWaitEvent(c->stream, c->meta_ready, 0));
   ensure_sort_capacity(c, max_nnz);
   plan_buckets(c);
   c->has_batch = true;
@@ -1170,7 +1220,7 @@ namespace {
 // monotonicity inside a table and the index range are checked on the device
 // while narrowing); sizes every device's CSR and the int64 staging buffer.
 void host_validate_and_size(sp_ctx* c, const int64_t* offsets, int64_t offsets_len,
-                            int64_t indices_len) {
+                            int64_t indices_len, bool two_slots = false) {
   const int64_t B = c->B;
   if (offsets_len != static_cast<int64_t>(c->M) * B + 1)
     raise(SP_ERR_MALFORMED_BATCH, "offsets length " + std::to_string(offsets_len) +
@@ -1197,11 +1247,21 @@ void host_validate_and_size(sp_ctx* c, const int64_t* offsets, int64_t offsets_l
     alloc_indices(c, v, n);
     stage_need += st;  // copies run ahead of the narrows: no reuse across devices
   }
-  if (stage_need > c->stage_cap) {
+  if (stage_need > c->stage_cap || (two_slots && c->d_stage64_alt == nullptr)) {
     SP_CUDA(cudaStreamSynchronize(c->stream));
-    if (c->d_stage64) cudaFree(c->d_stage64);
-    SP_CUDA(cudaMalloc(&c->d_stage64, std::max<int64_t>(stage_need, 1) * sizeof(int64_t)));
-    c->stage_cap = std::max<int64_t>(stage_need, 1);
+    SP_CUDA(cudaStreamSynchronize(c->copy_stream));
+    const int64_t cap = std::max<int64_t>({stage_need, c->stage_cap, 1});
+    if (stage_need > c->stage_cap) {
+      if (c->d_stage64) cudaFree(c->d_stage64);
+      SP_CUDA(cudaMalloc(&c->d_stage64, cap * sizeof(int64_t)));
+      if (c->d_stage64_alt) {
+        cudaFree(c->d_stage64_alt);
+        c->d_stage64_alt = nullptr;
+      }
+    }
+    if (two_slots && c->d_stage64_alt == nullptr)
+      SP_CUDA(cudaMalloc(&c->d_stage64_alt, cap * sizeof(int64_t)));
+    c->stage_cap = cap;
   }
 }
 
@@ -1222,18 +1282,19 @@ cudaEvent_t upload_event(sp_ctx* c, size_t& n_ev) {
 // flags malformed data in d_flag, clamping it so later kernels stay in
 // bounds). chunk_done(v, t0, t1) runs after the narrows of local tables
 // [t0, t1) of device v are enqueued on the compute stream.
+// flag: this step's validation flag; slot: staging buffer 0 or 1 (the copy
+// stream only waits for the narrows of the last step that used the slot, so
+// with two slots a step's H2D overlaps the previous step's compute).
 template <class F>
-void enqueue_upload(sp_ctx* c, const int64_t* offsets, const int64_t* indices, F&& chunk_done) {
+void enqueue_upload(sp_ctx* c, const int64_t* offsets, const int64_t* indices, F&& chunk_done,
+                    int32_t* flag = nullptr, int slot = 0) {
   const int64_t B = c->B;
   const int64_t kUploadChunk = c->upload_chunk;
+  if (flag == nullptr) flag = c->d_flag;
   size_t n_ev = 0;
-  SP_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int32_t), c->stream));
-  {
-    // the staging buffer may still be read by the previous upload's narrows
-    cudaEvent_t e = upload_event(c, n_ev);
-    SP_CUDA(cudaEventRecord(e, c->stream));
-    SP_CUDA(cudaStreamWaitEvent(c->copy_stream, e, 0));
-  }
+  SP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t), c->stream));
+  if (c->stage_used[slot]) SP_CUDA(cudaStreamWaitEvent(c->copy_stream, c->stage_free[slot], 0));
+  int64_t* const stage = slot == 0 ? c->d_stage64 : c->d_stage64_alt;
   int64_t so = 0;  // staging offset (int64 elements), across all devices
   for (auto& v : c->vdevs) {
     const int T = static_cast<int>(v.tables.size());
@@ -1253,7 +1314,7 @@ void enqueue_upload(sp_ctx* c, const int64_t* offsets, const int64_t* indices, F
         const int64_t n_off = (g1 - g0) * B + 1;
         const int64_t i0 = offsets[g0 * B];
         const int64_t n_idx = offsets[g1 * B] - i0;
-        int64_t* s_off = c->d_stage64 + so;
+        int64_t* s_off = stage + so;
         int64_t* s_idx = s_off + n_off;
         SP_CUDA(cudaMemcpyAsync(s_off, offsets + g0 * B, n_off * sizeof(int64_t),
                                 cudaMemcpyHostToDevice, c->copy_stream));
@@ -1268,7 +1329,7 @@ void enqueue_upload(sp_ctx* c, const int64_t* offsets, const int64_t* indices, F
           const int64_t tn = v.table_nnz[t];
           launch_narrow_table(s_off + (g - g0) * B, s_idx + (offsets[g * B] - i0), c->B, tn,
                               c->tables[g].hash_size, base, v.d_off + int64_t(t) * B,
-                              v.d_idx + base, c->d_flag, c->stream);
+                              v.d_idx + base, flag, c->stream);
           base += static_cast<int32_t>(tn);
         }
         chunk_done(v, c0, c1);
@@ -1279,6 +1340,8 @@ void enqueue_upload(sp_ctx* c, const int64_t* offsets, const int64_t* indices, F
     }
     if (v.tables.empty()) SP_CUDA(cudaMemsetAsync(v.d_off, 0, sizeof(int32_t), c->stream));
   }
+  SP_CUDA(cudaEventRecord(c->stage_free[slot], c->stream));
+  c->stage_used[slot] = true;
 }
 
 void raise_batch_flag(int32_t flag) {
@@ -1656,6 +1719,65 @@ int sp_run_iteration(sp_ctx* ctx, sp_breakdown* out) {
   });
 }
 
+}  // extern "C"
+
+namespace sp {
+namespace {
+
+// One host-buffer step, enqueued: upload (slot, flag) pipelined with K1 per
+// chunk and the per-group backward sorts, then stages 2-4 with the SGD
+// guarded by the step's validation flag. Events ev[0..7] time its stages.
+void enqueue_batch_step(sp_ctx* c, const int64_t* offsets, const int64_t* indices,
+                        int32_t* flag, int slot, bool pipelined = false) {
+  finish_batch(c, slot, pipelined);  // layout of this batch (sort positions, SGD tiles)
+  c->has_batch = false;
+  cudaStream_t st = c->stream;
+  const bool ov = overlap_active(c);
+  for (auto& v : c->vdevs) SP_CUDA(cudaEventRecord(v.ev[0], st));
+  enqueue_upload(
+      c, offsets, indices,
+      [&](VDev& v, int t0, int t1) {
+        const int64_t k0 = v.tile_start[t0], k1 = v.tile_start[t1];
+        const bool emit = ov ? c->overlap_mode == 2 : (c->fuse_keys && !v.bucketed);
+        {
+          ProfScope prof(c, kProfFwd);
+          launch_tbe_forward(v.d_meta_canon, v.d_tiles_canon + k0, k1 - k0, c->B, v.d_off,
+                             v.d_idx, c->d_w, c->wt, v.d_pooled, c->d_rowmap, v.W,
+                             emit ? v.d_keys : nullptr, emit ? v.d_bags : nullptr, c->bags16,
+                             st);
+        }
+        if (t1 == static_cast<int>(v.tables.size())) {
+          v.keys_valid = emit;
+          SP_CUDA(cudaEventRecord(v.ev[1], st));
+        }
+        const int g = v.group_of_table[t1 - 1];
+        if (ov && v.groups[g].t1 == t1) {
+          // the group's CSR is on the device: sort it on the side stream
+          SP_CUDA(cudaEventRecord(c->ev_fork, st));
+          SP_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+          if (c->overlap_mode == 2) {
+            ProfScope prof(c, kProfSort, c->side);
+            sort_pairs_of(c, v, v.groups[g], c->side);
+          } else {
+            sort_group(c, v, g, c->side);
+          }
+          if (g + 1 == static_cast<int>(v.groups.size()))
+            SP_CUDA(cudaEventRecord(c->ev_join, c->side));
+        }
+      },
+      flag, slot);
+  for (auto& v : c->vdevs)
+    if (v.tables.empty()) SP_CUDA(cudaEventRecord(v.ev[1], st));
+  timed_exchange_and_backward(c, ov, flag);
+  SP_CUDA(cudaEventRecord(c->slot_done[slot], st));
+  c->slot_done_used[slot] = true;
+}
+
+}  // namespace
+}  // namespace sp
+
+extern "C" {
+
 // The reference-facing step with host buffers: the LookupBatch's H2D is
 // pipelined with the forward (K1 runs on each uploaded chunk of tables while
 // the next chunk is in flight) and, with one (virtual) device, with the
@@ -1669,48 +1791,69 @@ int sp_run_batch(sp_ctx* ctx, const int64_t* offsets, int64_t offsets_len,
     check_ctx(ctx);
     sp_ctx* c = ctx;
     host_validate_and_size(c, offsets, offsets_len, indices_len);
-    finish_batch(c);  // host-side layout of this batch (sort positions, SGD tiles)
-    c->has_batch = false;
-    cudaStream_t st = c->stream;
-    const bool ov = overlap_active(c);
-    for (auto& v : c->vdevs) SP_CUDA(cudaEventRecord(v.ev[0], st));
-    enqueue_upload(c, offsets, indices, [&](VDev& v, int t0, int t1) {
-      const int64_t k0 = v.tile_start[t0], k1 = v.tile_start[t1];
-      const bool emit = ov ? c->overlap_mode == 2 : (c->fuse_keys && !v.bucketed);
-      {
-        ProfScope prof(c, kProfFwd);
-        launch_tbe_forward(v.d_meta_canon, v.d_tiles_canon + k0, k1 - k0, c->B, v.d_off,
-                           v.d_idx, c->d_w, c->wt, v.d_pooled, c->d_rowmap, v.W, emit ? v.d_keys : nullptr,
-                           emit ? v.d_bags : nullptr, c->bags16, st);
-      }
-      if (t1 == static_cast<int>(v.tables.size())) {
-        v.keys_valid = emit;
-        SP_CUDA(cudaEventRecord(v.ev[1], st));
-      }
-      const int g = v.group_of_table[t1 - 1];
-      if (ov && v.groups[g].t1 == t1) {
-        // the group's CSR is on the device: sort it on the side stream
-        SP_CUDA(cudaEventRecord(c->ev_fork, st));
-        SP_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-        if (c->overlap_mode == 2) {
-          ProfScope prof(c, kProfSort, c->side);
-          sort_pairs_of(c, v, v.groups[g], c->side);
-        } else {
-          sort_group(c, v, g, c->side);
-        }
-        if (g + 1 == static_cast<int>(v.groups.size()))
-          SP_CUDA(cudaEventRecord(c->ev_join, c->side));
-      }
-    });
-    for (auto& v : c->vdevs)
-      if (v.tables.empty()) SP_CUDA(cudaEventRecord(v.ev[1], st));
-    timed_exchange_and_backward(c, ov, c->d_flag);
+    enqueue_batch_step(c, offsets, indices, c->d_flag, 0);
     int32_t flag = 0;
-    SP_CUDA(cudaMemcpyAsync(&flag, c->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    SP_CUDA(cudaStreamSynchronize(st));
+    SP_CUDA(cudaMemcpyAsync(&flag, c->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                            c->stream));
+    SP_CUDA(cudaStreamSynchronize(c->stream));
     raise_batch_flag(flag);
     c->has_batch = true;
     collect_breakdown(c, out);
+  });
+}
+
+// n consecutive host-buffer steps (a training segment fed by a data
+// loader): step s's H2D (staging slot s % 2) overlaps step s-1's compute;
+// K1 of step s still runs after step s-1's SGD (stream order), so every step
+// sees the tables its predecessor updated. step_ms[s] (may be null): device
+// time from the end of step s-1 (for s = 0: the start of its upload) to the
+// end of step s. Every step's validation flag is checked at the end: an
+// invalid step skipped its update and the call raises for the first one.
+int sp_run_batches(sp_ctx* ctx, int32_t n, const int64_t* const* offsets,
+                   const int64_t* offsets_len, const int64_t* const* indices,
+                   const int64_t* indices_len, double* step_ms) {
+  return guarded([&] {
+    check_ctx(ctx);
+    sp_ctx* c = ctx;
+    if (n < 1 || offsets == nullptr || indices == nullptr || offsets_len == nullptr ||
+        indices_len == nullptr)
+      raise(SP_ERR_BAD_INPUT, "sp_run_batches needs n >= 1 batches");
+    if (n > c->step_flags_cap) {
+      SP_CUDA(cudaStreamSynchronize(c->stream));
+      if (c->d_step_flags) cudaFree(c->d_step_flags);
+      SP_CUDA(cudaMalloc(&c->d_step_flags, n * sizeof(int32_t)));
+      c->step_flags_cap = n;
+    }
+    std::vector<cudaEvent_t> ev(n + 1);
+    for (auto& e : ev) SP_CUDA(cudaEventCreate(&e));
+    try {
+      for (int s = 0; s < n; ++s) {
+        host_validate_and_size(c, offsets[s], offsets_len[s], indices_len[s], true);
+        if (s == 0) SP_CUDA(cudaEventRecord(ev[0], c->copy_stream));
+        enqueue_batch_step(c, offsets[s], indices[s], c->d_step_flags + s, s & 1, s > 0);
+        SP_CUDA(cudaEventRecord(ev[s + 1], c->stream));
+      }
+      std::vector<int32_t> flags(n);
+      SP_CUDA(cudaMemcpyAsync(flags.data(), c->d_step_flags, n * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost, c->stream));
+      SP_CUDA(cudaStreamSynchronize(c->stream));
+      if (step_ms)
+        for (int s = 0; s < n; ++s) step_ms[s] = elapsed(ev[s], ev[s + 1]);
+      for (auto& e : ev) cudaEventDestroy(e);
+      ev.clear();
+      for (int s = 0; s < n; ++s)
+        if (flags[s]) {
+          try {
+            raise_batch_flag(flags[s]);
+          } catch (const Status& e) {
+            raise(e.code, "step " + std::to_string(s) + ": " + e.what());
+          }
+        }
+      c->has_batch = true;
+    } catch (...) {
+      for (auto& e : ev) cudaEventDestroy(e);
+      throw;
+    }
   });
 }
 

@@ -96,3 +96,45 @@ def test_run_batch_rejects_bad_batch_without_update(chunking):
     # a good batch afterwards works
     sh.run_batch(LookupBatch(idx, off, 3, B))
     sh.close()
+
+
+def test_run_batches_equals_sequential_steps(chunking):
+    """sp_run_batches (step s's H2D under step s-1's compute) == the same
+    steps one sp_run_batch at a time, bit for bit; a bad step in the middle
+    updates nothing and is reported by index."""
+    B = 96
+    dims = [16, 64, 32, 128, 8]
+    task, placement = random_task(77, dims, 1, B)
+    weights = random_weights(21, task.tables)
+    batches = []
+    for seed in (3, 4, 5):
+        off, idx = orc.synth_batch(as_dicts(task.tables), B, seed=seed)
+        batches.append(LookupBatch(idx, off, len(dims), B))
+    grad = np.random.default_rng(8).uniform(-1, 1, size=(B, sum(dims))).astype(np.float32)
+    a = _shard(task, placement, weights, 0.02)
+    a.set_grad(grad)
+    ms = a.run_batches(batches)
+    assert len(ms) == 3 and all(m > 0 for m in ms)
+    b = _shard(task, placement, weights, 0.02)
+    b.set_grad(grad)
+    for bt in batches:
+        b.run_batch(bt)
+    for i in range(len(dims)):
+        np.testing.assert_array_equal(a.get_table(i), b.get_table(i))
+    # bad middle step
+    bad_idx = batches[1].indices.copy()
+    bad_idx[0] = -1
+    bad = LookupBatch(bad_idx, batches[1].offsets, len(dims), B)
+    c = _shard(task, placement, weights, 0.02)
+    c.set_grad(grad)
+    with pytest.raises(ShardplanError) as e:
+        c.run_batches([batches[0], bad, batches[2]])
+    assert e.value.kind == "bad_input" and "step 1" in str(e.value)
+    d = _shard(task, placement, weights, 0.02)
+    d.set_grad(grad)
+    d.run_batch(batches[0])
+    d.run_batch(batches[2])
+    for i in range(len(dims)):
+        np.testing.assert_array_equal(c.get_table(i), d.get_table(i))
+    for sh in (a, b, c, d):
+        sh.close()
