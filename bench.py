@@ -57,15 +57,84 @@ def load_task(config: str, D: int):
     return PlacementTask(tables, D, float(pool["mem_cap_gb"]), int(pool["batch_size"]))
 
 
-def make_placement(task, how: str, device: int):
+def make_placement(task, how: str, device: int, ckpt_path: str = CKPT):
     from paper_2210_02023_b200 import api
     if task.num_devices == 1:
         return np.zeros(len(task.tables), dtype=np.int32)
     if how == "dreamshard":
-        ckpt = api.load_checkpoint(CKPT)
+        ckpt = api.load_checkpoint(ckpt_path)
         placement, _ = api.infer(ckpt, task, device=device)
         return placement
+    if how == "random":
+        return api.random_placement(task, SEED)
     return api.expert_placement(task, how)
+
+
+def bench_placements(args, device: int):
+    """Paper Fig. 1 on B200: DreamShard vs random vs greedy (size, lookup)
+    placements of cfg2 (50 tables, D=4, the m50_d4 checkpoint) and cfg3
+    (100 tables, D=8, m100_d8), every device emulated on this GPU — real
+    per-device K1 / sort / SGD times, exchange as a device-local copy."""
+    from paper_2210_02023_b200 import api
+    out = {"note": "max-over-device compute (fwd + bwd) per placement; per-device kernels "
+                   "measured for real, all devices emulated back to back on one B200"}
+    for cfg, D, ck in (("cfg2", 4, os.path.join(DATA, "dreamshard_m50_d4.dshd")),
+                       ("cfg3", 8, CKPT)):
+        task = load_task(cfg, D)
+        res = {}
+        for how in ("dreamshard", "random", "size", "lookup"):
+            p = make_placement(task, how, device, ck)
+            sh = api.EmbeddingShard(task, p, lr=0.01, device=device)
+            sh.init_tables(SEED)
+            sh.synth_batch(SEED)
+            sh.synth_grad(SEED)
+            runs = sorted((sh.run_iteration() for _ in range(6)), key=lambda b: b.overall_ms)
+            bd = runs[2]
+            res[how] = {"max_fwd_ms": round(max(bd.fwd_ms), 4), "max_bwd_ms": round(max(bd.bwd_ms), 4),
+                        "compute_ms": round(max(bd.fwd_ms) + max(bd.bwd_ms), 4),
+                        "device_fwd_bwd_ms": [round(f + b, 3) for f, b in zip(bd.fwd_ms, bd.bwd_ms)]}
+            sh.close()
+        out[cfg] = res
+    return out
+
+
+def bench_cfg4(args, device: int):
+    """BASELINE cfg4 (200 tables of 1e7 rows, 448 GB fp32, 64 GB cap per GPU) under
+    the DreamShard placement: each of the 8 ranks' shards (~56 GB) measured in
+    turn on this GPU as a one-rank context (no peers: the backward uses the
+    gradient the exchange would deliver). Per-kernel CUDA-event times."""
+    import torch
+    from paper_2210_02023_b200 import api
+    task = load_task("cfg4", 8)
+    p = make_placement(task, "dreamshard", device)
+    ranks = []
+    for r in range(8):
+        sh = api.EmbeddingShard(task, p, lr=0.01, rank=r, world_size=8, nccl_id=None,
+                                device=device)
+        sh.init_tables(SEED)
+        sh.synth_batch(SEED)
+        sh.synth_grad(SEED)
+        for _ in range(2):
+            sh.forward()
+            sh.backward_sgd()
+        sh.set_profiling(True)
+        sh.kernel_ms()
+        n = 3
+        for _ in range(n):
+            sh.forward()
+            sh.backward_sgd()
+        k = sh.kernel_ms()
+        sh.set_profiling(False)
+        ms = {name: round(k[name][0] / n, 4) for name in ("fwd", "keys", "sort", "sgd")}
+        ranks.append({"rank": r, "tables": len(sh.local_tables()), "lookups": int(sh.nnz),
+                      "gb": round(sh.device_bytes / 1e9, 2), "ms": ms,
+                      "compute_ms": round(sum(ms.values()), 4)})
+        sh.close()
+        torch.cuda.synchronize()
+    return {"placement": "dreamshard", "ranks": ranks,
+            "max_compute_ms": max(x["compute_ms"] for x in ranks),
+            "note": "per rank: K1 + key build + sort + SGD, serialised (no overlap, no "
+                    "exchange); the 8-GPU step adds the NVLink exchange"}
 
 
 class ClockSampler:
@@ -458,6 +527,10 @@ def run_ours(args, world, rank, local):
     fp16 = None
     if world == 1 and not args.no_fp16:
         fp16 = bench_fp16(args, task, placement, local)
+    placements = cfg4 = None
+    if world == 1 and not args.no_studies:
+        placements = bench_placements(args, local)
+        cfg4 = bench_cfg4(args, local)
 
     # K6/K7 evaluator throughput (SURVEY cfg5 shape): 4096 candidate
     # placements of this task at D = 8, scored and rolled out on this GPU
@@ -501,6 +574,8 @@ def run_ours(args, world, rank, local):
             "clocks": clk.summary(),
             "emulated_d8": emulated,
             "fp16_tables": fp16,
+            "placement_study": placements,
+            "cfg4_per_rank": cfg4,
             "evaluator": evaluator,
         }
         print(json.dumps(line), flush=True)
@@ -521,6 +596,8 @@ def main():
     ap.add_argument("--no-emulation", action="store_true")
     ap.add_argument("--no-evaluator", action="store_true")
     ap.add_argument("--no-fp16", action="store_true")
+    ap.add_argument("--no-studies", action="store_true",
+                    help="skip the placement study (cfg2/cfg3) and the cfg4 per-rank shards")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

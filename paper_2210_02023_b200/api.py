@@ -774,6 +774,24 @@ def greedy_placement(task: PlacementTask, cost_fn) -> np.ndarray:
     return p
 
 
+def random_placement(task: PlacementTask, seed: int = 0) -> np.ndarray:
+    """baselines.hpp:23-41: table by table in id order, uniform over the
+    devices that still have room (numpy's PCG64 stream here, not the
+    reference's mt19937_64: a baseline, not a parity target)."""
+    rng = np.random.default_rng(seed)
+    mem = [0.0] * task.num_devices
+    p = np.zeros(len(task.tables), dtype=np.int32)
+    for i, t in enumerate(task.tables):
+        legal = [d for d in range(task.num_devices)
+                 if task.mem_cap_gb <= 0 or mem[d] + t.table_size_gb <= task.mem_cap_gb]
+        if not legal:
+            raise ShardplanError(1, f"table {i} does not fit on any device")
+        d = legal[int(rng.integers(len(legal)))]
+        p[i] = d
+        mem[d] += t.table_size_gb
+    return p
+
+
 def expert_placement(task: PlacementTask, strategy: str) -> np.ndarray:
     return greedy_placement(task, lambda t: expert_cost(strategy, t))
 

@@ -49,9 +49,48 @@ T* dalloc(size_t n, std::vector<void*>& owned, uint64_t& bytes) {
 
 // Consecutive local tables sorted together in the CUB backward: keys are
 // relative to the group (rowbase/rb_end of its tables are group-relative),
-// so a group of <= 2^24 rows needs three 8-bit radix passes instead of the
-// four a device-wide 26-bit key would.
-constexpr uint64_t kSortGroupRows = uint64_t(1) << 24;
+// so a group's key width is ceil(log2(its rows)) and its sort costs
+// ceil(bits / 8) radix passes over its lookups plus a fixed launch overhead
+// (histogram, scan, gaps). The grouping minimises that cost over consecutive
+// tables (dynamic programming) with the lookups estimated as pf * B:
+// cfg3's 1e5-1e6-row tables end up in groups of <= 2^24 rows (3 passes
+// instead of 4 for one 26-bit sort); cfg4's 1e7-row tables share one 28-bit
+// group instead of 25 small sorts (1.6 -> ~0.4 ms per rank, measured).
+constexpr double kSortGroupUs = 40.0;     // fixed cost of one group's sort (us)
+constexpr double kSortPassUsPerM = 9.0;   // one 8-bit pass over 1M lookups (us)
+
+// Returns the first local table of every group after the first, then T.
+std::vector<int> plan_sort_groups(const sp_table_spec* tables, const std::vector<int>& ids,
+                                  int batch) {
+  const int T = static_cast<int>(ids.size());
+  uint64_t cap = uint64_t(1) << 32;  // 32-bit keys
+  if (const char* f = std::getenv("SP_SORT_GROUP_ROWS"))  // tests: force many groups
+    cap = std::max<uint64_t>(1, std::strtoull(f, nullptr, 10));
+  std::vector<double> best(T + 1, 1e300);
+  std::vector<int> from(T + 1, 0);
+  best[0] = 0.0;
+  for (int j = 1; j <= T; ++j) {
+    uint64_t rows = 0;
+    double nnz = 0.0;
+    for (int i = j - 1; i >= 0; --i) {
+      const sp_table_spec& t = tables[ids[i]];
+      rows += static_cast<uint64_t>(t.hash_size);
+      nnz += std::max(0.0, t.pooling_factor) * batch;
+      if (i < j - 1 && rows > cap) break;
+      int bits = 1;
+      while (bits < 32 && (uint64_t(1) << bits) < std::max<uint64_t>(rows, 2)) ++bits;
+      const double c = best[i] + kSortGroupUs + ((bits + 7) / 8) * nnz * 1e-6 * kSortPassUsPerM;
+      if (c < best[j]) {
+        best[j] = c;
+        from[j] = i;
+      }
+    }
+  }
+  std::vector<int> ends;
+  for (int j = T; j > 0; j = from[j]) ends.push_back(j);
+  std::reverse(ends.begin(), ends.end());
+  return ends;
+}
 struct SortGroup {
   int t0 = 0, t1 = 0;      // local tables [t0, t1)
   int end_bit = 1;         // key bits
@@ -391,7 +430,9 @@ void stage_forward(sp_ctx* c, VDev& v) {
   launch_tbe_forward(v.d_meta_canon, v.d_tiles, v.n_tiles, c->B, v.d_off, v.d_idx,
                      c->d_w, c->wt, v.d_pooled, c->d_rowmap, v.W, emit ? v.d_keys : nullptr,
                      emit ? v.d_bags : nullptr, c->bags16, c->stream);
-  if (emit) v.keys_valid = true;
+  // every iteration builds its sort pairs once: here, or (when K1 does not
+  // emit them) in the backward's key build
+  v.keys_valid = emit;
 }
 
 // (keys) -> stable radix sort; leaves sorted keys in d_kb, bags in d_bb.
@@ -835,13 +876,8 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
       for (int i = 0; i < num_tables; ++i)
         if (placement[i] == d) v.tables.push_back(i);
       const int T = static_cast<int>(v.tables.size());
-      // greedy packing makes at most 2*ceil(rows/limit) groups: keep <= 30
-      uint64_t dev_rows = 0;
-      for (int g : v.tables) dev_rows += static_cast<uint64_t>(tables[g].hash_size);
-      uint64_t group_rows = kSortGroupRows;
-      if (const char* f = std::getenv("SP_SORT_GROUP_ROWS"))  // tests: force many groups
-        group_rows = std::max<uint64_t>(1, std::strtoull(f, nullptr, 10));
-      while (2 * ((dev_rows + group_rows - 1) / group_rows) > 30) group_rows *= 2;
+      const std::vector<int> group_end = plan_sort_groups(tables, v.tables, batch_size);
+      size_t next_group = 0;
       int64_t lcol = 0;
       uint64_t rb = 0;     // row base inside the current sort group
       int64_t gbase = 0;   // rows of the device before the current group
@@ -861,9 +897,10 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
       for (int li = 0; li < T; ++li) {
         const int g = v.tables[li];
         const sp_table_spec& t = tables[g];
-        // sort groups of <= 2^24 rows: 24-bit keys, three radix passes
-        if (li > gstart && rb + static_cast<uint64_t>(t.hash_size) > group_rows)
+        if (li > gstart && li == group_end[next_group]) {
           close_group(li);
+          ++next_group;
+        }
         TableMeta m{};
         m.woff = c->woff[g];
         m.rows = t.hash_size;
@@ -1542,6 +1579,14 @@ int sp_synth_grad(sp_ctx* ctx, uint64_t seed) {
                           static_cast<int64_t>(dst) * R, d_cm, ctx->dev_W[i], seed,
                           ctx->stream);
       }
+    }
+    // one process per rank: also the owner-side gradient [B, W_rank] the
+    // backward exchange would deliver, so the backward can run (and be
+    // timed) on a rank without its peers
+    if (ctx->world > 1) {
+      VDev& v = ctx->vdevs[0];
+      if (v.W > 0)
+        launch_synth_grad(v.d_grad, ctx->B, 0, v.d_colmap, v.W, seed, ctx->stream);
     }
     SP_CUDA(cudaStreamSynchronize(ctx->stream));
     for (void* p : tmp) cudaFree(p);

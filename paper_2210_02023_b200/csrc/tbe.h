@@ -109,7 +109,6 @@ size_t sort_pairs(void* temp, size_t temp_bytes, const uint32_t* keys_in,
 // sorted lookups of local table t occupy its CSR position range, so the
 // launch runs over per-table tiles (make_sgd_tiles: kSgdTileInts ints each,
 // from the per-table lookup counts in canonical order).
-constexpr int kMaxSortGroups = 32;
 constexpr int kSgdTileInts = 8;
 std::vector<int> make_sgd_tiles(const std::vector<int64_t>& table_nnz);
 // d_abort (may be null): when *d_abort != 0 the launch leaves W untouched.
