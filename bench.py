@@ -290,6 +290,40 @@ def config_dict(args, task):
             "parallelism": f"table-wise model parallel x{task.num_devices}"}
 
 
+def bench_evaluator_sweep(device: int, n: int = 4096):
+    """BASELINE cfg5: the generalisation sweep, M in {20, 50, 100, 200} tables x
+    D in {1, 2, 4, 8} devices, 4096 greedy rollouts and 4096 cost-net scorings of
+    random placements per task on the GPU evaluator (m100_d8 checkpoint;
+    tables from the cfg3 pool, repeated for M = 200)."""
+    import torch
+    from paper_2210_02023_b200 import api
+    ckpt = api.load_checkpoint(CKPT)
+    base = load_task("cfg3", 8)
+    rows = []
+    for M in (20, 50, 100, 200):
+        tabs = [base.tables[i % len(base.tables)] for i in range(M)]
+        tabs = [api.TableDesc(i, t.dim, t.hash_size, t.pooling_factor, t.table_size_gb, t.dist)
+                for i, t in enumerate(tabs)]
+        for D in (1, 2, 4, 8):
+            task = api.PlacementTask(tabs, D, base.mem_cap_gb, base.batch_size)
+            ev = api.Evaluator(ckpt, task, device=device)
+            rng = np.random.default_rng(M * 10 + D)
+            placements = rng.integers(0, D, size=(n, M)).astype(np.int32)
+            r = {"tables": M, "devices": D}
+            for name, fn in (("eval_batch_ms", lambda: ev.eval_batch(placements)),
+                             ("greedy_rollouts_ms", lambda: ev.rollout(n, "greedy"))):
+                fn()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                fn()
+                torch.cuda.synchronize()
+                r[name] = round((time.perf_counter() - t0) * 1e3, 3)
+            ev.close()
+            rows.append(r)
+    return {"candidates": n, "rows": rows,
+            "note": "host wall ms per call (4096 candidates) incl. H2D/D2H"}
+
+
 def bench_fp16(args, task, placement, device: int):
     """The same iteration with the tables stored in fp16 (2 B/param): device
     ms/iter over the timed loop and each hot kernel in isolation."""
@@ -537,6 +571,7 @@ def run_ours(args, world, rank, local):
     evaluator = None
     if rank == 0 and not args.no_evaluator:
         evaluator = bench_evaluator(args, local)
+        evaluator["sweep"] = bench_evaluator_sweep(local)
 
     if rank == 0:
         line = {
