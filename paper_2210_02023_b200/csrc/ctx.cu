@@ -427,6 +427,17 @@ bool overlap_active(const sp_ctx* c) {
 void stage_forward(sp_ctx* c, VDev& v) {
   const bool emit = c->fuse_keys && !v.bucketed && v.nnz > 0 && !overlap_active(c);
   ProfScope prof(c, kProfFwd);
+  static const bool per_table = std::getenv("SP_K1_PER_TABLE") != nullptr;  // diagnostic
+  if (per_table) {
+    for (size_t li = 0; li < v.tables.size(); ++li)
+      launch_tbe_forward(v.d_meta_canon, v.d_tiles_canon + v.tile_start[li],
+                         v.tile_start[li + 1] - v.tile_start[li], c->B, v.d_off, v.d_idx,
+                         c->d_w, c->wt, v.d_pooled, c->d_rowmap, v.W,
+                         emit ? v.d_keys : nullptr, emit ? v.d_bags : nullptr, c->bags16,
+                         c->stream);
+    v.keys_valid = emit;
+    return;
+  }
   launch_tbe_forward(v.d_meta_canon, v.d_tiles, v.n_tiles, c->B, v.d_off, v.d_idx,
                      c->d_w, c->wt, v.d_pooled, c->d_rowmap, v.W, emit ? v.d_keys : nullptr,
                      emit ? v.d_bags : nullptr, c->bags16, c->stream);
