@@ -338,6 +338,38 @@ int sp_rollout_batch(sp_evaluator* ev, int32_t mode, const double* uniforms,
                      int32_t n_cand, int32_t precision, int32_t* placements,
                      double* predicted, int32_t* status, int32_t* n_refined);
 
+/* ---- GPU training of the cost network ----------------------
+ * costnet_loss_and_grad (costnet.hpp:349-427) + AdamState::update with
+ * linear decay (nn.hpp:163-200) in fp64 on the device, the parameters
+ * resident there between steps. params: CostNet::param_vector order
+ * (15652: table 21-128-32, heads fwd/bwd/comm/overall 32-64-1). features:
+ * the normalised feature rows (TaskFeatures.rows of every task) [n_rows][21];
+ * a sample's tables are rows of that array. Predictions are bit-identical
+ * to the reference; gradients equal it up to the association of the final
+ * sum over the minibatch (deterministic). */
+typedef struct sp_costnet_trainer sp_costnet_trainer;
+typedef struct sp_costnet_batch {  /* CostSample list (costnet.hpp:297-304) */
+  int32_t n_samples;
+  const int32_t* dev_off;          /* [n+1]: devices of sample s */
+  const int32_t* tab_off;          /* [dev_off[n]+1]: tables of device d */
+  const int32_t* tab_row;          /* feature row of each table (any order) */
+  const double* target_q;          /* [dev_off[n]][3] */
+  const double* target_overall;    /* [n], NaN = no overall target; may be NULL */
+} sp_costnet_batch;
+int sp_costnet_trainer_create(const double* params, int64_t n_params, const double* features,
+                              int64_t n_rows, const double* mask, int32_t red_tables,
+                              int32_t red_devices, int32_t table_output_relu, double lr,
+                              int64_t total_steps, int32_t cuda_device,
+                              sp_costnet_trainer** out);
+void sp_costnet_trainer_destroy(sp_costnet_trainer* t);
+/* loss (and optionally grad[15652]) of one minibatch, no update */
+int sp_costnet_loss_grad(sp_costnet_trainer* t, const sp_costnet_batch* batch, double* loss,
+                         double* grad);
+/* one step of costnet_train_steps (costnet.hpp:431-446) on a given minibatch */
+int sp_costnet_train_step(sp_costnet_trainer* t, const sp_costnet_batch* batch, double* loss);
+int sp_costnet_trainer_get(sp_costnet_trainer* t, double* params, double* m, double* v,
+                           int64_t* step);
+
 #ifdef __cplusplus
 }
 #endif

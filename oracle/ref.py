@@ -100,6 +100,14 @@ def lib():
             c_i32_p, c_double_p, c_i32_p, c_double_p]
         L.ref_feature_vector.argtypes = [ctypes.c_void_p, c_double_p, c_double_p,
                                          c_double_p]
+        L.ref_rng_index.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, c_i64_p]
+        _cost = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, c_double_p,
+                 ctypes.c_int64, ctypes.c_int, c_i32_p, c_i32_p, c_i32_p, c_double_p,
+                 c_double_p]
+        L.ref_costnet_loss_grad.argtypes = [c_double_p] + _cost + [c_double_p, c_double_p]
+        L.ref_costnet_train_steps.argtypes = [c_double_p] + _cost + [
+            ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int64, ctypes.c_uint64,
+            c_double_p]
         _lib = L
     return _lib
 
@@ -277,3 +285,44 @@ def action_probs(ckpt, tables, D, partial, q, legal):
                                   _p(q, ctypes.c_double), _p(legal, ctypes.c_int32),
                                   _p(probs, ctypes.c_double)))
     return probs
+
+
+def rng_index(seed, n, bound):
+    """n draws of Rng(seed).index(bound) (rng.hpp:48-54)."""
+    out = np.zeros(n, dtype=np.int64)
+    lib().ref_rng_index(seed, n, bound, _p(out, ctypes.c_int64))
+    return out
+
+
+def _cost_args(batch, features, mask, red_tables, red_devices, table_relu):
+    f = np.ascontiguousarray(features, dtype=np.float64)
+    m = None if mask is None else np.ascontiguousarray(mask, dtype=np.float64)
+    return [red_tables, red_devices, table_relu,
+            None if m is None else m.ctypes.data_as(ctypes.c_void_p),
+            _p(f, ctypes.c_double), f.shape[0], batch["n"],
+            _p(np.ascontiguousarray(batch["dev_off"], dtype=np.int32), ctypes.c_int32), _p(np.ascontiguousarray(batch["tab_off"], dtype=np.int32), ctypes.c_int32),
+            _p(np.ascontiguousarray(batch["tab_row"], dtype=np.int32), ctypes.c_int32), _p(np.ascontiguousarray(batch["target_q"], dtype=np.float64), ctypes.c_double),
+            _p(np.ascontiguousarray(batch["target_overall"], dtype=np.float64), ctypes.c_double)], (f, m)
+
+
+def costnet_loss_grad(params, batch, features, mask=None, red_tables=0, red_devices=2,
+                      table_relu=0):
+    """costnet_loss_and_grad (costnet.hpp:349-427) of the reference."""
+    p = np.ascontiguousarray(params, dtype=np.float64)
+    args, keep = _cost_args(batch, features, mask, red_tables, red_devices, table_relu)
+    grad = np.zeros_like(p)
+    loss = np.zeros(1)
+    _check(lib().ref_costnet_loss_grad(_p(p, ctypes.c_double), *args, _p(grad, ctypes.c_double),
+                                       _p(loss, ctypes.c_double)))
+    return float(loss[0]), grad
+
+
+def costnet_train_steps(params, batch, features, n_steps, n_batch, lr, total_steps, seed,
+                        mask=None, red_tables=0, red_devices=2, table_relu=0):
+    """costnet_train_steps (costnet.hpp:431-446), batches from Rng(seed)."""
+    p = np.array(params, dtype=np.float64, copy=True)
+    args, keep = _cost_args(batch, features, mask, red_tables, red_devices, table_relu)
+    ml = np.zeros(1)
+    _check(lib().ref_costnet_train_steps(_p(p, ctypes.c_double), *args, n_steps, n_batch, lr,
+                                         total_steps, seed, _p(ml, ctypes.c_double)))
+    return p, float(ml[0])

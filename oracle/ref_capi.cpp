@@ -255,6 +255,90 @@ uint64_t ref_subseed(uint64_t seed, const char* stream) {
   return subseed(seed, stream);
 }
 
+void ref_rng_index(uint64_t seed, int64_t n, int64_t bound, int64_t* out) {
+  Rng rng(seed);
+  for (int64_t i = 0; i < n; ++i) out[i] = static_cast<int64_t>(rng.index(bound));
+}
+
+// ---- costnet.hpp training (checker of csrc/train.cu) ---------------------
+
+namespace {
+struct CostSetup {
+  CostNet net;
+  std::shared_ptr<const TaskFeatures> feats;
+  std::vector<CostSample> samples;
+};
+
+CostSetup cost_setup(const double* params, int red_tables, int red_devices, int table_relu,
+                     const double* mask, const double* features, int64_t n_rows, int n,
+                     const int32_t* dev_off, const int32_t* tab_off, const int32_t* tab_row,
+                     const double* target_q, const double* target_ov) {
+  CostSetup c;
+  FeatureMask fm = full_feature_mask();
+  if (mask)
+    for (int f = 0; f < kNumFeatures; ++f) fm[f] = mask[f] != 0.0;
+  c.net = CostNet::make(0, static_cast<Reduction>(red_tables), static_cast<Reduction>(red_devices),
+                        fm, table_relu != 0);
+  std::vector<double> pv(params, params + c.net.param_count());
+  c.net.set_param_vector(pv);
+  auto tf = std::make_shared<TaskFeatures>();
+  for (int64_t r = 0; r < n_rows; ++r) {
+    FeatureVec v{};
+    for (int f = 0; f < kNumFeatures; ++f) v[f] = features[r * kNumFeatures + f];
+    tf->rows.push_back(v);
+  }
+  c.feats = tf;
+  for (int s = 0; s < n; ++s) {
+    CostSample cs;
+    cs.features = c.feats;
+    for (int d = dev_off[s]; d < dev_off[s + 1]; ++d) {
+      cs.device_tables.emplace_back(tab_row + tab_off[d], tab_row + tab_off[d + 1]);
+      cs.target_q.push_back({target_q[3 * d], target_q[3 * d + 1], target_q[3 * d + 2]});
+    }
+    if (target_ov && !std::isnan(target_ov[s])) cs.target_overall = target_ov[s];
+    c.samples.push_back(std::move(cs));
+  }
+  return c;
+}
+}  // namespace
+
+int ref_costnet_loss_grad(const double* params, int red_tables, int red_devices, int table_relu,
+                          const double* mask, const double* features, int64_t n_rows, int n,
+                          const int32_t* dev_off, const int32_t* tab_off, const int32_t* tab_row,
+                          const double* target_q, const double* target_ov, double* grad,
+                          double* loss) {
+  return guarded([&] {
+    CostSetup c = cost_setup(params, red_tables, red_devices, table_relu, mask, features,
+                             n_rows, n, dev_off, tab_off, tab_row, target_q, target_ov);
+    std::vector<const CostSample*> batch;
+    for (const CostSample& s : c.samples) batch.push_back(&s);
+    std::vector<double> g;
+    *loss = costnet_loss_and_grad(c.net, batch, g);
+    std::copy(g.begin(), g.end(), grad);
+  });
+}
+
+// costnet_train_steps (costnet.hpp:431-446) over the samples as the replay
+// buffer, minibatches drawn by Rng(seed); params updated in place.
+int ref_costnet_train_steps(double* params, int red_tables, int red_devices, int table_relu,
+                            const double* mask, const double* features, int64_t n_rows, int n,
+                            const int32_t* dev_off, const int32_t* tab_off,
+                            const int32_t* tab_row, const double* target_q,
+                            const double* target_ov, int n_steps, int n_batch, double lr,
+                            int64_t total_steps, uint64_t seed, double* mean_loss) {
+  return guarded([&] {
+    CostSetup c = cost_setup(params, red_tables, red_devices, table_relu, mask, features,
+                             n_rows, n, dev_off, tab_off, tab_row, target_q, target_ov);
+    ReplayBuffer buf;
+    for (CostSample& s : c.samples) buf.add(std::move(s));
+    AdamState adam(c.net.param_count(), lr, total_steps);
+    Rng rng(seed);
+    *mean_loss = costnet_train_steps(c.net, buf, n_steps, n_batch, adam, rng);
+    const std::vector<double> pv = c.net.param_vector();
+    std::copy(pv.begin(), pv.end(), params);
+  });
+}
+
 // ---- harness.hpp / checkpoint.hpp ---------------------------------------
 
 int ref_train(const sp_table_spec* pool_tables, int n_pool, int batch,

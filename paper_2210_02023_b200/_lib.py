@@ -57,6 +57,12 @@ SIGNATURES = {
     "sp_ctx_algorithmic_bytes": (c_i32, [c_vp, P(c_f64)]),
     "sp_ctx_set_profiling": (c_i32, [c_vp, c_i32]),
     "sp_ctx_set_overlap": (c_i32, [c_vp, c_i32]),
+    "sp_costnet_trainer_create": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i32, c_i32, c_i32,
+                                          c_f64, c_i64, c_i32, P(c_vp)]),
+    "sp_costnet_trainer_destroy": (None, [c_vp]),
+    "sp_costnet_loss_grad": (c_i32, [c_vp, c_vp, P(c_f64), c_vp]),
+    "sp_costnet_train_step": (c_i32, [c_vp, c_vp, P(c_f64)]),
+    "sp_costnet_trainer_get": (c_i32, [c_vp, c_vp, c_vp, c_vp, P(c_i64)]),
     "sp_ipc_export": (c_i32, [c_vp, c_vp]),
     "sp_ipc_import": (c_i32, [c_vp, c_vp]),
     "sp_ctx_synchronize": (c_i32, [c_vp]),
@@ -84,6 +90,19 @@ class SpTableSpec(ctypes.Structure):
         ("pooling_factor", c_f64),
         ("table_size_gb", c_f64),
         ("dist", c_f64 * 17),
+    ]
+
+
+class SpCostnetBatch(ctypes.Structure):
+    """sp_costnet_batch: a CostSample list (costnet.hpp:297-304)."""
+
+    _fields_ = [
+        ("n_samples", c_i32),
+        ("dev_off", c_vp),
+        ("tab_off", c_vp),
+        ("tab_row", c_vp),
+        ("target_q", c_vp),
+        ("target_overall", c_vp),
     ]
 
 

@@ -28,7 +28,7 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
-from ._lib import SpBreakdown, SpNets, SpTableSpec, ShardplanError, check, lib
+from ._lib import SpBreakdown, SpCostnetBatch, SpNets, SpTableSpec, ShardplanError, check, lib
 
 NUM_BINS = 17
 NUM_FEATURES = 21
@@ -578,6 +578,92 @@ class MeasuredCostProvider(CostProvider):
 # checkpoint.hpp (DSHD) and the GPU evaluator
 
 REDUCTIONS = {"sum": 0, "mean": 1, "max": 2}
+
+
+class CostNetTrainer:
+    """GPU training of the cost network (sp_costnet_trainer): the parameters
+    stay on the device; each step is costnet_loss_and_grad + Adam with linear
+    decay (costnet.hpp:349-446, nn.hpp:163-200) in fp64.
+
+    A batch is a dict: n, dev_off[n+1], tab_off[devices+1], tab_row (feature
+    row of each table), target_q[devices][3], target_overall[n] (NaN = none).
+    """
+
+    N_PARAMS = 15652
+
+    def __init__(self, params, features, mask=None, red_tables: int = 0,
+                 red_devices: int = 2, table_output_relu: bool = False, lr: float = 5e-4,
+                 total_steps: int = 0, device: int = 0):
+        p = np.ascontiguousarray(params, dtype=np.float64)
+        f = np.ascontiguousarray(features, dtype=np.float64)
+        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.float64)
+        h = ctypes.c_void_p()
+        check(lib().sp_costnet_trainer_create(_ptr(p), p.size, _ptr(f), f.shape[0],
+                                              _ptr(m) if m is not None else None, red_tables,
+                                              red_devices, int(table_output_relu), lr,
+                                              total_steps, device, ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().sp_costnet_trainer_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 (interpreter shutdown)
+            pass
+
+    @staticmethod
+    def _batch(b):
+        arrs = {k: np.ascontiguousarray(b[k], dtype=np.int32) for k in ("dev_off", "tab_off",
+                                                                         "tab_row")}
+        arrs["target_q"] = np.ascontiguousarray(b["target_q"], dtype=np.float64)
+        arrs["target_overall"] = np.ascontiguousarray(b["target_overall"], dtype=np.float64)
+        sb = SpCostnetBatch(int(b["n"]), arrs["dev_off"].ctypes.data,
+                                 arrs["tab_off"].ctypes.data, arrs["tab_row"].ctypes.data,
+                                 arrs["target_q"].ctypes.data,
+                                 arrs["target_overall"].ctypes.data)
+        return sb, arrs
+
+    def loss_grad(self, batch):
+        sb, keep = self._batch(batch)
+        loss = ctypes.c_double()
+        grad = np.zeros(self.N_PARAMS)
+        check(lib().sp_costnet_loss_grad(self._h, ctypes.byref(sb), ctypes.byref(loss),
+                                         _ptr(grad)))
+        return loss.value, grad
+
+    def step(self, batch) -> float:
+        sb, keep = self._batch(batch)
+        loss = ctypes.c_double()
+        check(lib().sp_costnet_train_step(self._h, ctypes.byref(sb), ctypes.byref(loss)))
+        return loss.value
+
+    def state(self):
+        p = np.zeros(self.N_PARAMS)
+        m = np.zeros(self.N_PARAMS)
+        v = np.zeros(self.N_PARAMS)
+        st = ctypes.c_int64()
+        check(lib().sp_costnet_trainer_get(self._h, _ptr(p), _ptr(m), _ptr(v), ctypes.byref(st)))
+        return p, m, v, st.value
+
+
+def costnet_subbatch(batch, picks):
+    """The minibatch of samples `picks` of a batch dict (replay-buffer draws)."""
+    dev_off, tab_off = batch["dev_off"], batch["tab_off"]
+    do, to, rows, tq, tov = [0], [0], [], [], []
+    for s in picks:
+        for d in range(dev_off[s], dev_off[s + 1]):
+            rows.extend(batch["tab_row"][tab_off[d]:tab_off[d + 1]])
+            to.append(len(rows))
+            tq.append(batch["target_q"][d])
+        do.append(len(to) - 1)
+        tov.append(batch["target_overall"][s])
+    return {"n": len(picks), "dev_off": np.array(do), "tab_off": np.array(to),
+            "tab_row": np.array(rows, dtype=np.int32), "target_q": np.array(tq).reshape(-1, 3),
+            "target_overall": np.array(tov)}
 
 
 @dataclass
