@@ -370,6 +370,39 @@ int sp_costnet_train_step(sp_costnet_trainer* t, const sp_costnet_batch* batch, 
 int sp_costnet_trainer_get(sp_costnet_trainer* t, double* params, double* m, double* v,
                            int64_t* step);
 
+/* REINFORCE on the policy network (policy.hpp:203-296) in fp64 on the
+ * device: params in PolicyNet::param_vector order (9345: table 21-128-32,
+ * cost 3-64-32, head 64-1). An episode is a list of steps (the state's
+ * device_tables, q, legal mask, action) of one task whose tables are the
+ * feature rows row0 .. row0 + ntab - 1. Per-episode gradient rows summed in
+ * episode order. */
+typedef struct sp_policy_trainer sp_policy_trainer;
+typedef struct sp_reinforce_batch {  /* Episode list (policy.hpp:189-201) */
+  int32_t n_episodes;
+  const int32_t* row0;      /* [n] */
+  const int32_t* ntab;      /* [n] */
+  const int32_t* step_off;  /* [n+1] */
+  const double* reward;     /* [n] */
+  const int32_t* dev_off;   /* [steps+1] */
+  const int32_t* action;    /* [steps] */
+  const int32_t* tab_off;   /* [devices+1] */
+  const int32_t* tab_id;    /* task-local table ids (any order in a device) */
+  const int32_t* legal;     /* [devices] 0/1 */
+  const double* q;          /* [devices][3] */
+} sp_reinforce_batch;
+int sp_policy_trainer_create(const double* params, int64_t n_params, const double* features,
+                             int64_t n_rows, const double* mask, double lr,
+                             int64_t total_steps, int32_t cuda_device,
+                             sp_policy_trainer** out);
+void sp_policy_trainer_destroy(sp_policy_trainer* t);
+int sp_reinforce_loss_grad(sp_policy_trainer* t, const sp_reinforce_batch* b, double w_entropy,
+                           double* objective, double* grad);
+/* reinforce_update (policy.hpp:287-296): one Adam step */
+int sp_reinforce_step(sp_policy_trainer* t, const sp_reinforce_batch* b, double w_entropy,
+                      double* objective);
+int sp_policy_trainer_get(sp_policy_trainer* t, double* params, double* m, double* v,
+                          int64_t* step);
+
 #ifdef __cplusplus
 }
 #endif

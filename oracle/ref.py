@@ -108,6 +108,12 @@ def lib():
         L.ref_costnet_train_steps.argtypes = [c_double_p] + _cost + [
             ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int64, ctypes.c_uint64,
             c_double_p]
+        _ep = [ctypes.c_void_p, c_double_p, ctypes.c_int, c_i32_p, c_i32_p, c_i32_p,
+               c_double_p, c_i32_p, c_i32_p, c_i32_p, c_i32_p, c_i32_p, c_double_p,
+               ctypes.c_double]
+        L.ref_reinforce_loss_grad.argtypes = [c_double_p] + _ep + [c_double_p, c_double_p]
+        L.ref_reinforce_updates.argtypes = [c_double_p] + _ep + [
+            ctypes.c_int, ctypes.c_double, ctypes.c_int64, c_double_p]
         _lib = L
     return _lib
 
@@ -326,3 +332,40 @@ def costnet_train_steps(params, batch, features, n_steps, n_batch, lr, total_ste
     _check(lib().ref_costnet_train_steps(_p(p, ctypes.c_double), *args, n_steps, n_batch, lr,
                                          total_steps, seed, _p(ml, ctypes.c_double)))
     return p, float(ml[0])
+
+
+_EP_INT = ("row0", "ntab", "step_off")
+_EP_INT2 = ("dev_off", "action", "tab_off", "tab_id", "legal")
+
+
+def _ep_args(eps, features, mask, w_entropy):
+    f = np.ascontiguousarray(features, dtype=np.float64)
+    m = None if mask is None else np.ascontiguousarray(mask, dtype=np.float64)
+    ints = {k: np.ascontiguousarray(eps[k], dtype=np.int32) for k in _EP_INT + _EP_INT2}
+    rew = np.ascontiguousarray(eps["reward"], dtype=np.float64)
+    q = np.ascontiguousarray(eps["q"], dtype=np.float64)
+    args = [None if m is None else m.ctypes.data_as(ctypes.c_void_p), _p(f, ctypes.c_double),
+            int(eps["n"])] + [_p(ints[k], ctypes.c_int32) for k in _EP_INT] + [
+            _p(rew, ctypes.c_double)] + [_p(ints[k], ctypes.c_int32) for k in _EP_INT2] + [
+            _p(q, ctypes.c_double), w_entropy]
+    return args, (f, m, ints, rew, q)
+
+
+def reinforce_loss_grad(params, eps, features, w_entropy, mask=None):
+    """reinforce_loss_and_grad (policy.hpp:203-283) of the reference."""
+    p = np.ascontiguousarray(params, dtype=np.float64)
+    args, keep = _ep_args(eps, features, mask, w_entropy)
+    grad = np.zeros_like(p)
+    obj = np.zeros(1)
+    _check(lib().ref_reinforce_loss_grad(_p(p, ctypes.c_double), *args,
+                                         _p(grad, ctypes.c_double), _p(obj, ctypes.c_double)))
+    return float(obj[0]), grad
+
+
+def reinforce_updates(params, eps, features, w_entropy, n_updates, lr, total_steps, mask=None):
+    p = np.array(params, dtype=np.float64, copy=True)
+    args, keep = _ep_args(eps, features, mask, w_entropy)
+    objs = np.zeros(n_updates)
+    _check(lib().ref_reinforce_updates(_p(p, ctypes.c_double), *args, n_updates, lr,
+                                       total_steps, _p(objs, ctypes.c_double)))
+    return p, objs

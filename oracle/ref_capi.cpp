@@ -339,6 +339,87 @@ int ref_costnet_train_steps(double* params, int red_tables, int red_devices, int
   });
 }
 
+namespace {
+struct PolicySetup {
+  PolicyNet net;
+  std::vector<Episode> episodes;
+};
+
+PolicySetup policy_setup(const double* params, const double* mask, const double* features,
+                         int n, const int32_t* row0, const int32_t* ntab,
+                         const int32_t* step_off, const double* reward,
+                         const int32_t* dev_off, const int32_t* action,
+                         const int32_t* tab_off, const int32_t* tab_id, const int32_t* legal,
+                         const double* q) {
+  PolicySetup c;
+  FeatureMask fm = full_feature_mask();
+  if (mask)
+    for (int f = 0; f < kNumFeatures; ++f) fm[f] = mask[f] != 0.0;
+  c.net = PolicyNet::make(0, fm);
+  std::vector<double> pv(params, params + c.net.param_count());
+  c.net.set_param_vector(pv);
+  for (int e = 0; e < n; ++e) {
+    auto tf = std::make_shared<TaskFeatures>();
+    for (int r = 0; r < ntab[e]; ++r) {
+      FeatureVec v{};
+      for (int f = 0; f < kNumFeatures; ++f)
+        v[f] = features[(static_cast<int64_t>(row0[e]) + r) * kNumFeatures + f];
+      tf->rows.push_back(v);
+    }
+    Episode ep;
+    ep.features = tf;
+    ep.reward = reward[e];
+    for (int st = step_off[e]; st < step_off[e + 1]; ++st) {
+      EpisodeStep es;
+      for (int d = dev_off[st]; d < dev_off[st + 1]; ++d) {
+        es.device_tables.emplace_back(tab_id + tab_off[d], tab_id + tab_off[d + 1]);
+        es.q.push_back({q[3 * d], q[3 * d + 1], q[3 * d + 2]});
+        es.legal.push_back(legal[d] != 0);
+      }
+      es.action = action[st];
+      ep.steps.push_back(std::move(es));
+    }
+    c.episodes.push_back(std::move(ep));
+  }
+  return c;
+}
+}  // namespace
+
+int ref_reinforce_loss_grad(const double* params, const double* mask, const double* features,
+                            int n, const int32_t* row0, const int32_t* ntab,
+                            const int32_t* step_off, const double* reward,
+                            const int32_t* dev_off, const int32_t* action,
+                            const int32_t* tab_off, const int32_t* tab_id,
+                            const int32_t* legal, const double* q, double w_entropy,
+                            double* grad, double* objective) {
+  return guarded([&] {
+    PolicySetup c = policy_setup(params, mask, features, n, row0, ntab, step_off, reward,
+                                 dev_off, action, tab_off, tab_id, legal, q);
+    std::vector<double> g;
+    *objective = reinforce_loss_and_grad(c.net, c.episodes, w_entropy, g);
+    std::copy(g.begin(), g.end(), grad);
+  });
+}
+
+// n_updates reinforce_update calls (policy.hpp:287-296) on the same
+// episodes with one AdamState(lr, total_steps); params updated in place.
+int ref_reinforce_updates(double* params, const double* mask, const double* features, int n,
+                          const int32_t* row0, const int32_t* ntab, const int32_t* step_off,
+                          const double* reward, const int32_t* dev_off, const int32_t* action,
+                          const int32_t* tab_off, const int32_t* tab_id, const int32_t* legal,
+                          const double* q, double w_entropy, int n_updates, double lr,
+                          int64_t total_steps, double* objectives) {
+  return guarded([&] {
+    PolicySetup c = policy_setup(params, mask, features, n, row0, ntab, step_off, reward,
+                                 dev_off, action, tab_off, tab_id, legal, q);
+    AdamState adam(c.net.param_count(), lr, total_steps);
+    for (int u = 0; u < n_updates; ++u)
+      objectives[u] = reinforce_update(c.net, c.episodes, w_entropy, adam);
+    const std::vector<double> pv = c.net.param_vector();
+    std::copy(pv.begin(), pv.end(), params);
+  });
+}
+
 // ---- harness.hpp / checkpoint.hpp ---------------------------------------
 
 int ref_train(const sp_table_spec* pool_tables, int n_pool, int batch,

@@ -63,6 +63,12 @@ SIGNATURES = {
     "sp_costnet_loss_grad": (c_i32, [c_vp, c_vp, P(c_f64), c_vp]),
     "sp_costnet_train_step": (c_i32, [c_vp, c_vp, P(c_f64)]),
     "sp_costnet_trainer_get": (c_i32, [c_vp, c_vp, c_vp, c_vp, P(c_i64)]),
+    "sp_policy_trainer_create": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp, c_f64, c_i64, c_i32,
+                                         P(c_vp)]),
+    "sp_policy_trainer_destroy": (None, [c_vp]),
+    "sp_reinforce_loss_grad": (c_i32, [c_vp, c_vp, c_f64, P(c_f64), c_vp]),
+    "sp_reinforce_step": (c_i32, [c_vp, c_vp, c_f64, P(c_f64)]),
+    "sp_policy_trainer_get": (c_i32, [c_vp, c_vp, c_vp, c_vp, P(c_i64)]),
     "sp_ipc_export": (c_i32, [c_vp, c_vp]),
     "sp_ipc_import": (c_i32, [c_vp, c_vp]),
     "sp_ctx_synchronize": (c_i32, [c_vp]),
@@ -104,6 +110,14 @@ class SpCostnetBatch(ctypes.Structure):
         ("target_q", c_vp),
         ("target_overall", c_vp),
     ]
+
+
+class SpReinforceBatch(ctypes.Structure):
+    """sp_reinforce_batch: an Episode list (policy.hpp:189-201)."""
+
+    _fields_ = [("n_episodes", c_i32)] + [(k, c_vp) for k in (
+        "row0", "ntab", "step_off", "reward", "dev_off", "action", "tab_off", "tab_id",
+        "legal", "q")]
 
 
 class SpBreakdown(ctypes.Structure):

@@ -28,7 +28,8 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
-from ._lib import SpBreakdown, SpCostnetBatch, SpNets, SpTableSpec, ShardplanError, check, lib
+from ._lib import (SpBreakdown, SpCostnetBatch, SpNets, SpReinforceBatch, SpTableSpec,
+                   ShardplanError, check, lib)
 
 NUM_BINS = 17
 NUM_FEATURES = 21
@@ -647,6 +648,68 @@ class CostNetTrainer:
         v = np.zeros(self.N_PARAMS)
         st = ctypes.c_int64()
         check(lib().sp_costnet_trainer_get(self._h, _ptr(p), _ptr(m), _ptr(v), ctypes.byref(st)))
+        return p, m, v, st.value
+
+
+class PolicyTrainer:
+    """GPU REINFORCE on the policy network (sp_policy_trainer):
+    reinforce_loss_and_grad + Adam (policy.hpp:203-296) in fp64, parameters
+    resident on the device. Episodes dict: n, row0[n], ntab[n], step_off[n+1],
+    reward[n], dev_off[steps+1], action[steps], tab_off[devices+1], tab_id,
+    legal[devices], q[devices][3]."""
+
+    N_PARAMS = 9345
+    _INT = ("row0", "ntab", "step_off", "dev_off", "action", "tab_off", "tab_id", "legal")
+
+    def __init__(self, params, features, mask=None, lr: float = 5e-4, total_steps: int = 0,
+                 device: int = 0):
+        p = np.ascontiguousarray(params, dtype=np.float64)
+        f = np.ascontiguousarray(features, dtype=np.float64)
+        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.float64)
+        h = ctypes.c_void_p()
+        check(lib().sp_policy_trainer_create(_ptr(p), p.size, _ptr(f), f.shape[0],
+                                             _ptr(m) if m is not None else None, lr,
+                                             total_steps, device, ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().sp_policy_trainer_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 (interpreter shutdown)
+            pass
+
+    def _batch(self, eps):
+        arrs = {k: np.ascontiguousarray(eps[k], dtype=np.int32) for k in self._INT}
+        arrs["reward"] = np.ascontiguousarray(eps["reward"], dtype=np.float64)
+        arrs["q"] = np.ascontiguousarray(eps["q"], dtype=np.float64)
+        sb = SpReinforceBatch(int(eps["n"]), *[arrs[k].ctypes.data for k in (
+            "row0", "ntab", "step_off", "reward", "dev_off", "action", "tab_off", "tab_id",
+            "legal", "q")])
+        return sb, arrs
+
+    def loss_grad(self, eps, w_entropy: float):
+        sb, keep = self._batch(eps)
+        obj = ctypes.c_double()
+        grad = np.zeros(self.N_PARAMS)
+        check(lib().sp_reinforce_loss_grad(self._h, ctypes.byref(sb), w_entropy,
+                                           ctypes.byref(obj), _ptr(grad)))
+        return obj.value, grad
+
+    def step(self, eps, w_entropy: float) -> float:
+        sb, keep = self._batch(eps)
+        obj = ctypes.c_double()
+        check(lib().sp_reinforce_step(self._h, ctypes.byref(sb), w_entropy, ctypes.byref(obj)))
+        return obj.value
+
+    def state(self):
+        p, m, v = (np.zeros(self.N_PARAMS) for _ in range(3))
+        st = ctypes.c_int64()
+        check(lib().sp_policy_trainer_get(self._h, _ptr(p), _ptr(m), _ptr(v), ctypes.byref(st)))
         return p, m, v, st.value
 
 

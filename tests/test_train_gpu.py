@@ -71,3 +71,62 @@ def test_train_steps_match_reference(red):
     assert abs(np.mean(losses) - want_mean) <= 1e-9 * abs(want_mean)
     np.testing.assert_allclose(got, want, rtol=1e-8, atol=1e-12)
     assert not np.allclose(got, params)  # it trained
+
+
+def _episodes(seed, n=6, rows=80):
+    """Random same-shape episodes of several tasks: each step assigns the
+    next table of a random order to a legal device; q and legality random."""
+    from paper_2210_02023_b200.api import PolicyTrainer  # noqa: F401 (import check)
+    rng = np.random.default_rng(seed)
+    feats = rng.normal(size=(rows, 21))
+    eps = {k: [] for k in ("row0", "ntab", "reward", "action", "tab_id", "legal", "q")}
+    step_off, dev_off, tab_off = [0], [0], [0]
+    for e in range(n):
+        M = int(rng.integers(5, 25))
+        D = int(rng.integers(2, 9))
+        row0 = int(rng.integers(0, rows - M))
+        eps["row0"].append(row0)
+        eps["ntab"].append(M)
+        eps["reward"].append(-rng.uniform(5, 20))
+        sets = [[] for _ in range(D)]
+        for t in rng.permutation(M):
+            legal = rng.uniform(size=D) < 0.8
+            if not legal.any():
+                legal[int(rng.integers(D))] = True
+            a = int(rng.choice(np.flatnonzero(legal)))
+            for d in range(D):
+                eps["tab_id"].extend(sets[d])
+                tab_off.append(len(eps["tab_id"]))
+                eps["legal"].append(int(legal[d]))
+                eps["q"].append(rng.uniform(0.0, 2.0, size=3) if sets[d] else np.zeros(3))
+            dev_off.append(len(tab_off) - 1)
+            eps["action"].append(a)
+            sets[a].append(int(t))
+        step_off.append(len(dev_off) - 1)
+    eps.update({"n": n, "step_off": step_off, "dev_off": dev_off, "tab_off": tab_off,
+                "q": np.array(eps["q"]).reshape(-1, 3)})
+    params = rng.normal(scale=0.2, size=9345)
+    return params, feats, eps
+
+
+def test_reinforce_grad_and_updates_match_reference():
+    from paper_2210_02023_b200.api import PolicyTrainer
+    params, feats, eps = _episodes(5)
+    mask = np.ones(21)
+    mask[[0, 9]] = 0.0
+    w = 0.001
+    want_obj, want_grad = ref.reinforce_loss_grad(params, eps, feats, w, mask)
+    tr = PolicyTrainer(params, feats, mask, lr=1e-3, total_steps=10)
+    obj, grad = tr.loss_grad(eps, w)
+    assert abs(obj - want_obj) <= 1e-12 * max(1.0, abs(want_obj))
+    scale = np.abs(want_grad).max()
+    np.testing.assert_allclose(grad, want_grad, rtol=1e-9, atol=1e-12 * scale)
+    # ten reinforce_update steps on the same episodes
+    want_p, want_objs = ref.reinforce_updates(params, eps, feats, w, 10, 1e-3, 10, mask)
+    objs = [tr.step(eps, w) for _ in range(10)]
+    got, _, _, nstep = tr.state()
+    tr.close()
+    assert nstep == 10
+    np.testing.assert_allclose(objs, want_objs, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(got, want_p, rtol=1e-8, atol=1e-12)
+    assert not np.allclose(got, params)
