@@ -2,20 +2,22 @@
 //
 //   K1 tbe_forward_kernel — fused multi-table sum-pooled EmbeddingBag
 //      forward (the reference's fused_kernel stage, oracle.hpp:163-174,
-//      executed for real). Optionally emits the backward's sort keys.
-//   K4 build_keys (when K1 did not emit them) -> CUB stable radix sort ->
-//      sgd_kernel — the backward (oracle.hpp:149 bwd_comp): duplicate rows
-//      are reduced in the sorted (= original) order before one coalesced
-//      row-wise SGD write-back.
+//      executed for real). Optionally emits the backward's sort pairs; with
+//      peer memory its stores land at the receiving ranks (the forward
+//      all-to-all fused into the lookup).
+//   K4 build_keys (when K1 did not emit them) -> CUB stable radix sort per
+//      sort group -> sgd_kernel — the backward (oracle.hpp:149 bwd_comp):
+//      duplicate rows are reduced in the sorted (= original) order and every
+//      unique row gets one L2 vector-reduction update.
 //
-// Both are HBM-bound random row gathers. Each block owns a tile: K1 a run
-// of consecutive bags of one table, K4 a run of sorted positions. The tile's
-// offsets/indices (K1) or keys/bags (K4) are staged in shared memory with
-// coalesced loads, so the only long-latency dependency left per bag/row is
-// the row gather itself. A warp is split into P spans (one bag / one unique
-// row each); a span splits into GB groups of L = dim/4 lanes, each lane
-// moving one 16-byte float4 slice, U rows in flight per group. Partial
-// sums combine with a fixed xor-shuffle tree: bitwise reproducible.
+// Both are HBM-bound random row gathers / updates over fp32 or fp16 tables
+// (16-byte row slices, Slice<T>). K1: a block owns a tile of consecutive bags
+// of one table, its offsets/indices staged in shared memory with coalesced
+// loads; a warp is split into P spans (one bag each), a span into GB groups
+// of L lanes, each lane moving one 16-byte slice with U rows in flight.
+// K4: a block owns a tile of sorted positions of one table; short runs go P
+// per warp round, hot runs are block-cooperative. Partial sums combine in
+// fixed trees: bitwise reproducible.
 #include <cub/cub.cuh>
 
 #include <type_traits>
