@@ -116,6 +116,7 @@ struct VDev {
   int* d_sgd_tiles[2] = {};
   int64_t sgd_tile_cap[2] = {};
   int64_t n_sgd_tiles = 0;
+  int64_t sgd_counts[2] = {};  // generic-dim (run-based) / segmented SGD tiles
   int cur = 0;  // slot of the current batch
   uint32_t* d_keys = nullptr;   // backward sort pairs (written by K1)
   uint32_t* d_bags = nullptr;
@@ -216,6 +217,9 @@ struct sp_ctx {
   int64_t stage_cap = 0;
   cudaEvent_t stage_free[2] = {};    // recorded after the narrows that read a slot
   bool stage_used[2] = {};
+  float* d_carry_f = nullptr;        // segmented SGD cross-tile carries
+  int32_t* d_carry_i = nullptr;
+  int64_t carry_cap = 0;
   int32_t* d_step_flags = nullptr;   // per-step validation flags (sp_run_batches)
   int64_t step_flags_cap = 0;
   // pinned host copies of a batch's layout metadata (SGD tiles, sort group
@@ -282,6 +286,8 @@ struct sp_ctx {
     if (d_stage64) cudaFree(d_stage64);
     if (d_stage64_alt) cudaFree(d_stage64_alt);
     if (d_step_flags) cudaFree(d_step_flags);
+    if (d_carry_f) cudaFree(d_carry_f);
+    if (d_carry_i) cudaFree(d_carry_i);
     for (auto* p : meta_host)
       if (p) cudaFreeHost(p);
     for (auto& e : stage_free)
@@ -511,8 +517,9 @@ void stage_backward(sp_ctx* c, VDev& v, bool sorted = false,
   }
   if (!sorted) stage_sort(c, v, c->stream);
   ProfScope prof(c, kProfSgd);
-  launch_sgd(v.d_meta_canon, v.d_sgd_tiles[v.cur], v.n_sgd_tiles, c->d_kb, c->d_bb, c->bags16,
-             v.d_grad, v.W, c->lr, c->d_w, c->wt, abort_flag, c->stream);
+  launch_sgd(v.d_meta_canon, v.d_sgd_tiles[v.cur], v.sgd_counts, c->d_kb, c->d_bb, c->bags16,
+             v.d_grad, v.W, c->lr, c->d_w, c->wt, c->d_carry_f, c->d_carry_i, abort_flag,
+             c->stream);
 }
 
 // One process per rank (world > 1); the exchange goes through peer memory
@@ -1180,7 +1187,7 @@ static void finish_batch(sp_ctx* c, int slot = 0, bool pipelined = false) {
   std::vector<std::vector<int>> tiles;
   size_t need = 0;
   for (auto& v : c->vdevs) {
-    tiles.push_back(make_sgd_tiles(v.table_nnz));
+    tiles.push_back(make_sgd_tiles(v.table_nnz, v.meta_canon, v.sgd_counts));
     need += tiles.back().size() * sizeof(int) + 16;
   }
   if (c->stage_used[slot]) SP_CUDA(cudaEventSynchronize(c->stage_free[slot]));
@@ -1209,6 +1216,15 @@ static void finish_batch(sp_ctx* c, int slot = 0, bool pipelined = false) {
     }
     const std::vector<int>& tl = tiles[vi];
     v.n_sgd_tiles = static_cast<int64_t>(tl.size()) / kSgdTileInts;
+    const int64_t wide = v.sgd_counts[1];
+    if (wide > c->carry_cap) {  // segmented SGD carries (shared, stream-ordered)
+      SP_CUDA(cudaStreamSynchronize(c->stream));
+      if (c->d_carry_f) cudaFree(c->d_carry_f);
+      if (c->d_carry_i) cudaFree(c->d_carry_i);
+      SP_CUDA(cudaMalloc(&c->d_carry_f, sgd_carry_floats(wide) * sizeof(float)));
+      SP_CUDA(cudaMalloc(&c->d_carry_i, wide * 4 * sizeof(int32_t)));
+      c->carry_cap = wide;
+    }
     if (static_cast<int64_t>(tl.size()) > v.sgd_tile_cap[slot]) {
       SP_CUDA(cudaStreamSynchronize(c->stream));
       SP_CUDA(cudaStreamSynchronize(c->side));

@@ -823,6 +823,275 @@ __global__ void __launch_bounds__(kBlockThreads, SP_SGD_MIN_BLOCKS)
 }
 
 // ---------------------------------------------------------------------------
+// K4 SGD for wide rows (256- and 512-byte rows: fp32 dims 64/128, fp16
+// dims 128/256): a segmented reduction over the sorted positions instead of
+// runs. A row of R 16-byte slices is one lane group (R = 32: the warp; R =
+// 16: a half warp); the tile's positions are cut into one contiguous chunk
+// per group and every group walks its chunk in position order with U
+// gradient rows in flight: all lanes of a group see the same row sequence,
+// so run boundaries are uniform, hot runs need no special path and there is
+// no per-run bookkeeping. A run inside one chunk is applied at its end (one
+// L2 vector reduction per slice); a run crossing chunk boundaries leaves its
+// partial sums in shared memory and is combined in chunk order after the
+// walk; one crossing the tile boundary leaves them in a per-tile carry,
+// combined in tile order by sgd_carry_kernel. Every sum is in position
+// order up to that fixed chunking: deterministic.
+
+constexpr int kCarryF = 256;  // floats per carry row (<= 512-byte rows of fp32 or fp16)
+enum { kNone = 0, kPart = 1, kWhole = 2 };
+
+constexpr int kSegChunksMax = kWarpsPerBlock * 32;  // R = 1: 32 groups per warp
+
+template <class BagT, class T>
+struct SegShared {
+  uint32_t row[kTilePos];
+  BagT bag[kTilePos];
+  alignas(16) float part[512 * Slice<T>::E];  // [C][2][R*E] with C*R = 256
+  int kind[kSegChunksMax][2];
+  uint32_t prow[kSegChunksMax][2];
+};
+
+// One tile of rows of R 16-byte slices (R = 1..32).
+template <int R, class BagT, class T>
+__device__ __forceinline__ void sgd_seg_tile(const TableMeta& m, const SgdTile& tile,
+                                             SegShared<BagT, T>& sh, bool cont_prev,
+                                             bool cont_next, const float* __restrict__ grad,
+                                             int64_t ldg, float lr, T* __restrict__ w,
+                                             float* __restrict__ carry_f,
+                                             int32_t* __restrict__ carry_i, int64_t slot) {
+  constexpr int E = Slice<T>::E;     // fp32 values per slice
+  constexpr int kSegU = 32 / E;      // gradient rows in flight per group
+  constexpr int G = 32 / R;          // groups per warp
+  constexpr int C = kWarpsPerBlock * G;
+  constexpr int W = R * E;           // floats per partial row
+  const int np = tile.np, tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int c = warp * G + lane / R, sub = lane % R;
+  const int cs = static_cast<int>(static_cast<int64_t>(np) * c / C);
+  const int ce = static_cast<int>(static_cast<int64_t>(np) * (c + 1) / C);
+  const float* gcol = grad + m.lcol + E * sub;
+  T* wbase = w + m.woff + E * sub;
+  float* part = sh.part;  // [C][2][W]
+  if (sub == 0) {
+    sh.kind[c][0] = kNone;
+    sh.kind[c][1] = kNone;
+  }
+  if (cs < ce) {
+    uint32_t run = sh.row[cs];
+    // the chunk's first run began earlier (previous chunk or tile)
+    bool head_open = cs > 0 ? sh.row[cs - 1] == run : cont_prev;
+    float acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = 0.f;
+    auto flush = [&](uint32_t row, bool open_before) {
+      if (open_before) {  // the chunk's head partial, combined after the walk
+#pragma unroll
+        for (int e = 0; e < E; ++e) part[(c * 2) * W + sub * E + e] = acc[e];
+        if (sub == 0) {
+          sh.kind[c][0] = kPart;
+          sh.prow[c][0] = row;
+        }
+      } else {
+        float d[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) d[e] = -lr * acc[e];
+        Slice<T>::red_add(wbase + static_cast<int64_t>(row) * m.dim, d);
+      }
+    };
+    for (int k = cs; k < ce; k += kSegU) {
+      float v[kSegU][E];
+#pragma unroll
+      for (int u = 0; u < kSegU; ++u) {
+        if (k + u < ce) {
+          load_grad<E>(gcol + static_cast<int64_t>(sh.bag[k + u]) * ldg, v[u]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e) v[u][e] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kSegU; ++u) {
+        if (k + u >= ce) break;
+        const uint32_t r = sh.row[k + u];
+        if (r != run) {
+          flush(run, head_open);
+          head_open = false;
+          run = r;
+#pragma unroll
+          for (int e = 0; e < E; ++e) acc[e] = 0.f;
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] += v[u][e];
+      }
+    }
+    // the chunk's last run: does it continue past the chunk?
+    const bool tail_open = ce < np ? sh.row[ce] == run : cont_next;
+    if (!tail_open) {
+      flush(run, head_open);
+    } else {
+      const int sl = head_open ? 0 : 1;  // whole chunk in one run : tail partial
+#pragma unroll
+      for (int e = 0; e < E; ++e) part[(c * 2 + sl) * W + sub * E + e] = acc[e];
+      if (sub == 0) {
+        sh.kind[c][sl] = head_open ? kWhole : kPart;
+        sh.prow[c][sl] = run;
+      }
+    }
+  }
+  __syncthreads();
+  // chains across chunks, in chunk order (lanes 0..R-1 of warp 0)
+  if (warp != 0 || lane >= R) return;
+  float acc[E];
+  bool open = false, from_prev = false;
+  uint32_t row = 0;
+  float* gh = carry_f + (slot * 2) * kCarryF;
+  float* gt = gh + kCarryF;
+  int head_kind = kNone, tail_kind = kNone;
+  for (int q = 0; q < C; ++q) {
+    const int kh = sh.kind[q][0];
+    if (kh != kNone) {
+      if (!open) {  // only the tile's first chunk can continue the previous tile
+        open = true;
+        from_prev = true;
+        row = sh.prow[q][0];
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] = 0.f;
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[e] += part[(q * 2) * W + lane * E + e];
+      if (kh == kPart) {  // the chain ends in chunk q
+        if (from_prev) {
+#pragma unroll
+          for (int e = 0; e < E; ++e) gh[lane * E + e] = acc[e];
+          head_kind = kPart;
+        } else {
+          float d[E];
+#pragma unroll
+          for (int e = 0; e < E; ++e) d[e] = -lr * acc[e];
+          Slice<T>::red_add(wbase + static_cast<int64_t>(row) * m.dim, d);
+        }
+        open = false;
+      }
+    }
+    if (sh.kind[q][1] == kPart) {  // a chain starts in chunk q
+      open = true;
+      from_prev = false;
+      row = sh.prow[q][1];
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[e] = part[(q * 2 + 1) * W + lane * E + e];
+    }
+  }
+  if (open) {
+    if (from_prev) {  // the whole tile is one run
+#pragma unroll
+      for (int e = 0; e < E; ++e) gh[lane * E + e] = acc[e];
+      head_kind = kWhole;
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) gt[lane * E + e] = acc[e];
+      tail_kind = kPart;
+    }
+  }
+  if (lane == 0) {
+    int32_t* ci = carry_i + slot * 4;
+    ci[0] = head_kind;
+    ci[1] = tail_kind;
+    ci[2] = static_cast<int32_t>(row);
+  }
+}
+
+template <class BagT, class T>
+__global__ void __launch_bounds__(kBlockThreads)
+    sgd_seg_kernel(const TableMeta* __restrict__ meta, const SgdTile* __restrict__ tiles,
+                   const uint32_t* __restrict__ keys, const BagT* __restrict__ bags,
+                   const float* __restrict__ grad, int64_t ldg, float lr, T* __restrict__ w,
+                   float* __restrict__ carry_f, int32_t* __restrict__ carry_i,
+                   const int32_t* __restrict__ abort_flag) {
+  if (abort_flag != nullptr && *abort_flag != 0) return;
+  __shared__ SegShared<BagT, T> sh;
+  const SgdTile tile = tiles[blockIdx.x];
+  const TableMeta m = meta[tile.t];
+  const int np = tile.np, p0 = tile.p0, tid = threadIdx.x;
+  for (int i = tid; i < np; i += kBlockThreads) {
+    sh.row[i] = __ldg(keys + p0 + i) - m.rowbase;
+    sh.bag[i] = __ldg(bags + p0 + i);
+  }
+  const bool cont_prev = p0 > tile.tstart && __ldg(keys + p0 - 1) == __ldg(keys + p0);
+  const bool cont_next = p0 + np < tile.pend && __ldg(keys + p0 + np) == __ldg(keys + p0 + np - 1);
+  __syncthreads();
+  switch (m.cls) {
+#define SP_SEG_CASE(C)                                                                    \
+  case C:                                                                                 \
+    sgd_seg_tile<(1 << C), BagT, T>(m, tile, sh, cont_prev, cont_next, grad, ldg, lr, w, \
+                                    carry_f, carry_i, blockIdx.x);                        \
+    break;
+    SP_SEG_CASE(0)
+    SP_SEG_CASE(1)
+    SP_SEG_CASE(2)
+    SP_SEG_CASE(3)
+    SP_SEG_CASE(4)
+    SP_SEG_CASE(5)
+#undef SP_SEG_CASE
+    default:
+      break;
+  }
+}
+
+// Runs crossing tiles: tile i's tail + the whole tiles after it + the head
+// of the tile where the run ends, in tile order; one warp per tile.
+template <int R, class T>
+__device__ __forceinline__ void sgd_carry_tile(const TableMeta& m, int i, int n_tiles, int lane,
+                                               float lr, T* __restrict__ w,
+                                               const float* __restrict__ carry_f,
+                                               const int32_t* __restrict__ carry_i) {
+  constexpr int E = Slice<T>::E;
+  if (lane >= R) return;
+  const uint32_t row = static_cast<uint32_t>(carry_i[static_cast<size_t>(i) * 4 + 2]);
+  float acc[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    acc[e] = carry_f[(static_cast<size_t>(i) * 2 + 1) * kCarryF + lane * E + e];
+  for (int j = i + 1; j < n_tiles; ++j) {
+    const int hk = carry_i[static_cast<size_t>(j) * 4];
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] += carry_f[(static_cast<size_t>(j) * 2) * kCarryF + lane * E + e];
+    if (hk != kWhole) break;
+  }
+  float d[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) d[e] = -lr * acc[e];
+  Slice<T>::red_add(w + m.woff + static_cast<int64_t>(row) * m.dim + E * lane, d);
+}
+
+template <class T>
+__global__ void sgd_carry_kernel(const TableMeta* __restrict__ meta,
+                                 const SgdTile* __restrict__ tiles, int n_tiles, float lr,
+                                 T* __restrict__ w, const float* __restrict__ carry_f,
+                                 const int32_t* __restrict__ carry_i,
+                                 const int32_t* __restrict__ abort_flag) {
+  if (abort_flag != nullptr && *abort_flag != 0) return;
+  const int i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n_tiles || carry_i[static_cast<size_t>(i) * 4 + 1] != kPart) return;
+  const TableMeta m = meta[tiles[i].t];
+  switch (m.cls) {
+#define SP_CARRY_CASE(C)                                                      \
+  case C:                                                                     \
+    sgd_carry_tile<(1 << C), T>(m, i, n_tiles, lane, lr, w, carry_f, carry_i); \
+    break;
+    SP_CARRY_CASE(0)
+    SP_CARRY_CASE(1)
+    SP_CARRY_CASE(2)
+    SP_CARRY_CASE(3)
+    SP_CARRY_CASE(4)
+    SP_CARRY_CASE(5)
+#undef SP_CARRY_CASE
+    default:
+      break;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Generator / layout kernels
 
 __device__ __forceinline__ void store_w(float* p, float v) { *p = v; }
@@ -1029,50 +1298,72 @@ size_t exclusive_scan_i32(void* temp, size_t temp_bytes, const int32_t* in,
   return bytes;
 }
 
-std::vector<int> make_sgd_tiles(const std::vector<int64_t>& table_nnz) {
+std::vector<int> make_sgd_tiles(const std::vector<int64_t>& table_nnz,
+                                const std::vector<TableMeta>& canon, int64_t counts[2]) {
+  // tiles of the generic-dim tables (run-based sgd_kernel), then the tiles
+  // of every other table (segmented sgd_seg_kernel), tables in order
   std::vector<int> out;
-  int64_t p = 0;
-  for (size_t t = 0; t < table_nnz.size(); ++t) {
-    const int64_t e = p + table_nnz[t];
-    for (int64_t q = p; q < e; q += kTilePos) {
-      SgdTile tl{};
-      tl.t = static_cast<int32_t>(t);
-      tl.p0 = static_cast<int32_t>(q);
-      tl.np = static_cast<int32_t>(std::min<int64_t>(kTilePos, e - q));
-      tl.tstart = static_cast<int32_t>(p);
-      tl.pend = static_cast<int32_t>(e);
-      const int* raw = reinterpret_cast<const int*>(&tl);
-      out.insert(out.end(), raw, raw + kSgdTileInts);
+  for (int part = 0; part < 2; ++part) {
+    counts[part] = 0;
+    int64_t p = 0;
+    for (size_t t = 0; t < table_nnz.size(); ++t) {
+      const int64_t e = p + table_nnz[t];
+      const int cls = t < canon.size() ? canon[t].cls : -1;
+      if ((cls >= 0 ? 1 : 0) == part)
+        for (int64_t q = p; q < e; q += kTilePos) {
+          SgdTile tl{};
+          tl.t = static_cast<int32_t>(t);
+          tl.p0 = static_cast<int32_t>(q);
+          tl.np = static_cast<int32_t>(std::min<int64_t>(kTilePos, e - q));
+          tl.tstart = static_cast<int32_t>(p);
+          tl.pend = static_cast<int32_t>(e);
+          const int* raw = reinterpret_cast<const int*>(&tl);
+          out.insert(out.end(), raw, raw + kSgdTileInts);
+          ++counts[part];
+        }
+      p = e;
     }
-    p = e;
   }
   return out;
 }
 
-void launch_sgd(const TableMeta* d_meta_canon, const int* d_tiles, int64_t n_tiles,
+void launch_sgd(const TableMeta* d_meta_canon, const int* d_tiles, const int64_t counts[2],
                 const uint32_t* d_keys, const void* d_bags, bool bags16, const float* d_grad,
-                int64_t ldg, float lr, void* d_w, WeightType wt, const int32_t* d_abort,
-                cudaStream_t st) {
-  if (n_tiles <= 0) return;
+                int64_t ldg, float lr, void* d_w, WeightType wt, float* d_carry_f,
+                int32_t* d_carry_i, const int32_t* d_abort, cudaStream_t st) {
   static_assert(sizeof(SgdTile) == kSgdTileInts * sizeof(int), "tile layout");
   const SgdTile* tiles = reinterpret_cast<const SgdTile*>(d_tiles);
-  const unsigned blocks = static_cast<unsigned>(n_tiles);
-  auto go = [&](auto elem) {
+  auto go = [&](auto elem, auto bag) {
     using T = typename decltype(elem)::type;
+    using BagT = typename decltype(bag)::type;
     T* w = static_cast<T*>(d_w);
-    if (bags16)
-      sgd_kernel<uint16_t, T><<<blocks, kBlockThreads, 0, st>>>(
-          d_meta_canon, tiles, d_keys, static_cast<const uint16_t*>(d_bags), d_grad, ldg, lr, w,
-          d_abort);
-    else
-      sgd_kernel<uint32_t, T><<<blocks, kBlockThreads, 0, st>>>(
-          d_meta_canon, tiles, d_keys, static_cast<const uint32_t*>(d_bags), d_grad, ldg, lr, w,
-          d_abort);
+    const BagT* bags = static_cast<const BagT*>(d_bags);
+    if (counts[1] > 0) {
+      sgd_seg_kernel<BagT, T><<<static_cast<unsigned>(counts[1]), kBlockThreads, 0, st>>>(
+          d_meta_canon, tiles + counts[0], d_keys, bags, d_grad, ldg, lr, w, d_carry_f,
+          d_carry_i, d_abort);
+      SP_LAUNCHED();
+      sgd_carry_kernel<T><<<static_cast<unsigned>((counts[1] + 7) / 8), 256, 0, st>>>(
+          d_meta_canon, tiles + counts[0], static_cast<int>(counts[1]), lr, w, d_carry_f,
+          d_carry_i, d_abort);
+      SP_LAUNCHED();
+    }
+    if (counts[0] > 0) {
+      sgd_kernel<BagT, T><<<static_cast<unsigned>(counts[0]), kBlockThreads, 0, st>>>(
+          d_meta_canon, tiles, d_keys, bags, d_grad, ldg, lr, w, d_abort);
+      SP_LAUNCHED();
+    }
   };
-  if (wt == WeightType::kF16) go(TypeTag<__half>{});
-  else go(TypeTag<float>{});
-  SP_LAUNCHED();
+  if (wt == WeightType::kF16) {
+    if (bags16) go(TypeTag<__half>{}, TypeTag<uint16_t>{});
+    else go(TypeTag<__half>{}, TypeTag<uint32_t>{});
+  } else {
+    if (bags16) go(TypeTag<float>{}, TypeTag<uint16_t>{});
+    else go(TypeTag<float>{}, TypeTag<uint32_t>{});
+  }
 }
+
+size_t sgd_carry_floats(int64_t n_wide_tiles) { return static_cast<size_t>(n_wide_tiles) * 2 * kCarryF; }
 
 void launch_init_weights(void* d_w, WeightType wt, int64_t rows, int dim, int32_t gid,
                          uint64_t seed, cudaStream_t st) {

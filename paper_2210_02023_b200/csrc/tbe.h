@@ -110,12 +110,17 @@ size_t sort_pairs(void* temp, size_t temp_bytes, const uint32_t* keys_in,
 // launch runs over per-table tiles (make_sgd_tiles: kSgdTileInts ints each,
 // from the per-table lookup counts in canonical order).
 constexpr int kSgdTileInts = 8;
-std::vector<int> make_sgd_tiles(const std::vector<int64_t>& table_nnz);
+// Tiles of generic-dim tables (run-based SGD), then of all others
+// (segmented SGD with cross-tile carries); counts[2] receives the two sizes.
+std::vector<int> make_sgd_tiles(const std::vector<int64_t>& table_nnz,
+                                const std::vector<TableMeta>& canon, int64_t counts[2]);
+// Carry floats the segmented SGD needs for n_wide_tiles tiles (ints: 4 per tile).
+size_t sgd_carry_floats(int64_t n_wide_tiles);
 // d_abort (may be null): when *d_abort != 0 the launch leaves W untouched.
-void launch_sgd(const TableMeta* d_meta_canon, const int* d_tiles, int64_t n_tiles,
+void launch_sgd(const TableMeta* d_meta_canon, const int* d_tiles, const int64_t counts[2],
                 const uint32_t* d_keys, const void* d_bags, bool bags16, const float* d_grad,
-                int64_t ldg, float lr, void* d_w, WeightType wt, const int32_t* d_abort,
-                cudaStream_t st);
+                int64_t ldg, float lr, void* d_w, WeightType wt, float* d_carry_f,
+                int32_t* d_carry_i, const int32_t* d_abort, cudaStream_t st);
 
 // ---- generator / layout helpers ------------------------------------------
 void launch_init_weights(void* d_w, WeightType wt, int64_t rows, int dim, int32_t gid,
