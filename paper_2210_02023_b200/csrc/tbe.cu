@@ -860,7 +860,10 @@ __device__ __forceinline__ void sgd_seg_tile(const TableMeta& m, const SgdTile& 
                                              float* __restrict__ carry_f,
                                              int32_t* __restrict__ carry_i, int64_t slot) {
   constexpr int E = Slice<T>::E;     // fp32 values per slice
-  constexpr int kSegU = 32 / E;      // gradient rows in flight per group
+#ifndef SP_SEG_ROWS
+#define SP_SEG_ROWS 32
+#endif
+  constexpr int kSegU = SP_SEG_ROWS / E;  // gradient rows in flight per group
   constexpr int G = 32 / R;          // groups per warp
   constexpr int C = kWarpsPerBlock * G;
   constexpr int W = R * E;           // floats per partial row
@@ -1000,8 +1003,11 @@ __device__ __forceinline__ void sgd_seg_tile(const TableMeta& m, const SgdTile& 
   }
 }
 
+#ifndef SP_SEG_MIN_BLOCKS
+#define SP_SEG_MIN_BLOCKS 4  // <= 64 registers; 3 or 5 blocks per SM measured slower
+#endif
 template <class BagT, class T>
-__global__ void __launch_bounds__(kBlockThreads)
+__global__ void __launch_bounds__(kBlockThreads, SP_SEG_MIN_BLOCKS)
     sgd_seg_kernel(const TableMeta* __restrict__ meta, const SgdTile* __restrict__ tiles,
                    const uint32_t* __restrict__ keys, const BagT* __restrict__ bags,
                    const float* __restrict__ grad, int64_t ldg, float lr, T* __restrict__ w,
