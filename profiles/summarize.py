@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def short(name):
-    for k in ("tbe_forward", "sgd_kernel", "build_keys", "Onesweep", "Histogram",
+    for k in ("tbe_forward", "sgd_seg_kernel", "sgd_carry_kernel", "sgd_kernel", "build_keys", "Onesweep", "Histogram",
               "ExclusiveSum", "rollout", "eval_kernel"):
         if k in name:
             return k
@@ -93,7 +93,7 @@ def main():
                 d.get("launch__registers_per_thread", ""),
                 d.get("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", ""),
                 d.get("lts__throughput.avg.pct_of_peak_sustained_elapsed", "")]) + " |")
-            k = {"tbe_forward": "fwd", "sgd_kernel": "sgd"}.get(short(d.get("Kernel Name", "")))
+            k = {"tbe_forward": "fwd", "sgd_kernel": "sgd", "sgd_seg_kernel": "sgd"}.get(short(d.get("Kernel Name", "")))
             if k:
                 traffic[f"cfg3/D1/{k}"] = (
                     to_bytes(d["dram__bytes_read.sum"], u["dram__bytes_read.sum"]) +
