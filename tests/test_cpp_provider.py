@@ -50,15 +50,16 @@ def test_provider_measures_on_gpu():
 
 
 TRAIN_BIN = os.path.join(ROOT, "tests", "cpp", "_bin", "measured_train_test")
+TOOL_BIN = os.path.join(ROOT, "tools", "_bin", "train_measured")
 
 
-def _build_train(exe):
+def _build_train(exe, src=None):
     cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
     cmd = [cxx, "-std=c++20", "-O2", "-DSHARDPLAN_B200_WITH_REFERENCE", "-I", REF,
            "-I", _json_include(),
            "-include", os.path.join(ROOT, "tests", "cpp", "ref_shim.hpp"),
            "-I", os.path.join(ROOT, "include"),
-           os.path.join(ROOT, "tests", "cpp", "measured_train_test.cpp"), "-o", exe,
+           src or os.path.join(ROOT, "tests", "cpp", "measured_train_test.cpp"), "-o", exe,
            os.path.join(LIBDIR, "_shardplan_b200.so"), f"-Wl,-rpath,{LIBDIR}"]
     subprocess.run(cmd, check=True, capture_output=True)
 
