@@ -253,7 +253,9 @@ __device__ __forceinline__ float* out_row(float* out, const RowMap* __restrict__
   return peer->base[j] + (b - j * peer->rows_per_part) * ld;
 }
 
-template <class G, bool kPeer, class T>
+// kStaged: every position of the tile is in s_idx (np <= kIdxCap), so the
+// index fetch has no per-slot bound check against the staging capacity.
+template <class G, bool kPeer, class T, bool kStaged = false>
 __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb,
                                               int p0, int warp, int lane,
                                               const int32_t* s_off,
@@ -286,7 +288,10 @@ __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int kk = k + u * GB;
-        r[u] = kk < end ? (kk < kIdxCap ? s_idx[kk] : __ldg(idx + p0 + kk)) : -1;
+        if (kStaged)
+          r[u] = kk < end ? s_idx[kk] : -1;
+        else
+          r[u] = kk < end ? (kk < kIdxCap ? s_idx[kk] : __ldg(idx + p0 + kk)) : -1;
       }
       float v[U][V][E];
 #pragma unroll
@@ -348,6 +353,9 @@ __device__ __forceinline__ void fwd_tile_warp_generic(
 
 // BagT: the sort payload — uint16_t when the batch fits 16 bits (6-byte
 // pairs through the radix sort instead of 8), else uint32_t.
+#ifndef SP_FWD_STAGED
+#define SP_FWD_STAGED 1
+#endif
 #ifdef SP_FWD_MIN_BLOCKS  // A/B builds; default: ptxas' own choice (32 registers)
 #define SP_FWD_BOUNDS __launch_bounds__(kBlockThreads, SP_FWD_MIN_BLOCKS)
 #else
@@ -389,10 +397,14 @@ __global__ void SP_FWD_BOUNDS
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   switch (m.cls) {
-#define SP_FWD_CASE(C)                                                         \
-  case C:                                                                      \
-    fwd_tile_warp<FwdG<C, T>, kPeer, T>(m, tile.b0, tile.nb, p0, warp, lane, s_off, s_idx, \
-                             idx, w, out, peer, ldo);                          \
+#define SP_FWD_CASE(C)                                                                    \
+  case C:                                                                                 \
+    if (SP_FWD_STAGED && np <= kIdxCap)                                                   \
+      fwd_tile_warp<FwdG<C, T>, kPeer, T, true>(m, tile.b0, tile.nb, p0, warp, lane, s_off, \
+                                                s_idx, idx, w, out, peer, ldo);           \
+    else                                                                                  \
+      fwd_tile_warp<FwdG<C, T>, kPeer, T>(m, tile.b0, tile.nb, p0, warp, lane, s_off,      \
+                                          s_idx, idx, w, out, peer, ldo);                 \
     break;
     SP_FWD_CASE(0)
     SP_FWD_CASE(1)
