@@ -487,6 +487,10 @@ struct HeadFlag {
 #define SP_SGD_LONG 32
 #endif
 constexpr int kTilePos = SP_SGD_TILE;  // <= 2048 (11-bit run starts)
+#ifndef SP_SEG_TILE
+#define SP_SEG_TILE 1024
+#endif
+constexpr int kSegTilePos = SP_SEG_TILE;  // segmented SGD tile (positions)
 constexpr int kPosPerThread = kTilePos / kBlockThreads;
 constexpr int kLongRun = SP_SGD_LONG;  // runs at least this long are block-cooperative
 constexpr int kRunChunk = 16;  // short runs claimed per warp at a time (>= max P)
@@ -856,8 +860,8 @@ constexpr int kSegChunksMax = kWarpsPerBlock * 32;  // R = 1: 32 groups per warp
 
 template <class BagT, class T>
 struct SegShared {
-  uint32_t row[kTilePos];
-  BagT bag[kTilePos];
+  uint32_t row[kSegTilePos];
+  BagT bag[kSegTilePos];
   alignas(16) float part[512 * Slice<T>::E];  // [C][2][R*E] with C*R = 256
   int kind[kSegChunksMax][2];
   uint32_t prow[kSegChunksMax][2];
@@ -1327,12 +1331,13 @@ std::vector<int> make_sgd_tiles(const std::vector<int64_t>& table_nnz,
     for (size_t t = 0; t < table_nnz.size(); ++t) {
       const int64_t e = p + table_nnz[t];
       const int cls = t < canon.size() ? canon[t].cls : -1;
+      const int64_t tp = part == 0 ? kTilePos : kSegTilePos;
       if ((cls >= 0 ? 1 : 0) == part)
-        for (int64_t q = p; q < e; q += kTilePos) {
+        for (int64_t q = p; q < e; q += tp) {
           SgdTile tl{};
           tl.t = static_cast<int32_t>(t);
           tl.p0 = static_cast<int32_t>(q);
-          tl.np = static_cast<int32_t>(std::min<int64_t>(kTilePos, e - q));
+          tl.np = static_cast<int32_t>(std::min<int64_t>(tp, e - q));
           tl.tstart = static_cast<int32_t>(p);
           tl.pend = static_cast<int32_t>(e);
           const int* raw = reinterpret_cast<const int*>(&tl);
