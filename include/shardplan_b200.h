@@ -167,6 +167,17 @@ int sp_ctx_synchronize(sp_ctx* ctx);
  * validate_batch (table.hpp:167-184) plus 0 <= index < hash_size. */
 int sp_upload_batch(sp_ctx* ctx, const int64_t* offsets, int64_t offsets_len,
                     const int64_t* indices, int64_t indices_len);
+/* A LookupBatch file written by the reference's save_lookup_batch
+ * (table.hpp:268-281; "DSLB", u32 version 1, u32 num_tables, u32 batch_size,
+ * u64 + i64 offsets[], u64 + i64 indices[], little-endian) loaded straight
+ * to the device: replaces load_lookup_batch (table.hpp:283-305) followed by
+ * sp_upload_batch. Only this context's tables' index segments are read;
+ * they stream through pinned host slots into device staging. Errors:
+ * SP_ERR_BAD_INPUT for an unreadable / non-DSLB / wrong-version / truncated
+ * file (the reference's messages), SP_ERR_MALFORMED_BATCH for a batch
+ * validate_batch rejects, SP_ERR_SHAPE_MISMATCH when num_tables/batch_size
+ * differ from the context's, then the checks of sp_upload_batch. */
+int sp_upload_batch_file(sp_ctx* ctx, const char* path);
 /* Same batch, generated on the device by the SURVEY §8d generator. */
 int sp_synth_batch(sp_ctx* ctx, uint64_t seed);
 /* The same generator for a whole host LookupBatch of `tables` (run on the
@@ -280,6 +291,16 @@ int sp_ingest_lookup_batch(const int64_t* offsets, int64_t offsets_len,
                            const int32_t* dims, const int64_t* hash_sizes,
                            int32_t bytes_per_param, int32_t cuda_device,
                            sp_table_spec* out_tables);
+
+/* ingest_lookup_batch(load_lookup_batch(path), dims, hash_sizes,
+ * bytes_per_param) (table.hpp:188-232, 283-305) with the file's indices
+ * streamed straight to the device. n_dims = the file's num_tables (else
+ * SP_ERR_BAD_INPUT like the reference); out_tables holds n_dims specs;
+ * num_tables_out / batch_size_out (nullable) receive the file's counts. */
+int sp_ingest_batch_file(const char* path, const int32_t* dims, const int64_t* hash_sizes,
+                         int32_t n_dims, int32_t bytes_per_param, int32_t cuda_device,
+                         sp_table_spec* out_tables, int32_t* num_tables_out,
+                         int32_t* batch_size_out);
 
 /* ------------------------------------------------------------------ */
 /* Batched cost/policy evaluator (costnet.hpp, policy.hpp).             */

@@ -190,6 +190,29 @@ def ingest(offsets, indices, T, B, dims, hash_sizes, bytes_per_param=2):
     return array_to_specs(out)[:T], mean, std
 
 
+def save_lookup_batch(path, offsets, indices, T, B):
+    """save_lookup_batch (table.hpp:268-281)."""
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    indices = np.ascontiguousarray(indices, dtype=np.int64)
+    _check(lib().ref_save_lookup_batch(str(path).encode(), _p(offsets, ctypes.c_int64),
+                                       len(offsets), _p(indices, ctypes.c_int64), len(indices),
+                                       T, B))
+
+
+def load_lookup_batch(path):
+    """load_lookup_batch (table.hpp:283-305) -> (offsets, indices, T, B)."""
+    n_off, n_idx = ctypes.c_int64(0), ctypes.c_int64(0)
+    T, B = ctypes.c_int(0), ctypes.c_int(0)
+    _check(lib().ref_load_lookup_batch(str(path).encode(), None, ctypes.byref(n_off), None,
+                                       ctypes.byref(n_idx), ctypes.byref(T), ctypes.byref(B)))
+    offsets = np.zeros(max(n_off.value, 1), dtype=np.int64)
+    indices = np.zeros(max(n_idx.value, 1), dtype=np.int64)
+    _check(lib().ref_load_lookup_batch(str(path).encode(), _p(offsets, ctypes.c_int64),
+                                       ctypes.byref(n_off), _p(indices, ctypes.c_int64),
+                                       ctypes.byref(n_idx), ctypes.byref(T), ctypes.byref(B)))
+    return offsets[:n_off.value], indices[:n_idx.value], T.value, B.value
+
+
 def evaluate_placement(tables, D, cap, B, placement):
     """CostOracle::evaluate_placement (oracle.hpp:187-240)."""
     arr = specs_to_array(tables)

@@ -160,6 +160,39 @@ int ref_validate_batch(const int64_t* offsets, int64_t offsets_len,
   });
 }
 
+// save_lookup_batch / load_lookup_batch (table.hpp:268-305), the DSLB file.
+int ref_save_lookup_batch(const char* path, const int64_t* offsets, int64_t offsets_len,
+                          const int64_t* indices, int64_t indices_len, int T, int B) {
+  return guarded([&] {
+    LookupBatch b;
+    b.num_tables = T;
+    b.batch_size = B;
+    b.offsets.assign(offsets, offsets + offsets_len);
+    b.indices.assign(indices, indices + indices_len);
+    save_lookup_batch(b, path);
+  });
+}
+
+// Loads `path`; writes the counts, and the arrays when the capacities
+// (*offsets_len / *indices_len on entry) suffice.
+int ref_load_lookup_batch(const char* path, int64_t* offsets, int64_t* offsets_len,
+                          int64_t* indices, int64_t* indices_len, int* T, int* B) {
+  return guarded([&] {
+    const LookupBatch b = load_lookup_batch(path);
+    const bool fits = offsets && indices &&
+                      *offsets_len >= static_cast<int64_t>(b.offsets.size()) &&
+                      *indices_len >= static_cast<int64_t>(b.indices.size());
+    if (fits) {
+      std::copy(b.offsets.begin(), b.offsets.end(), offsets);
+      std::copy(b.indices.begin(), b.indices.end(), indices);
+    }
+    *offsets_len = static_cast<int64_t>(b.offsets.size());
+    *indices_len = static_cast<int64_t>(b.indices.size());
+    *T = b.num_tables;
+    *B = b.batch_size;
+  });
+}
+
 // ---- synth.hpp ----------------------------------------------------------
 
 int ref_synth_pool(int num_tables, const int32_t* dims, const double* weights,

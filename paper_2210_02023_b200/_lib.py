@@ -35,6 +35,7 @@ SIGNATURES = {
     "sp_set_table": (c_i32, [c_vp, c_i32, c_vp]),
     "sp_get_table": (c_i32, [c_vp, c_i32, c_vp]),
     "sp_upload_batch": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_i64]),
+    "sp_upload_batch_file": (c_i32, [c_vp, ctypes.c_char_p]),
     "sp_synth_batch": (c_i32, [c_vp, c_u64]),
     "sp_batch_nnz": (c_i32, [c_vp, P(c_i64)]),
     "sp_synth_lookup_batch": (c_i32, [c_vp, c_i32, c_i32, c_u64, c_i32, c_vp, c_vp, P(c_i64)]),
@@ -77,6 +78,8 @@ SIGNATURES = {
     "sp_host_free": (None, [c_vp]),
     "sp_ingest_lookup_batch": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp,
                                        c_i32, c_i32, c_vp]),
+    "sp_ingest_batch_file": (c_i32, [ctypes.c_char_p, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp,
+                                     P(c_i32), P(c_i32)]),
     "sp_evaluator_create": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_f64, c_i32, P(c_vp)]),
     "sp_evaluator_destroy": (None, [c_vp]),
     "sp_evaluator_order": (c_i32, [c_vp, c_vp]),

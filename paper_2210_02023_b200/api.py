@@ -134,6 +134,69 @@ def validate_batch(b: LookupBatch) -> None:
         raise ShardplanError(3, "last offset != indices length")
 
 
+# Binary lookup-batch file (table.hpp:235-305): "DSLB", u32 version,
+# u32 num_tables, u32 batch_size, u64 offsets_len, i64 offsets[],
+# u64 indices_len, i64 indices[], little-endian.
+BATCH_FILE_VERSION = 1  # kBatchVersion, table.hpp:240
+_DSLB_HEADER = np.dtype([("magic", "S4"), ("version", "<u4"), ("num_tables", "<u4"),
+                         ("batch_size", "<u4"), ("offsets_len", "<u8")])
+
+
+def save_lookup_batch(b: LookupBatch, path: str) -> None:
+    """save_lookup_batch (table.hpp:268-281): validates, then writes the
+    DSLB file byte for byte like the reference."""
+    validate_batch(b)
+    hdr = np.zeros(1, dtype=_DSLB_HEADER)
+    hdr["magic"], hdr["version"] = b"DSLB", BATCH_FILE_VERSION
+    hdr["num_tables"], hdr["batch_size"], hdr["offsets_len"] = (b.num_tables, b.batch_size,
+                                                                len(b.offsets))
+    try:
+        with open(path, "wb") as f:
+            f.write(hdr.tobytes())
+            f.write(b.offsets.astype("<i8", copy=False).tobytes())
+            f.write(np.array([len(b.indices)], dtype="<u8").tobytes())
+            f.write(b.indices.astype("<i8", copy=False).tobytes())
+    except OSError as e:
+        raise ShardplanError(10, f"cannot open {path} for writing") from e
+
+
+def load_lookup_batch(path: str) -> LookupBatch:
+    """load_lookup_batch (table.hpp:283-305) into host memory (the device
+    path is EmbeddingShard.upload_batch_file / ingest_batch_file, which
+    never hold the indices on the host)."""
+    try:
+        raw = np.fromfile(path, dtype=np.uint8)
+    except OSError as e:
+        raise ShardplanError(10, f"cannot open {path}") from e
+    if len(raw) < 4 or raw[:4].tobytes() != b"DSLB":
+        raise ShardplanError(10, f"{path}: not a lookup batch file")
+
+    def u(pos, dt, n=1):
+        size = np.dtype(dt).itemsize * n
+        if pos + size > len(raw):
+            raise ShardplanError(10, "unexpected end of file")
+        return raw[pos:pos + size].view(dt)
+
+    version = int(u(4, "<u4")[0])
+    if version != BATCH_FILE_VERSION:
+        raise ShardplanError(10, f"unsupported batch version {version}")
+    T, B, n_off = int(u(8, "<u4")[0]), int(u(12, "<u4")[0]), int(u(16, "<u8")[0])
+    if n_off > (len(raw) - 24) // 8:
+        raise ShardplanError(10, "unexpected end of file")
+    offsets = u(24, "<i8", n_off).astype(np.int64)
+    pos = 24 + 8 * n_off
+    n_idx = int(u(pos, "<u8")[0])
+    if n_idx > (len(raw) - pos - 8) // 8:
+        raise ShardplanError(10, "unexpected end of file")
+    indices = u(pos + 8, "<i8", n_idx).astype(np.int64)
+    # the reference's int fields
+    T = T - (1 << 32) if T >= 1 << 31 else T
+    B = B - (1 << 32) if B >= 1 << 31 else B
+    b = LookupBatch(indices, offsets, T, B)
+    validate_batch(b)
+    return b
+
+
 def compute_feature_stats(tables: Sequence[TableDesc]):
     """table.hpp:108-131: per-feature (mean, std) of ln(1+x)."""
     if not tables:
@@ -167,6 +230,27 @@ def ingest_lookup_batch(b: LookupBatch, dims: Sequence[int], hash_sizes: Sequenc
                         list(s.dist)) for s in out][:b.num_tables]
     mean, std = compute_feature_stats(tables)
     return tables, mean, std
+
+
+def ingest_batch_file(path: str, dims: Sequence[int], hash_sizes: Sequence[int],
+                      bytes_per_param: int = DEFAULT_BYTES_PER_PARAM, device: int = 0):
+    """ingest_lookup_batch(load_lookup_batch(path), ...) (table.hpp:188-232,
+    283-305) with the file's indices streamed straight to the GPU.
+
+    Returns (tables, feature_mean, feature_std, batch_size)."""
+    dims_a = np.ascontiguousarray(dims, dtype=np.int32)
+    hs_a = np.ascontiguousarray(hash_sizes, dtype=np.int64)
+    if len(dims_a) != len(hs_a):
+        raise ShardplanError(10, "dims/hash_sizes length != num_tables")
+    out = (SpTableSpec * max(len(dims_a), 1))()
+    nt, bs = ctypes.c_int32(), ctypes.c_int32()
+    check(lib().sp_ingest_batch_file(os.fsencode(path), _ptr(dims_a), _ptr(hs_a), len(dims_a),
+                                     bytes_per_param, device, out, ctypes.byref(nt),
+                                     ctypes.byref(bs)))
+    tables = [TableDesc(s.id, s.dim, s.hash_size, s.pooling_factor, s.table_size_gb,
+                        list(s.dist)) for s in out][:nt.value]
+    mean, std = compute_feature_stats(tables)
+    return tables, mean, std, bs.value
 
 
 # ---------------------------------------------------------------------------
@@ -345,6 +429,12 @@ class EmbeddingShard:
             raise ShardplanError(8, "batch shape does not match the task")
         check(lib().sp_upload_batch(self._h, _ptr(b.offsets), len(b.offsets), _ptr(b.indices),
                                     len(b.indices)))
+
+    def upload_batch_file(self, path: str):
+        """load_lookup_batch(path) (table.hpp:283-305) + upload_batch, the
+        indices streamed from the file straight to the device (only this
+        shard's tables are read)."""
+        check(lib().sp_upload_batch_file(self._h, os.fsencode(path)))
 
     def upload_batch_ptr(self, offsets_ptr: int, offsets_len: int, indices_ptr: int,
                          indices_len: int):

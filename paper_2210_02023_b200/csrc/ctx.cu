@@ -25,6 +25,7 @@
 #include "nccl_loader.h"
 #include "synth.cuh"
 #include "bwd.h"
+#include "dslb.h"
 #include "tbe.h"
 
 namespace sp {
@@ -214,6 +215,9 @@ struct sp_ctx {
   size_t temp_bytes = 0;
   int64_t* d_stage64 = nullptr;      // int64 staging of an uploaded LookupBatch
   int64_t* d_stage64_alt = nullptr;  // second slot (sp_run_batches: next step's H2D)
+  int64_t* file_off = nullptr;       // pinned offsets of a DSLB file (sp_upload_batch_file)
+  int64_t file_off_cap = 0;
+  std::unique_ptr<sp::DslbStreamer> file_ring;  // pinned ring: file -> device indices
   int64_t stage_cap = 0;
   cudaEvent_t stage_free[2] = {};    // recorded after the narrows that read a slot
   bool stage_used[2] = {};
@@ -285,6 +289,8 @@ struct sp_ctx {
         if (p) cudaFree(p);
     if (d_stage64) cudaFree(d_stage64);
     if (d_stage64_alt) cudaFree(d_stage64_alt);
+    file_ring.reset();
+    if (file_off) cudaFreeHost(file_off);
     if (d_step_flags) cudaFree(d_step_flags);
     if (d_carry_f) cudaFree(d_carry_f);
     if (d_carry_i) cudaFree(d_carry_i);
@@ -1349,9 +1355,11 @@ cudaEvent_t upload_event(sp_ctx* c, size_t& n_ev) {
 // flag: this step's validation flag; slot: staging buffer 0 or 1 (the copy
 // stream only waits for the narrows of the last step that used the slot, so
 // with two slots a step's H2D overlaps the previous step's compute).
-template <class F>
-void enqueue_upload(sp_ctx* c, const int64_t* offsets, const int64_t* indices, F&& chunk_done,
-                    int32_t* flag = nullptr, int slot = 0) {
+// copy_idx(dst, i0, n, stream) enqueues the H2D of indices [i0, i0 + n) into
+// the device staging slot (from host memory, or streamed from a DSLB file).
+template <class F, class CopyIdx>
+void enqueue_upload_from(sp_ctx* c, const int64_t* offsets, CopyIdx&& copy_idx, F&& chunk_done,
+                         int32_t* flag = nullptr, int slot = 0) {
   const int64_t B = c->B;
   const int64_t kUploadChunk = c->upload_chunk;
   if (flag == nullptr) flag = c->d_flag;
@@ -1382,9 +1390,7 @@ void enqueue_upload(sp_ctx* c, const int64_t* offsets, const int64_t* indices, F
         int64_t* s_idx = s_off + n_off;
         SP_CUDA(cudaMemcpyAsync(s_off, offsets + g0 * B, n_off * sizeof(int64_t),
                                 cudaMemcpyHostToDevice, c->copy_stream));
-        if (n_idx)
-          SP_CUDA(cudaMemcpyAsync(s_idx, indices + i0, n_idx * sizeof(int64_t),
-                                  cudaMemcpyHostToDevice, c->copy_stream));
+        if (n_idx) copy_idx(s_idx, i0, n_idx, c->copy_stream);
         cudaEvent_t e = upload_event(c, n_ev);
         SP_CUDA(cudaEventRecord(e, c->copy_stream));
         SP_CUDA(cudaStreamWaitEvent(c->stream, e, 0));
@@ -1408,6 +1414,18 @@ void enqueue_upload(sp_ctx* c, const int64_t* offsets, const int64_t* indices, F
   c->stage_used[slot] = true;
 }
 
+template <class F>
+void enqueue_upload(sp_ctx* c, const int64_t* offsets, const int64_t* indices, F&& chunk_done,
+                    int32_t* flag = nullptr, int slot = 0) {
+  enqueue_upload_from(
+      c, offsets,
+      [indices](int64_t* dst, int64_t i0, int64_t n, cudaStream_t st) {
+        SP_CUDA(cudaMemcpyAsync(dst, indices + i0, n * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                st));
+      },
+      chunk_done, flag, slot);
+}
+
 void raise_batch_flag(int32_t flag) {
   if (flag & 1) raise(SP_ERR_MALFORMED_BATCH, "offsets decrease inside a table");
   if (flag & 2) raise(SP_ERR_BAD_INPUT, "lookup index outside [0, hash_size)");
@@ -1425,6 +1443,54 @@ int sp_upload_batch(sp_ctx* ctx, const int64_t* offsets, int64_t offsets_len,
     sp_ctx* c = ctx;
     host_validate_and_size(c, offsets, offsets_len, indices_len);
     enqueue_upload(c, offsets, indices, [](VDev&, int, int) {});
+    int32_t flag = 0;
+    SP_CUDA(cudaMemcpyAsync(&flag, c->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    SP_CUDA(cudaStreamSynchronize(c->stream));
+    raise_batch_flag(flag);
+    finish_batch(c);
+  });
+}
+
+// load_lookup_batch (table.hpp:283-305) + sp_upload_batch without a host
+// copy of the indices: the header and offsets are read on the host, each
+// local table run's index segment is streamed file -> pinned ring -> device
+// staging (only this context's tables are read), then narrowed and
+// validated exactly like sp_upload_batch.
+int sp_upload_batch_file(sp_ctx* ctx, const char* path) {
+  return guarded([&] {
+    check_ctx(ctx);
+    sp_ctx* c = ctx;
+    DslbFile f;
+    f.open(path);
+    f.validate_shape();
+    if (static_cast<int>(f.num_tables) != c->M || static_cast<int>(f.batch_size) != c->B)
+      raise(SP_ERR_SHAPE_MISMATCH, "batch shape (" + std::to_string(f.num_tables) + " tables, B=" +
+                                       std::to_string(f.batch_size) +
+                                       ") does not match the context");
+    const int64_t n_off = static_cast<int64_t>(f.offsets_len);
+    if (c->file_off_cap < n_off) {
+      SP_CUDA(cudaStreamSynchronize(c->stream));
+      SP_CUDA(cudaStreamSynchronize(c->copy_stream));
+      if (c->file_off) cudaFreeHost(c->file_off);
+      c->file_off = nullptr;
+      c->file_off_cap = 0;
+      SP_CUDA(cudaMallocHost(&c->file_off, n_off * sizeof(int64_t)));
+      c->file_off_cap = n_off;
+    } else {
+      // the previous upload's offset copies may still read the buffer
+      SP_CUDA(cudaStreamSynchronize(c->copy_stream));
+    }
+    f.read_offsets(c->file_off, 0, n_off);
+    const int64_t indices_len = static_cast<int64_t>(f.indices_len);
+    host_validate_and_size(c, c->file_off, n_off, indices_len);
+    if (!c->file_ring) c->file_ring = std::make_unique<DslbStreamer>();
+    DslbStreamer* ring = c->file_ring.get();
+    enqueue_upload_from(
+        c, c->file_off,
+        [&](int64_t* dst, int64_t i0, int64_t n, cudaStream_t st) {
+          ring->indices_to_device(f, i0, n, dst, st);
+        },
+        [](VDev&, int, int) {});
     int32_t flag = 0;
     SP_CUDA(cudaMemcpyAsync(&flag, c->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
     SP_CUDA(cudaStreamSynchronize(c->stream));

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "common.h"
+#include "dslb.h"
 
 namespace sp {
 namespace {
@@ -81,13 +82,17 @@ int bits_for(uint64_t v) {  // bits to represent v (>= 1)
 
 using namespace sp;
 
-extern "C" int sp_ingest_lookup_batch(const int64_t* offsets, int64_t offsets_len,
-                                      const int64_t* indices, int64_t indices_len,
-                                      int32_t num_tables, int32_t batch_size,
-                                      const int32_t* dims, const int64_t* hash_sizes,
-                                      int32_t bytes_per_param, int32_t cuda_device,
-                                      sp_table_spec* out_tables) {
-  return guarded([&] {
+namespace sp {
+namespace {
+
+// The ingest on device: fill_idx(d_idx, stream) enqueues the batch's
+// indices into the device buffer d_idx (from host memory or a DSLB file).
+template <class FillIdx>
+void ingest_impl(const int64_t* offsets, int64_t offsets_len, FillIdx&& fill_idx,
+                 int64_t indices_len, int32_t num_tables, int32_t batch_size,
+                 const int32_t* dims, const int64_t* hash_sizes, int32_t bytes_per_param,
+                 int32_t cuda_device, sp_table_spec* out_tables) {
+  {
     const int T = num_tables;
     const int64_t B = batch_size;
     // validate_batch (table.hpp:167-184)
@@ -128,7 +133,7 @@ extern "C" int sp_ingest_lookup_batch(const int64_t* offsets, int64_t offsets_le
       int32_t bad = 0;
       if (n > 0) {
         int64_t* d_idx = static_cast<int64_t*>(al(n * 8));
-        SP_CUDA(cudaMemcpyAsync(d_idx, indices, n * 8, cudaMemcpyHostToDevice, st));
+        fill_idx(d_idx, st);
         // index range (the reference counts any int64 value)
         int64_t* d_mm = static_cast<int64_t*>(al(16));
         size_t tb1 = 0, tb2 = 0;
@@ -196,5 +201,66 @@ extern "C" int sp_ingest_lookup_batch(const int64_t* offsets, int64_t offsets_le
       throw;
     }
     cleanup();
+  }
+}
+
+}  // namespace
+}  // namespace sp
+
+extern "C" int sp_ingest_lookup_batch(const int64_t* offsets, int64_t offsets_len,
+                                      const int64_t* indices, int64_t indices_len,
+                                      int32_t num_tables, int32_t batch_size,
+                                      const int32_t* dims, const int64_t* hash_sizes,
+                                      int32_t bytes_per_param, int32_t cuda_device,
+                                      sp_table_spec* out_tables) {
+  return guarded([&] {
+    ingest_impl(
+        offsets, offsets_len,
+        [&](int64_t* d_idx, cudaStream_t st) {
+          SP_CUDA(cudaMemcpyAsync(d_idx, indices, indices_len * 8, cudaMemcpyHostToDevice, st));
+        },
+        indices_len, num_tables, batch_size, dims, hash_sizes, bytes_per_param, cuda_device,
+        out_tables);
+  });
+}
+
+// ingest_lookup_batch(load_lookup_batch(path), dims, hash_sizes, bytes)
+// (table.hpp:188-232, 283-305) with the indices streamed from the file
+// straight into device memory (dslb.h). n_dims must equal the file's
+// num_tables (the reference's "dims/hash_sizes length != num_tables").
+extern "C" int sp_ingest_batch_file(const char* path, const int32_t* dims,
+                                    const int64_t* hash_sizes, int32_t n_dims,
+                                    int32_t bytes_per_param, int32_t cuda_device,
+                                    sp_table_spec* out_tables, int32_t* num_tables_out,
+                                    int32_t* batch_size_out) {
+  return guarded([&] {
+    DslbFile f;
+    f.open(path);
+    f.validate_shape();
+    const int64_t n_off = static_cast<int64_t>(f.offsets_len);
+    std::vector<int64_t> off(static_cast<size_t>(n_off));
+    f.read_offsets(off.data(), 0, n_off);
+    // the rest of validate_batch (table.hpp:176-183); ingest_impl repeats the
+    // O(T) checks and checks monotonicity on the device
+    if (off[0] != 0) raise(SP_ERR_MALFORMED_BATCH, "offsets must start at 0");
+    for (int64_t k = 1; k < n_off; ++k)
+      if (off[k] < off[k - 1])
+        raise(SP_ERR_MALFORMED_BATCH, "offsets decrease at position " + std::to_string(k));
+    if (static_cast<uint64_t>(off.back()) != f.indices_len)
+      raise(SP_ERR_MALFORMED_BATCH, "last offset != indices length");
+    if (n_dims != static_cast<int32_t>(f.num_tables))
+      raise(SP_ERR_BAD_INPUT, "dims/hash_sizes length != num_tables");
+    if (num_tables_out) *num_tables_out = static_cast<int32_t>(f.num_tables);
+    if (batch_size_out) *batch_size_out = static_cast<int32_t>(f.batch_size);
+    DslbStreamer ring;
+    ingest_impl(
+        off.data(), n_off,
+        [&](int64_t* d_idx, cudaStream_t st) {
+          ring.indices_to_device(f, 0, static_cast<int64_t>(f.indices_len), d_idx, st);
+        },
+        static_cast<int64_t>(f.indices_len), static_cast<int32_t>(f.num_tables),
+        static_cast<int32_t>(f.batch_size), dims, hash_sizes, bytes_per_param, cuda_device,
+        out_tables);
+    ring.drain();
   });
 }
