@@ -71,7 +71,10 @@ def main():
     if r.returncode != 0:
         raise SystemExit(f"train_measured failed: {r.stderr[-2000:]}")
     metrics = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
-    models = {"dreamshard_oracle": api.load_checkpoint(os.path.join(DATA, "dreamshard_m50_d4.dshd")),
+    oracle_ckpt = os.path.join(DATA, f"dreamshard_m{args.tables}_d{args.devices}.dshd")
+    if not os.path.exists(oracle_ckpt):
+        oracle_ckpt = os.path.join(DATA, "dreamshard_m50_d4.dshd")
+    models = {"dreamshard_oracle": api.load_checkpoint(oracle_ckpt),
               "dreamshard_measured": api.load_checkpoint(ckpt)}
     results = {}
     for cfg, D in (("cfg2", 4), ("cfg3", 4), ("cfg3", 8)):
@@ -85,10 +88,13 @@ def main():
             row[how] = measure(task, api.expert_placement(task, how))
         results[f"{cfg}_d{D}"] = row
     out = {"train_seconds": round(train_s, 1), "iterations": args.iterations,
+           "train_tables": args.tables, "train_devices": args.devices,
+           "oracle_checkpoint": os.path.basename(oracle_ckpt),
            "train_metrics": metrics, "max_device_compute_ms": results,
            "note": "placements measured on one B200 with every device emulated: max over "
                    "devices of the measured fwd + bwd compute (exchange excluded), median of 5"}
-    with open(os.path.join(args.out, "measured_dreamshard.json"), "w") as f:
+    name = f"measured_dreamshard_m{args.tables}_d{args.devices}.json"
+    with open(os.path.join(args.out, name), "w") as f:
         json.dump(out, f, indent=1)
     print(json.dumps(out))
 
