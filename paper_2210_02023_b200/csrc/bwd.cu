@@ -22,6 +22,8 @@
 // SGD needs no run-boundary bookkeeping across blocks.
 #include <cub/cub.cuh>
 
+#include <atomic>
+
 #include "bwd.h"
 #include "common.h"
 #include "tbe.h"
@@ -512,13 +514,17 @@ bool bucket_plan(const std::vector<TableMeta>& canon, const std::vector<int64_t>
 }
 
 void set_bwd_attributes() {
-  static bool done = false;  // once per process (same device properties)
-  if (done) return;
+  // function attributes are per device: once per device of this process
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  SP_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (done.load() & bit) return;
   SP_CUDA(cudaFuncSetAttribute(bwd_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(sizeof(ScatterShared))));
   SP_CUDA(cudaFuncSetAttribute(bwd_bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(sizeof(BucketShared))));
-  done = true;
+  done.fetch_or(bit);
 }
 
 void launch_bwd_partition(const BucketMeta* d_bm, int n_tables, int n_tiles, int64_t n_cnt,
