@@ -215,6 +215,10 @@ struct sp_ctx {
   size_t temp_bytes = 0;
   int64_t* d_stage64 = nullptr;      // int64 staging of an uploaded LookupBatch
   int64_t* d_stage64_alt = nullptr;  // second slot (sp_run_batches: next step's H2D)
+  std::vector<cudaStream_t> sort_st;   // SP_SORT_STREAMS - 1 extra sort streams
+  std::vector<void*> sort_temp;        // their CUB scratch (temp_bytes each)
+  std::vector<cudaEvent_t> ev_sjoin;
+  cudaEvent_t ev_sfork = nullptr;
   int64_t* file_off = nullptr;       // pinned offsets of a DSLB file (sp_upload_batch_file)
   int64_t file_off_cap = 0;
   std::unique_ptr<sp::DslbStreamer> file_ring;  // pinned ring: file -> device indices
@@ -290,6 +294,12 @@ struct sp_ctx {
     if (d_stage64) cudaFree(d_stage64);
     if (d_stage64_alt) cudaFree(d_stage64_alt);
     file_ring.reset();
+    for (auto& st2 : sort_st) {
+      cudaStreamSynchronize(st2);
+      cudaStreamDestroy(st2);
+    }
+    for (auto& e : ev_sjoin) cudaEventDestroy(e);
+    if (ev_sfork) cudaEventDestroy(ev_sfork);
     if (file_off) cudaFreeHost(file_off);
     if (d_step_flags) cudaFree(d_step_flags);
     if (d_carry_f) cudaFree(d_carry_f);
@@ -347,6 +357,7 @@ void ensure_sort_capacity(sp_ctx* c, int64_t n) {
                                  c->stream);
   c->temp_bytes = std::max({t1, t2, static_cast<size_t>(256)});
   c->d_temp = dalloc<uint8_t>(c->temp_bytes, c->sort_owned, dummy);
+  for (auto& t : c->sort_temp) t = dalloc<uint8_t>(c->temp_bytes, c->sort_owned, dummy);
   // bucketed backward: (row, bag) pairs in bucket order + oversize scratch
   c->d_prow = dalloc<int32_t>(cap, c->sort_owned, dummy);
   c->d_pbag = dalloc<int32_t>(cap, c->sort_owned, dummy);
@@ -459,10 +470,11 @@ void stage_forward(sp_ctx* c, VDev& v) {
 }
 
 // (keys) -> stable radix sort; leaves sorted keys in d_kb, bags in d_bb.
-void sort_pairs_of(sp_ctx* c, VDev& v, const SortGroup& g, cudaStream_t st) {
+void sort_pairs_of(sp_ctx* c, VDev& v, const SortGroup& g, cudaStream_t st,
+                   void* temp = nullptr) {
   if (g.p1 == g.p0) return;
   const size_t bb = c->bags16 ? 2 : 4;
-  sort_pairs(c->d_temp, c->temp_bytes, v.d_keys + g.p0, c->d_kb + g.p0,
+  sort_pairs(temp ? temp : c->d_temp, c->temp_bytes, v.d_keys + g.p0, c->d_kb + g.p0,
              reinterpret_cast<const char*>(v.d_bags) + g.p0 * bb,
              reinterpret_cast<char*>(c->d_bb) + g.p0 * bb, c->bags16, g.p1 - g.p0, g.end_bit,
              st);
@@ -478,7 +490,24 @@ void stage_sort(sp_ctx* c, VDev& v, cudaStream_t st, bool rebuild = false) {
     v.keys_valid = true;
   }
   ProfScope prof(c, kProfSort, st);
-  for (const SortGroup& g : v.groups) sort_pairs_of(c, v, g, st);
+  const int S = static_cast<int>(c->sort_st.size()) + 1;
+  if (S == 1 || v.groups.size() < 2) {
+    for (const SortGroup& g : v.groups) sort_pairs_of(c, v, g, st);
+    return;
+  }
+  // SP_SORT_STREAMS > 1: groups round-robin over st and the extra sort
+  // streams (each with its own CUB scratch), joined back into st
+  SP_CUDA(cudaEventRecord(c->ev_sfork, st));
+  for (int k = 1; k < S; ++k) SP_CUDA(cudaStreamWaitEvent(c->sort_st[k - 1], c->ev_sfork, 0));
+  for (size_t gi = 0; gi < v.groups.size(); ++gi) {
+    const int k = static_cast<int>(gi % S);
+    if (k == 0) sort_pairs_of(c, v, v.groups[gi], st);
+    else sort_pairs_of(c, v, v.groups[gi], c->sort_st[k - 1], c->sort_temp[k - 1]);
+  }
+  for (int k = 1; k < S; ++k) {
+    SP_CUDA(cudaEventRecord(c->ev_sjoin[k - 1], c->sort_st[k - 1]));
+    SP_CUDA(cudaStreamWaitEvent(st, c->ev_sjoin[k - 1], 0));
+  }
 }
 
 // Keys (from the CSR) and the stable sort of one sort group's lookups.
@@ -827,6 +856,21 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
       int lo = 0, hi = 0;
       SP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
       SP_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi));
+      const char* ss = std::getenv("SP_SORT_STREAMS");
+      // SP_SORT_STREAMS (default 4): sort groups run concurrently; CUB's
+      // onesweep passes are look-back latency-bound at ~22 warps/SM, so
+      // independent groups overlap (cfg3 isolated sort 1.10 -> 0.97 ms)
+      const int extra = std::max(0, std::min(7, (ss ? std::atoi(ss) : 4) - 1));
+      for (int k = 0; k < extra; ++k) {
+        cudaStream_t s2;
+        cudaEvent_t e2;
+        SP_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, hi));
+        SP_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+        c->sort_st.push_back(s2);
+        c->ev_sjoin.push_back(e2);
+        c->sort_temp.push_back(nullptr);
+      }
+      if (extra > 0) SP_CUDA(cudaEventCreateWithFlags(&c->ev_sfork, cudaEventDisableTiming));
     }
     SP_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     SP_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
@@ -1105,7 +1149,8 @@ int sp_ctx_device_bytes(sp_ctx* ctx, uint64_t* bytes) {
   return guarded([&] {
     check_ctx(ctx);
     uint64_t b = ctx->dev_bytes;
-    b += ctx->sort_cap * 4 * 3 + ctx->temp_bytes + ctx->stage_cap * 8;
+    b += ctx->sort_cap * 4 * 3 + ctx->temp_bytes * (1 + ctx->sort_temp.size()) +
+         ctx->stage_cap * 8;
     for (auto& v : ctx->vdevs) b += v.idx_cap * 12;
     *bytes = b;
   });
