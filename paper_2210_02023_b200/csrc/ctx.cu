@@ -482,7 +482,27 @@ void sort_pairs_of(sp_ctx* c, VDev& v, const SortGroup& g, cudaStream_t st,
 
 // rebuild: derive the keys from the CSR even if K1 emitted them (the
 // overlapped sort does not wait for K1).
+void sort_group(sp_ctx* c, VDev& v, int gi, cudaStream_t st, void* temp = nullptr);
+
 void stage_sort(sp_ctx* c, VDev& v, cudaStream_t st, bool rebuild = false) {
+  const int S = static_cast<int>(c->sort_st.size()) + 1;
+  if (S > 1 && v.groups.size() > 1 && (!v.keys_valid || rebuild) && !c->profiling) {
+    // each group's key build and sort on its own stream: group g's sort
+    // starts as soon as its own keys exist
+    SP_CUDA(cudaEventRecord(c->ev_sfork, st));
+    for (int k = 1; k < S; ++k) SP_CUDA(cudaStreamWaitEvent(c->sort_st[k - 1], c->ev_sfork, 0));
+    for (size_t gi = 0; gi < v.groups.size(); ++gi) {
+      const int k = static_cast<int>(gi % S);
+      if (k == 0) sort_group(c, v, static_cast<int>(gi), st);
+      else sort_group(c, v, static_cast<int>(gi), c->sort_st[k - 1], c->sort_temp[k - 1]);
+    }
+    for (int k = 1; k < S; ++k) {
+      SP_CUDA(cudaEventRecord(c->ev_sjoin[k - 1], c->sort_st[k - 1]));
+      SP_CUDA(cudaStreamWaitEvent(st, c->ev_sjoin[k - 1], 0));
+    }
+    v.keys_valid = true;
+    return;
+  }
   if (!v.keys_valid || rebuild) {
     ProfScope prof(c, kProfKeys, st);
     launch_build_keys(v.d_meta_canon, static_cast<int>(v.tables.size()), c->B, v.d_off,
@@ -490,7 +510,6 @@ void stage_sort(sp_ctx* c, VDev& v, cudaStream_t st, bool rebuild = false) {
     v.keys_valid = true;
   }
   ProfScope prof(c, kProfSort, st);
-  const int S = static_cast<int>(c->sort_st.size()) + 1;
   if (S == 1 || v.groups.size() < 2) {
     for (const SortGroup& g : v.groups) sort_pairs_of(c, v, g, st);
     return;
@@ -511,7 +530,7 @@ void stage_sort(sp_ctx* c, VDev& v, cudaStream_t st, bool rebuild = false) {
 }
 
 // Keys (from the CSR) and the stable sort of one sort group's lookups.
-void sort_group(sp_ctx* c, VDev& v, int gi, cudaStream_t st) {
+void sort_group(sp_ctx* c, VDev& v, int gi, cudaStream_t st, void* temp) {
   const SortGroup& g = v.groups[gi];
   {
     ProfScope prof(c, kProfKeys, st);
@@ -519,7 +538,7 @@ void sort_group(sp_ctx* c, VDev& v, int gi, cudaStream_t st) {
                       v.d_bags, c->bags16, st);
   }
   ProfScope prof(c, kProfSort, st);
-  sort_pairs_of(c, v, g, st);
+  sort_pairs_of(c, v, g, st, temp);
 }
 
 // Bucketed backward (bwd.cu): partition pairs into row buckets, then one
