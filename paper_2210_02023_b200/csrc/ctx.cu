@@ -62,7 +62,7 @@ constexpr double kSortPassUsPerM = 9.0;   // one 8-bit pass over 1M lookups (us)
 
 // Returns the first local table of every group after the first, then T.
 std::vector<int> plan_sort_groups(const sp_table_spec* tables, const std::vector<int>& ids,
-                                  int batch) {
+                                  int batch, int min_groups = 1) {
   const int T = static_cast<int>(ids.size());
   uint64_t cap = uint64_t(1) << 32;  // 32-bit keys
   if (const char* f = std::getenv("SP_SORT_GROUP_ROWS"))  // tests: force many groups
@@ -90,6 +90,39 @@ std::vector<int> plan_sort_groups(const sp_table_spec* tables, const std::vector
   std::vector<int> ends;
   for (int j = T; j > 0; j = from[j]) ends.push_back(j);
   std::reverse(ends.begin(), ends.end());
+  // The groups sort concurrently (SP_SORT_STREAMS): split the heaviest
+  // multi-table group at its lookup midpoint until there are min_groups.
+  // Splitting never widens a key, so no pass is added.
+  auto nnz_of = [&](int a, int b) {
+    double n = 0.0;
+    for (int i = a; i < b; ++i) n += std::max(0.0, tables[ids[i]].pooling_factor) * batch;
+    return n;
+  };
+  while (static_cast<int>(ends.size()) < min_groups) {
+    int best_g = -1;
+    double best_n = 0.0;
+    for (size_t g = 0; g < ends.size(); ++g) {
+      const int a = g == 0 ? 0 : ends[g - 1], b = ends[g];
+      const double n = nnz_of(a, b);
+      if (b - a >= 2 && n > best_n) {
+        best_n = n;
+        best_g = static_cast<int>(g);
+      }
+    }
+    if (best_g < 0) break;
+    const int a = best_g == 0 ? 0 : ends[best_g - 1], b = ends[best_g];
+    int cut = a + 1;
+    double acc = 0.0, best_gap = 1e300;
+    for (int i = a + 1; i < b; ++i) {
+      acc += nnz_of(i - 1, i);
+      const double gap = std::abs(2.0 * acc - best_n);
+      if (gap < best_gap) {
+        best_gap = gap;
+        cut = i;
+      }
+    }
+    ends.insert(ends.begin() + best_g, cut);
+  }
   return ends;
 }
 struct SortGroup {
@@ -963,7 +996,8 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
       for (int i = 0; i < num_tables; ++i)
         if (placement[i] == d) v.tables.push_back(i);
       const int T = static_cast<int>(v.tables.size());
-      const std::vector<int> group_end = plan_sort_groups(tables, v.tables, batch_size);
+      const std::vector<int> group_end =
+          plan_sort_groups(tables, v.tables, batch_size, static_cast<int>(c->sort_st.size()) + 1);
       size_t next_group = 0;
       int64_t lcol = 0;
       uint64_t rb = 0;     // row base inside the current sort group
