@@ -1058,10 +1058,8 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
         return ta.pooling_factor * ta.dim > tb.pooling_factor * tb.dim;
       });
       {
-        static const int mode = [] {
-          const char* e = std::getenv("SP_FWD_ORDER");
-          return e ? std::atoi(e) : 2;
-        }();
+        const char* fo = std::getenv("SP_FWD_ORDER");  // read per context
+        const int mode = fo ? std::atoi(fo) : 2;
         auto interleave = [&](std::vector<int> o) {  // o[0], o[n-1], o[1], o[n-2], ...
           std::vector<int> r;
           for (size_t i = 0, j = o.size(); i < j;) {
