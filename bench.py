@@ -98,6 +98,41 @@ def bench_placements(args, device: int):
     return out
 
 
+def bench_ranks(config: str, D: int, device: int, placement=None):
+    """Every rank of a D-GPU placement measured alone on this GPU as a
+    one-rank context (sp_run_local): K1 with the key build + sort overlapped,
+    then the SGD on the resident gradient — each rank's compute per
+    iteration as it runs on its own B200, without the NVLink exchange.
+    Median of 5 after 2 warm-ups."""
+    import torch
+    from paper_2210_02023_b200 import api
+    task = load_task(config, D)
+    p = make_placement(task, "dreamshard", device) if placement is None else placement
+    ranks = []
+    for r in range(D):
+        sh = api.EmbeddingShard(task, p, lr=0.01, rank=r, world_size=D, nccl_id=None,
+                                device=device)
+        sh.init_tables(SEED)
+        sh.synth_batch(SEED)
+        sh.synth_grad(SEED)
+        for _ in range(2):
+            sh.run_local()
+        runs = sorted((sh.run_local() for _ in range(5)), key=lambda x: x[0] + x[1])
+        f, b = runs[2]
+        ranks.append({"rank": r, "tables": len(sh.local_tables()), "lookups": int(sh.nnz),
+                      "fwd_ms": round(f, 4), "bwd_ms": round(b, 4),
+                      "compute_ms": round(f + b, 4)})
+        sh.close()
+        torch.cuda.synchronize()
+    return {"placement": "dreamshard", "ranks": ranks,
+            "max_fwd_ms": max(x["fwd_ms"] for x in ranks),
+            "max_bwd_ms": max(x["bwd_ms"] for x in ranks),
+            "max_compute_ms": max(x["compute_ms"] for x in ranks),
+            "note": "each rank's shard alone on this B200 (sp_run_local: the rank's K1 with "
+                    "its sort overlapped, then its SGD; exchange excluded); the metric's "
+                    "compute part is max fwd + max bwd over ranks"}
+
+
 def bench_cfg4(args, device: int):
     """BASELINE cfg4 (200 tables of 1e7 rows, 448 GB fp32, 64 GB cap per GPU) under
     the DreamShard placement: each of the 8 ranks' shards (~56 GB) measured in
@@ -561,10 +596,12 @@ def run_ours(args, world, rank, local):
     fp16 = None
     if world == 1 and not args.no_fp16:
         fp16 = bench_fp16(args, task, placement, local)
-    placements = cfg4 = None
+    placements = cfg4 = cfg3_d8 = None
     if world == 1 and not args.no_studies:
         placements = bench_placements(args, local)
         cfg4 = bench_cfg4(args, local)
+        cfg4["overlapped"] = bench_ranks("cfg4", 8, local)
+        cfg3_d8 = bench_ranks("cfg3", 8, local)
 
     # K6/K7 evaluator throughput (SURVEY cfg5 shape): 4096 candidate
     # placements of this task at D = 8, scored and rolled out on this GPU
@@ -611,6 +648,7 @@ def run_ours(args, world, rank, local):
             "fp16_tables": fp16,
             "placement_study": placements,
             "cfg4_per_rank": cfg4,
+            "cfg3_d8_per_rank": cfg3_d8,
             "evaluator": evaluator,
         }
         print(json.dumps(line), flush=True)

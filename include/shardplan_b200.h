@@ -233,6 +233,12 @@ int sp_get_sorted(sp_ctx* ctx, int32_t dev, uint32_t* keys, uint32_t* bags,
  * (oracle.hpp:206-227). Synchronizes the stream. In NCCL mode the per-device
  * arrays hold every rank's numbers (gathered), identical on all ranks. */
 int sp_run_iteration(sp_ctx* ctx, sp_breakdown* out);
+/* This context's compute of one iteration without the exchanges: ms[0] =
+ * the forward stage (K1 with the backward's key build and sort overlapped,
+ * as in sp_run_iteration), ms[1] = the backward stage (SGD on the resident
+ * gradient). Measures one rank of a multi-GPU placement on its own (no NCCL
+ * id or peers needed) — the compute part of that rank's CostBreakdown. */
+int sp_run_local(sp_ctx* ctx, double ms[2]);
 /* sp_upload_batch + sp_run_iteration in one call, pipelined: the H2D of the
  * host LookupBatch overlaps the forward of the tables already on the device
  * (and, with one device per context, their backward sort). The device-side

@@ -51,6 +51,7 @@ SIGNATURES = {
     "sp_get_local_pooled": (c_i32, [c_vp, c_i32, c_vp]),
     "sp_get_sorted": (c_i32, [c_vp, c_i32, c_vp, c_vp, P(c_i64), c_vp, P(c_i64)]),
     "sp_run_iteration": (c_i32, [c_vp, c_vp]),
+    "sp_run_local": (c_i32, [c_vp, c_vp]),
     "sp_run_batch": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "sp_run_batches": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "sp_enqueue_iteration": (c_i32, [c_vp]),

@@ -505,6 +505,13 @@ class EmbeddingShard:
         return CostBreakdown(list(f), list(b), list(c), bd.fwd_comm_stage_ms,
                              bd.bwd_comm_stage_ms, bd.overall_ms)
 
+    def run_local(self):
+        """This shard's compute of one iteration, exchanges left out:
+        (forward-stage ms, backward-stage ms) (sp_run_local)."""
+        ms = np.zeros(2)
+        check(lib().sp_run_local(self._h, _ptr(ms)))
+        return float(ms[0]), float(ms[1])
+
     def run_batch(self, b: LookupBatch) -> CostBreakdown:
         """upload_batch + run_iteration in one pipelined call (sp_run_batch):
         the H2D of the host LookupBatch overlaps the forward of the tables

@@ -1954,6 +1954,32 @@ void collect_breakdown(sp_ctx* c, sp_breakdown* out) {
 
 extern "C" {
 
+// This context's compute of one iteration with the exchanges left out: the
+// forward stage (K1, with the backward's key build and sort overlapped on
+// the side streams exactly as in sp_run_iteration) and the backward stage
+// (join + SGD on the resident gradient). One rank of a multi-GPU placement
+// can be measured alone this way (no NCCL id or peers needed).
+int sp_run_local(sp_ctx* ctx, double ms[2]) {
+  return guarded([&] {
+    check_ctx(ctx);
+    require_batch(ctx);
+    if (!ms) raise(SP_ERR_BAD_INPUT, "null output");
+    sp_ctx* c = ctx;
+    cudaStream_t st = c->stream;
+    VDev& v0 = c->vdevs[0];
+    const bool ov = overlap_active(c);
+    SP_CUDA(cudaEventRecord(v0.ev[0], st));
+    forward_stage(c, ov);
+    SP_CUDA(cudaEventRecord(v0.ev[1], st));
+    if (ov) join_sort(c);
+    for (auto& v : c->vdevs) stage_backward(c, v, ov);
+    SP_CUDA(cudaEventRecord(v0.ev[7], st));
+    SP_CUDA(cudaStreamSynchronize(st));
+    ms[0] = elapsed(v0.ev[0], v0.ev[1]);
+    ms[1] = elapsed(v0.ev[1], v0.ev[7]);
+  });
+}
+
 int sp_run_iteration(sp_ctx* ctx, sp_breakdown* out) {
   return guarded([&] {
     check_ctx(ctx);

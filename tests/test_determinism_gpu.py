@@ -54,3 +54,27 @@ def test_schedules_are_bit_identical(monkeypatch, D):
                 {"SP_SORT_GROUP_ROWS": "3000", "SP_SORT_STREAMS": "4"},
                 {"SP_SORT_GROUP_ROWS": "3000", "SP_SORT_STREAMS": "1"}):
         _same(ref, _run(monkeypatch, env, D))
+
+
+def test_run_local_equals_stage_calls(monkeypatch):
+    """sp_run_local (overlapped forward stage + SGD, no exchange) updates the
+    tables exactly like forward() + backward_sgd() on a rank context of a
+    multi-GPU placement, and times both stages."""
+    task, placement = random_task(77, DIMS, 2, B, rows_range=(50, 5000))
+    off, idx = orc.synth_batch(as_dicts(task.tables), B, seed=5)
+    out = []
+    for local in (True, False):
+        sh = EmbeddingShard(task, placement, lr=0.03, rank=1, world_size=2, nccl_id=None)
+        sh.init_tables(4)
+        sh.upload_batch(LookupBatch(idx, off, len(DIMS), B))
+        sh.synth_grad(6)
+        if local:
+            f, b = sh.run_local()
+            assert f > 0 and b > 0
+        else:
+            sh.forward()
+            sh.backward_sgd()
+        out.append([sh.get_table(t) for t in sh.local_tables()])
+        sh.close()
+    for x, y in zip(*out):
+        np.testing.assert_array_equal(x, y)
