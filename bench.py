@@ -428,10 +428,39 @@ def bench_evaluator(args, device: int, n: int = 4096):
         out[name] = round((time.perf_counter() - t0) * 1e3, 3)
         if name != "eval_batch_ms":
             out[name.replace("_ms", "_refined")] = int(r[3])
-    out["note"] = ("host wall time per call incl. H2D/D2H; reference CPU: infer (one greedy "
-                   "rollout) 65-91 ms at M=100, EstimatedCostProvider::overall 10-16 us per "
-                   "placement (SURVEY §6)")
+    out["note"] = ("host wall time per call incl. H2D/D2H; the reference's own CPU code for "
+                   "the same calls, timed on this host: reference_cpu")
     ev.close()
+    return out
+
+
+def bench_reference_evaluator(n_eval: int = 1024, n_sampled: int = 8):
+    """The reference's own CPU code for the evaluator's calls, timed on this
+    box's host (oracle/_ref = the unmodified reference, compiled): infer
+    (harness.hpp:332), EstimatedCostProvider::overall (costnet.hpp:454-515)
+    per placement, and sampled rollouts — cfg3 tables, D = 8, the same
+    checkpoint as the GPU evaluator. One thread, like the reference."""
+    from oracle import ref
+    with open(os.path.join(DATA, "pools.json")) as f:
+        pool = json.load(f)["cfg3"]
+    tables = pool["tables"]
+    cap, B = float(pool["mem_cap_gb"]), int(pool["batch_size"])
+    M = len(tables)
+    out = {"kind": "reference", "threads": 1, "tables": M, "devices": 8}
+    t0 = time.perf_counter()
+    ref.infer(CKPT, tables, 8, cap, B)
+    out["infer_ms"] = round((time.perf_counter() - t0) * 1e3, 2)
+    placements = np.random.default_rng(0).integers(0, 8, size=(n_eval, M)).astype(np.int32)
+    t0 = time.perf_counter()
+    ref.costnet_overall(CKPT, tables, 8, placements)
+    out["overall_us_per_placement"] = round((time.perf_counter() - t0) * 1e6 / n_eval, 2)
+    t0 = time.perf_counter()
+    ref.sampled_rollouts(CKPT, tables, 8, cap, B, 2210, n_sampled)
+    out["sampled_rollout_ms"] = round((time.perf_counter() - t0) * 1e3 / n_sampled, 2)
+    out["note"] = ("4096 candidates on the host at these rates: eval_batch "
+                   f"{out['overall_us_per_placement'] * 4096 / 1e3:.0f} ms, greedy rollouts "
+                   f"{out['infer_ms'] * 4096 / 1e3:.0f} s, sampled rollouts "
+                   f"{out['sampled_rollout_ms'] * 4096 / 1e3:.0f} s (single-threaded)")
     return out
 
 
@@ -609,6 +638,9 @@ def run_ours(args, world, rank, local):
     if rank == 0 and not args.no_evaluator:
         evaluator = bench_evaluator(args, local)
         evaluator["sweep"] = bench_evaluator_sweep(local)
+        if world == 1 and not args.no_cpu and os.path.exists(os.path.join(
+                ROOT, "oracle", "_ref", "libshardplan_ref.so")):
+            evaluator["reference_cpu"] = bench_reference_evaluator()
 
     if rank == 0:
         line = {
