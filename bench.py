@@ -590,6 +590,18 @@ def run_ours(args, world, rank, local):
     e2e_ms = allreduce_max(e2e_ms, world)
     del keep
 
+    # (before the multi-threaded CPU baseline, whose threads would share the
+    # host with the evaluator's host-side work)
+    # K6/K7 evaluator throughput (SURVEY cfg5 shape): 4096 candidate
+    # placements of this task at D = 8, scored and rolled out on this GPU
+    evaluator = None
+    if rank == 0 and not args.no_evaluator:
+        evaluator = bench_evaluator(args, local)
+        evaluator["sweep"] = bench_evaluator_sweep(local)
+        if world == 1 and not args.no_cpu and os.path.exists(os.path.join(
+                ROOT, "oracle", "_ref", "libshardplan_ref.so")):
+            evaluator["reference_cpu"] = bench_reference_evaluator()
+
     # CPU baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -632,15 +644,6 @@ def run_ours(args, world, rank, local):
         cfg4["overlapped"] = bench_ranks("cfg4", 8, local)
         cfg3_d8 = bench_ranks("cfg3", 8, local)
 
-    # K6/K7 evaluator throughput (SURVEY cfg5 shape): 4096 candidate
-    # placements of this task at D = 8, scored and rolled out on this GPU
-    evaluator = None
-    if rank == 0 and not args.no_evaluator:
-        evaluator = bench_evaluator(args, local)
-        evaluator["sweep"] = bench_evaluator_sweep(local)
-        if world == 1 and not args.no_cpu and os.path.exists(os.path.join(
-                ROOT, "oracle", "_ref", "libshardplan_ref.so")):
-            evaluator["reference_cpu"] = bench_reference_evaluator()
 
     if rank == 0:
         line = {
