@@ -538,10 +538,20 @@ struct sp_evaluator {
   float *d_crepr32 = nullptr, *d_prepr32 = nullptr;
   int32_t* d_order = nullptr;
   double* d_need = nullptr;
+  // Per-call scratch, cached across calls: each entry point allocates its
+  // buffers in a fixed sequence, so slot k of pool[site] is always the same
+  // logical buffer; it is reallocated only when a call needs it larger
+  // (a cudaMalloc/cudaFree per call cost milliseconds of host time).
+  struct Scratch {
+    std::vector<std::pair<void*, size_t>> slots;
+  };
+  Scratch pool[2];  // 0: eval_batch, 1: rollout_batch
   ~sp_evaluator() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
     for (void* p : owned) cudaFree(p);
+    for (auto& sc : pool)
+      for (auto& s : sc.slots) cudaFree(s.first);
     if (stream) cudaStreamDestroy(stream);
   }
   template <class T>
@@ -666,17 +676,22 @@ int sp_eval_batch(sp_evaluator* ev, const int32_t* placements, int32_t n_cand,
     SP_CUDA(cudaSetDevice(ev->device));
     if (n_cand <= 0) return;
     const int M = ev->M, D = ev->D;
-    std::vector<void*> tmp;
-    auto cleanup = [&] {
-      cudaStreamSynchronize(ev->stream);
-      for (void* p : tmp) cudaFree(p);
-    };
+    size_t slot = 0;
+    auto cleanup = [&] { cudaStreamSynchronize(ev->stream); };
     try {
       auto al = [&](size_t bytes) {
-        void* p = nullptr;
-        SP_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 4)));
-        tmp.push_back(p);
-        return p;
+        bytes = std::max<size_t>(bytes, 4);
+        auto& slots = ev->pool[0].slots;
+        if (slot == slots.size()) slots.push_back({nullptr, 0});
+        auto& sl = slots[slot++];
+        if (sl.second < bytes) {
+          SP_CUDA(cudaStreamSynchronize(ev->stream));
+          if (sl.first) cudaFree(sl.first);
+          sl = {nullptr, 0};
+          SP_CUDA(cudaMalloc(&sl.first, bytes));
+          sl.second = bytes;
+        }
+        return sl.first;
       };
       int32_t* d_p = static_cast<int32_t*>(al(static_cast<size_t>(n_cand) * M * 4));
       float* d_o = static_cast<float*>(al(static_cast<size_t>(n_cand) * 4));
@@ -724,17 +739,22 @@ int sp_rollout_batch(sp_evaluator* ev, int32_t mode, const double* uniforms,
     if (n_refined) *n_refined = 0;
     if (n_cand <= 0) return;
     const int M = ev->M;
-    std::vector<void*> tmp;
-    auto cleanup = [&] {
-      cudaStreamSynchronize(ev->stream);
-      for (void* p : tmp) cudaFree(p);
-    };
+    size_t slot = 0;
+    auto cleanup = [&] { cudaStreamSynchronize(ev->stream); };
     try {
       auto al = [&](size_t bytes) {
-        void* p = nullptr;
-        SP_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 4)));
-        tmp.push_back(p);
-        return p;
+        bytes = std::max<size_t>(bytes, 4);
+        auto& slots = ev->pool[1].slots;
+        if (slot == slots.size()) slots.push_back({nullptr, 0});
+        auto& sl = slots[slot++];
+        if (sl.second < bytes) {
+          SP_CUDA(cudaStreamSynchronize(ev->stream));
+          if (sl.first) cudaFree(sl.first);
+          sl = {nullptr, 0};
+          SP_CUDA(cudaMalloc(&sl.first, bytes));
+          sl.second = bytes;
+        }
+        return sl.first;
       };
       RolloutArgs a{};
       a.order = ev->d_order;
