@@ -10,6 +10,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "common.h"
@@ -252,7 +253,15 @@ extern "C" int sp_ingest_batch_file(const char* path, const int32_t* dims,
       raise(SP_ERR_BAD_INPUT, "dims/hash_sizes length != num_tables");
     if (num_tables_out) *num_tables_out = static_cast<int32_t>(f.num_tables);
     if (batch_size_out) *batch_size_out = static_cast<int32_t>(f.batch_size);
-    DslbStreamer ring;
+    // pinned slots cached per device across calls (allocating them costs
+    // more than streaming a cfg3 file); deliberately never freed, so no CUDA
+    // call runs during static destruction
+    static std::mutex ring_mu;
+    static DslbStreamer* rings[64] = {};
+    std::lock_guard<std::mutex> lk(ring_mu);
+    DslbStreamer*& rp = rings[cuda_device & 63];
+    if (!rp) rp = new DslbStreamer();
+    DslbStreamer& ring = *rp;
     ingest_impl(
         off.data(), n_off,
         [&](int64_t* d_idx, cudaStream_t st) {
