@@ -229,3 +229,26 @@ def test_hot_rows_and_empty_tables(bwd_path):
                                 off, idx, B, grad, 0.001, [0, 1, 2])
     for i in range(3):
         np.testing.assert_allclose(sh.get_table(i), want[i], rtol=RTOL, atol=1e-4)
+
+
+def test_runs_spanning_many_sgd_tiles(bwd_path):
+    """Tables of 1-3 rows at B = 4096: every row's run covers thousands of
+    sorted positions, i.e. dozens of segmented-SGD tiles (1024 positions),
+    so the per-chunk partials and the cross-tile carries are all exercised;
+    plus a 4-row fp32 table of dim 8 and a generic dim (12)."""
+    B = 4096
+    dims = [16, 64, 128, 8, 12]
+    tables = make_tables(dims, [1, 2, 3, 4, 3], [8.0, 6.0, 5.0, 4.0, 3.0])
+    task = PlacementTask(tables, 1, 0.0, B)
+    weights = random_weights(9, tables)
+    off, idx = orc.synth_batch(as_dicts(tables), B, seed=31)
+    grad = np.random.default_rng(5).uniform(-1, 1, size=(B, sum(dims))).astype(np.float32)
+    sh = _shard(task, [0] * len(dims), weights, lr=0.001)
+    sh.upload_batch(LookupBatch(idx, off, len(dims), B))
+    sh.set_grad(grad)
+    sh.run_iteration()
+    want = orc.tbe_backward_sgd(dims, [t.hash_size for t in tables], weights, off, idx, B, grad,
+                                0.001, list(range(len(dims))))
+    for i in range(len(dims)):
+        np.testing.assert_allclose(sh.get_table(i), want[i], rtol=RTOL, atol=1e-5)
+    sh.close()
