@@ -339,8 +339,11 @@ class HostBuffer:
         self.array = np.frombuffer(buf, dtype=self.dtype)[:n]
 
     def __del__(self):
-        if getattr(self, "_p", None) and self._p.value:
-            lib().sp_host_free(self._p)
+        try:
+            if getattr(self, "_p", None) and self._p.value:
+                lib().sp_host_free(self._p)
+        except Exception:  # interpreter shutdown: the library binding is gone
+            pass
             self._p = ctypes.c_void_p()
 
 
@@ -383,7 +386,10 @@ class EmbeddingShard:
             self._h = ctypes.c_void_p()
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown: the library binding is gone
+            pass
 
     # -- properties
     @property
@@ -921,7 +927,10 @@ class Evaluator:
             self._h = ctypes.c_void_p()
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown: the library binding is gone
+            pass
 
     def order(self) -> np.ndarray:
         """predicted_order (harness.hpp:131-137)."""
