@@ -160,7 +160,7 @@ def bench_cfg4(args, device: int):
             sh.backward_sgd()
         k = sh.kernel_ms()
         sh.set_profiling(False)
-        ms = {name: round(k[name][0] / n, 4) for name in ("fwd", "keys", "sort", "sgd")}
+        ms = {name: round(k[name][0] / n, 4) for name in ("fwd", "sort", "sgd")}
         ranks.append({"rank": r, "tables": len(sh.local_tables()), "lookups": int(sh.nnz),
                       "gb": round(sh.device_bytes / 1e9, 2), "ms": ms,
                       "compute_ms": round(sum(ms.values()), 4)})
@@ -168,7 +168,7 @@ def bench_cfg4(args, device: int):
         torch.cuda.synchronize()
     return {"placement": "dreamshard", "ranks": ranks,
             "max_compute_ms": max(x["compute_ms"] for x in ranks),
-            "note": "per rank: K1 + key build + sort + SGD, serialised (no overlap, no "
+            "note": "per rank: K1 + sort + SGD, serialised (no overlap, no "
                     "exchange); the 8-GPU step adds the NVLink exchange"}
 
 
@@ -537,12 +537,9 @@ def run_ours(args, world, rank, local):
     per_launch = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in kms.items()}
     # per-launch algorithmic bytes as the library runs each kernel
     # (sp_ctx_algorithmic_bytes documents the formulas)
-    alg = {"fwd": ab["fwd"], "sgd": ab["bwd"], "sort": ab["sort"],
-           "keys": 4.0 * (T_local * task.batch_size + 1) + 10.0 * nnz}
+    alg = {"fwd": ab["fwd"], "sgd": ab["bwd"], "sort": ab["sort"]}
     kernels = {}
-    for k in ("fwd", "keys", "sort", "sgd"):
-        if k == "keys" and kms[k][1] == 0:
-            continue
+    for k in ("fwd", "sort", "sgd"):
         t = per_launch.get(k, 0.0)
         kernels[k] = {"ms": round(t, 4),
                       "share": round(kms[k][0] / max(1e-9, sum(v[0] for v in kms.values())), 3),

@@ -267,15 +267,22 @@ int sp_enqueue_iteration(sp_ctx* ctx);
  * times; 0 iters only builds the graph. Reports kernel nodes per graph. */
 int sp_graph_replay(sp_ctx* ctx, int32_t iters, int32_t* kernels_per_iter);
 
-/* The backward's key build + radix sort reads only the batch: by default
- * (one device per context) it runs on a high-priority side stream,
- * concurrently with the forward and the exchanges. on = 0 serialises it
- * behind K1 (per-kernel timing in isolation). */
+/* The backward's stable sort (K4a) reads only the batch: by default (one
+ * device per context) it runs on a high-priority side stream, concurrently
+ * with the forward and the exchanges. on = 0 serialises it behind K1
+ * (per-kernel timing in isolation). */
 int sp_ctx_set_overlap(sp_ctx* ctx, int32_t on);
+/* K4a sort plan override: buckets and warp-tiles of about `lookups` lookups
+ * per table (0 = the default ~sqrt(64 n) rule). The sorted result does not
+ * depend on it; tests use small targets to cover many buckets and tiles. */
+int sp_ctx_set_sort_target(sp_ctx* ctx, int64_t lookups);
+/* Indices per H2D chunk of the pipelined host-buffer upload (default 2^23);
+ * results do not depend on it. */
+int sp_ctx_set_upload_chunk(sp_ctx* ctx, int64_t indices);
 
 /* Per-kernel CUDA-event timing of the hot-path launches enqueued while
  * enabled (on the context stream): sp_ctx_kernel_ms returns the summed ms
- * and launch counts of [0]=K1 forward, [1]=key build, [2]=radix sort,
+ * and launch counts of [0]=K1 forward, [1]=(unused), [2]=K4a sort,
  * [3]=K4 SGD, [4]=exchange, and resets the accumulators (synchronizes). */
 int sp_ctx_set_profiling(sp_ctx* ctx, int32_t on);
 int sp_ctx_kernel_ms(sp_ctx* ctx, double ms[5], int64_t counts[5]);

@@ -59,6 +59,8 @@ SIGNATURES = {
     "sp_ctx_algorithmic_bytes": (c_i32, [c_vp, P(c_f64)]),
     "sp_ctx_set_profiling": (c_i32, [c_vp, c_i32]),
     "sp_ctx_set_overlap": (c_i32, [c_vp, c_i32]),
+    "sp_ctx_set_sort_target": (c_i32, [c_vp, c_i64]),
+    "sp_ctx_set_upload_chunk": (c_i32, [c_vp, c_i64]),
     "sp_costnet_trainer_create": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i32, c_i32, c_i32,
                                           c_f64, c_i64, c_i32, P(c_vp)]),
     "sp_costnet_trainer_destroy": (None, [c_vp]),

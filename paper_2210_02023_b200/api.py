@@ -584,10 +584,21 @@ class EmbeddingShard:
         (default) or serialised behind it (sp_ctx_set_overlap)."""
         check(lib().sp_ctx_set_overlap(self._h, 1 if on else 0))
 
+    def set_sort_target(self, lookups: int):
+        """K4a sort plan override (sp_ctx_set_sort_target): buckets and
+        warp-tiles of about `lookups` lookups, 0 = default. Results are
+        independent of it."""
+        check(lib().sp_ctx_set_sort_target(self._h, int(lookups)))
+
+    def set_upload_chunk(self, indices: int):
+        """Indices per H2D chunk of the pipelined host-buffer upload
+        (sp_ctx_set_upload_chunk). Results are independent of it."""
+        check(lib().sp_ctx_set_upload_chunk(self._h, int(indices)))
+
     def set_profiling(self, on: bool):
         check(lib().sp_ctx_set_profiling(self._h, 1 if on else 0))
 
-    KERNELS = ("fwd", "keys", "sort", "sgd", "exchange")
+    KERNELS = ("fwd", "unused", "sort", "sgd", "exchange")
 
     def kernel_ms(self) -> dict:
         """Summed CUDA-event ms and launch counts per hot kernel since the

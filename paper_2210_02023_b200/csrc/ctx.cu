@@ -24,7 +24,6 @@
 #include "common.h"
 #include "nccl_loader.h"
 #include "synth.cuh"
-#include "bwd.h"
 #include "dslb.h"
 #include "tbe.h"
 
@@ -48,103 +47,15 @@ T* dalloc(size_t n, std::vector<void*>& owned, uint64_t& bytes) {
   return static_cast<T*>(p);
 }
 
-// Consecutive local tables sorted together in the CUB backward: keys are
-// relative to the group (rowbase/rb_end of its tables are group-relative),
-// so a group's key width is ceil(log2(its rows)) and its sort costs
-// ceil(bits / 8) radix passes over its lookups plus a fixed launch overhead
-// (histogram, scan, gaps). The grouping minimises that cost over consecutive
-// tables (dynamic programming) with the lookups estimated as pf * B:
-// cfg3's 1e5-1e6-row tables end up in groups of <= 2^24 rows (3 passes
-// instead of 4 for one 26-bit sort); cfg4's 1e7-row tables share one 28-bit
-// group instead of 25 small sorts (1.6 -> ~0.4 ms per rank, measured).
-constexpr double kSortGroupUs = 40.0;     // fixed cost of one group's sort (us)
-constexpr double kSortPassUsPerM = 9.0;   // one 8-bit pass over 1M lookups (us)
-
-// Returns the first local table of every group after the first, then T.
-std::vector<int> plan_sort_groups(const sp_table_spec* tables, const std::vector<int>& ids,
-                                  int batch, int min_groups = 1) {
-  const int T = static_cast<int>(ids.size());
-  uint64_t cap = uint64_t(1) << 32;  // 32-bit keys
-  if (const char* f = std::getenv("SP_SORT_GROUP_ROWS"))  // tests: force many groups
-    cap = std::max<uint64_t>(1, std::strtoull(f, nullptr, 10));
-  std::vector<double> best(T + 1, 1e300);
-  std::vector<int> from(T + 1, 0);
-  best[0] = 0.0;
-  for (int j = 1; j <= T; ++j) {
-    uint64_t rows = 0;
-    double nnz = 0.0;
-    for (int i = j - 1; i >= 0; --i) {
-      const sp_table_spec& t = tables[ids[i]];
-      rows += static_cast<uint64_t>(t.hash_size);
-      nnz += std::max(0.0, t.pooling_factor) * batch;
-      if (i < j - 1 && rows > cap) break;
-      int bits = 1;
-      while (bits < 32 && (uint64_t(1) << bits) < std::max<uint64_t>(rows, 2)) ++bits;
-      const double c = best[i] + kSortGroupUs + ((bits + 7) / 8) * nnz * 1e-6 * kSortPassUsPerM;
-      if (c < best[j]) {
-        best[j] = c;
-        from[j] = i;
-      }
-    }
-  }
-  std::vector<int> ends;
-  for (int j = T; j > 0; j = from[j]) ends.push_back(j);
-  std::reverse(ends.begin(), ends.end());
-  // The groups sort concurrently (SP_SORT_STREAMS): split the heaviest
-  // multi-table group at its lookup midpoint until there are min_groups.
-  // Splitting never widens a key, so no pass is added.
-  auto nnz_of = [&](int a, int b) {
-    double n = 0.0;
-    for (int i = a; i < b; ++i) n += std::max(0.0, tables[ids[i]].pooling_factor) * batch;
-    return n;
-  };
-  while (static_cast<int>(ends.size()) < min_groups) {
-    int best_g = -1;
-    double best_n = 0.0;
-    for (size_t g = 0; g < ends.size(); ++g) {
-      const int a = g == 0 ? 0 : ends[g - 1], b = ends[g];
-      const double n = nnz_of(a, b);
-      if (b - a >= 2 && n > best_n) {
-        best_n = n;
-        best_g = static_cast<int>(g);
-      }
-    }
-    if (best_g < 0) break;
-    const int a = best_g == 0 ? 0 : ends[best_g - 1], b = ends[best_g];
-    int cut = a + 1;
-    double acc = 0.0, best_gap = 1e300;
-    for (int i = a + 1; i < b; ++i) {
-      acc += nnz_of(i - 1, i);
-      const double gap = std::abs(2.0 * acc - best_n);
-      if (gap < best_gap) {
-        best_gap = gap;
-        cut = i;
-      }
-    }
-    ends.insert(ends.begin() + best_g, cut);
-  }
-  return ends;
-}
-struct SortGroup {
-  int t0 = 0, t1 = 0;      // local tables [t0, t1)
-  int end_bit = 1;         // key bits
-  int64_t row_base = 0;    // device rows before the group (key offset)
-  int64_t p0 = 0, p1 = 0;  // positions of its lookups in the CSR
-};
-
 struct VDev {
   int vid = 0;
-  std::vector<SortGroup> groups;
   std::vector<int> tables;  // global ids, ascending
   std::vector<TableMeta> meta_canon;
-  std::vector<uint32_t> rb_end;
   std::vector<int32_t> colmap;  // local col -> global col
   int64_t W = 0, rows_total = 0, n_tiles = 0;
-  int end_bit = 1;
   int4* d_tiles = nullptr;      // K1 tiles in launch order (heavy tables first)
   int4* d_tiles_canon = nullptr;  // K1 tiles in table order (pipelined upload path)
   std::vector<int64_t> tile_start;  // first canonical tile of each local table (+ end)
-  std::vector<int> group_of_table;  // sort group of each local table
   // K4 SGD tiles of the current batch, one buffer per staging slot (a step's
   // tiles upload while the previous step's SGD may still read its own)
   int* d_sgd_tiles[2] = {};
@@ -152,17 +63,19 @@ struct VDev {
   int64_t n_sgd_tiles = 0;
   int64_t sgd_counts[2] = {};  // generic-dim (run-based) / segmented SGD tiles
   int cur = 0;  // slot of the current batch
-  uint32_t* d_keys = nullptr;   // backward sort pairs (written by K1)
-  uint32_t* d_bags = nullptr;
-  bool keys_valid = false;
-  // K4 v2 (bwd.cu): bucket layout of the current batch
-  bool bucketed = false;
-  std::vector<BucketMeta> bmeta;
-  BucketMeta* d_bm = nullptr;
-  int64_t n_cnt = 0;
-  int n_btiles = 0, n_buckets = 0;
+  // K4a sort (sort.cu): the plan and its device copies, the count matrix,
+  // the bucket starts and the packed intermediates (nnz entries)
+  SortPlan splan;
+  SortTable* d_stabs = nullptr;
+  int2* d_wtiles = nullptr;
+  int2* d_bkts = nullptr;
+  int* d_cnt = nullptr;
+  int* d_bstart = nullptr;
+  int2* d_big = nullptr;   // large-bucket list (+ its count)
+  int* d_nbig = nullptr;
+  void* d_mid = nullptr;
+  int64_t mid_cap = 0;
   TableMeta* d_meta_canon = nullptr;
-  uint32_t* d_rb_end = nullptr;
   int32_t* d_colmap = nullptr;
   int32_t* d_off = nullptr;
   int32_t* d_idx = nullptr;
@@ -232,26 +145,12 @@ struct sp_ctx {
   float* d_recv = nullptr;     // rows_per_dst * W_total per destination
   float* d_gin = nullptr;
   int n_dst = 1;               // destinations held here (D in emulation)
-  uint32_t *d_kb = nullptr, *d_bb = nullptr;  // sorted keys / bags
-  uint32_t* d_seg = nullptr;
-  bool fuse_keys = true;       // K1 emits the backward's sort pairs (CUB path)
-  bool use_buckets = false;    // K4 v2 bucketed sort + SGD (SP_BWD=bucket); slower on
-                               // B200 so far (profiles/r01_notes.md), CUB path default
-  int32_t *d_prow = nullptr, *d_pbag = nullptr, *d_scr = nullptr;  // bucketed pairs
-  int32_t *d_cnt = nullptr, *d_cpos = nullptr;
-  int64_t cnt_cap = 0;
-  std::vector<void*> bucket_owned;
-  int32_t* d_nseg = nullptr;
+  uint32_t *d_kb = nullptr, *d_bb = nullptr;  // sorted keys / bags (shared, stream-ordered)
+  int64_t sort_target = 0;     // sort plan bucket/tile size override (tests), 0 = default
   int32_t* d_flag = nullptr;
   int64_t sort_cap = 0;
-  void* d_temp = nullptr;
-  size_t temp_bytes = 0;
   int64_t* d_stage64 = nullptr;      // int64 staging of an uploaded LookupBatch
   int64_t* d_stage64_alt = nullptr;  // second slot (sp_run_batches: next step's H2D)
-  std::vector<cudaStream_t> sort_st;   // SP_SORT_STREAMS - 1 extra sort streams
-  std::vector<void*> sort_temp;        // their CUB scratch (temp_bytes each)
-  std::vector<cudaEvent_t> ev_sjoin;
-  cudaEvent_t ev_sfork = nullptr;
   int64_t* file_off = nullptr;       // pinned offsets of a DSLB file (sp_upload_batch_file)
   int64_t file_off_cap = 0;
   std::unique_ptr<sp::DslbStreamer> file_ring;  // pinned ring: file -> device indices
@@ -263,8 +162,8 @@ struct sp_ctx {
   int64_t carry_cap = 0;
   int32_t* d_step_flags = nullptr;   // per-step validation flags (sp_run_batches)
   int64_t step_flags_cap = 0;
-  // pinned host copies of a batch's layout metadata (SGD tiles, sort group
-  // starts), one per staging slot: a pageable H2D would wait for the stream
+  // pinned host copies of a batch's layout metadata (SGD tiles), one per
+  // staging slot: a pageable H2D would wait for the stream
   uint8_t* meta_host[2] = {};
   size_t meta_cap[2] = {};
   cudaEvent_t slot_done[2] = {};     // after the SGD of the last step that used a slot
@@ -273,17 +172,13 @@ struct sp_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // H2D of uploaded batches
   // The backward's sort depends only on the batch, not on the gradient: with
-  // one (virtual) device it runs on `side` concurrently with the forward and
-  // the exchanges (SP_OVERLAP=0 serialises it behind K1 again).
+  // one (virtual) device it runs on the high-priority `side` stream
+  // concurrently with the forward and the exchanges (sp_ctx_set_overlap(0)
+  // serialises it behind K1).
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool overlap_sort = true;
-  // 1: keys rebuilt from the CSR + the whole sort on the side stream under K1;
-  // 2 (SP_OVERLAP=2): K1 per sort group emitting the keys, each group's sort
-  // under K1 of the next groups (measured slower at cfg3: 4.81 vs 4.43 ms,
-  // the last group's sort is left exposed)
-  int overlap_mode = 1;
-  int64_t upload_chunk = int64_t(8) << 20;  // indices per H2D chunk (SP_UPLOAD_CHUNK)
+  int64_t upload_chunk = int64_t(8) << 20;  // indices per H2D chunk (sp_ctx_set_upload_chunk)
   std::vector<cudaEvent_t> upload_events;
   ncclComm_t comm = nullptr;
   // Peer-memory exchange (sp_ipc_import): every rank's receive and gradient
@@ -320,19 +215,15 @@ struct sp_ctx {
       if (e) cudaEventDestroy(e);
     for (auto& e : ev_pool) cudaEventDestroy(e);
     for (auto& v : vdevs)
-      for (void* p : {static_cast<void*>(v.d_idx), static_cast<void*>(v.d_keys),
-                       static_cast<void*>(v.d_bags), static_cast<void*>(v.d_sgd_tiles[0]),
-                       static_cast<void*>(v.d_sgd_tiles[1])})
+      for (void* p : {static_cast<void*>(v.d_idx), v.d_mid, static_cast<void*>(v.d_sgd_tiles[0]),
+                       static_cast<void*>(v.d_sgd_tiles[1]), static_cast<void*>(v.d_stabs),
+                       static_cast<void*>(v.d_wtiles), static_cast<void*>(v.d_bkts),
+                       static_cast<void*>(v.d_cnt), static_cast<void*>(v.d_bstart),
+                       static_cast<void*>(v.d_big), static_cast<void*>(v.d_nbig)})
         if (p) cudaFree(p);
     if (d_stage64) cudaFree(d_stage64);
     if (d_stage64_alt) cudaFree(d_stage64_alt);
     file_ring.reset();
-    for (auto& st2 : sort_st) {
-      cudaStreamSynchronize(st2);
-      cudaStreamDestroy(st2);
-    }
-    for (auto& e : ev_sjoin) cudaEventDestroy(e);
-    if (ev_sfork) cudaEventDestroy(ev_sfork);
     if (file_off) cudaFreeHost(file_off);
     if (d_step_flags) cudaFree(d_step_flags);
     if (d_carry_f) cudaFree(d_carry_f);
@@ -344,7 +235,6 @@ struct sp_ctx {
     for (auto& e : slot_done)
       if (e) cudaEventDestroy(e);
     if (meta_ready) cudaEventDestroy(meta_ready);
-    for (void* p : bucket_owned) cudaFree(p);
     for (void* p : sort_owned) cudaFree(p);
     for (void* p : owned) cudaFree(p);
     if (comm) sp::nccl().CommDestroy(comm);
@@ -370,9 +260,9 @@ void* wptr(const sp_ctx* c, int g) {
   return static_cast<uint8_t*>(c->d_w) + c->woff[g] * elem_bytes(c->wt);
 }
 
-// Frees and re-allocates the shared sort scratch for n positions.
+// Frees and re-allocates the shared sorted keys / bags for n positions.
 void ensure_sort_capacity(sp_ctx* c, int64_t n) {
-  if (n <= c->sort_cap && c->d_temp) return;
+  if (n <= c->sort_cap && c->d_kb) return;
   SP_CUDA(cudaStreamSynchronize(c->stream));
   if (c->side) SP_CUDA(cudaStreamSynchronize(c->side));
   for (void* p : c->sort_owned) cudaFree(p);
@@ -381,50 +271,53 @@ void ensure_sort_capacity(sp_ctx* c, int64_t n) {
   uint64_t dummy = 0;
   c->d_kb = dalloc<uint32_t>(cap, c->sort_owned, dummy);
   c->d_bb = dalloc<uint32_t>(cap, c->sort_owned, dummy);
-  c->d_seg = dalloc<uint32_t>(cap + 1, c->sort_owned, dummy);
-  int max_bit = 1;
-  for (auto& v : c->vdevs) max_bit = std::max(max_bit, v.end_bit);
-  const size_t t1 = sort_pairs(nullptr, 0, c->d_kb, c->d_kb, c->d_bb, c->d_bb, c->bags16, cap,
-                               max_bit, c->stream);
-  const size_t t2 = select_heads(nullptr, 0, c->d_kb, cap, c->d_seg, c->d_nseg,
-                                 c->stream);
-  c->temp_bytes = std::max({t1, t2, static_cast<size_t>(256)});
-  c->d_temp = dalloc<uint8_t>(c->temp_bytes, c->sort_owned, dummy);
-  for (auto& t : c->sort_temp) t = dalloc<uint8_t>(c->temp_bytes, c->sort_owned, dummy);
-  // bucketed backward: (row, bag) pairs in bucket order + oversize scratch
-  c->d_prow = dalloc<int32_t>(cap, c->sort_owned, dummy);
-  c->d_pbag = dalloc<int32_t>(cap, c->sort_owned, dummy);
-  c->d_scr = dalloc<int32_t>(cap, c->sort_owned, dummy);
   c->sort_cap = cap;
 }
 
-// Bucket layouts of every (virtual) device for the current batch.
-void plan_buckets(sp_ctx* c) {
-  int64_t need = 0;
-  for (auto& v : c->vdevs) {
-    v.bucketed = c->use_buckets && c->wt == WeightType::kF32 && !v.tables.empty() &&
-                 bucket_plan(v.meta_canon, v.table_nnz, c->B, v.bmeta, v.n_cnt, v.n_btiles,
-                             v.n_buckets);
-    if (!v.bucketed) continue;
-    if (!v.d_bm) v.d_bm = dalloc<BucketMeta>(v.tables.size(), c->bucket_owned, c->dev_bytes);
-    SP_CUDA(cudaMemcpy(v.d_bm, v.bmeta.data(), v.bmeta.size() * sizeof(BucketMeta),
-                       cudaMemcpyHostToDevice));
-    need = std::max(need, v.n_cnt);
-  }
-  if (need > c->cnt_cap) {
-    SP_CUDA(cudaStreamSynchronize(c->stream));
-    if (c->d_cnt) cudaFree(c->d_cnt);
-    if (c->d_cpos) cudaFree(c->d_cpos);
-    SP_CUDA(cudaMalloc(&c->d_cnt, need * sizeof(int32_t)));
-    SP_CUDA(cudaMalloc(&c->d_cpos, need * sizeof(int32_t)));
-    c->cnt_cap = need;
-    const size_t tb = bwd_scan_temp_bytes(need, c->stream);
-    if (tb > c->temp_bytes) {
-      uint64_t dummy = 0;
-      c->temp_bytes = tb;
-      c->d_temp = dalloc<uint8_t>(tb, c->sort_owned, dummy);
-    }
-  }
+// The sort's packed intermediates for idx_cap lookups: the pairs, then the
+// scratch of buckets too large for shared memory.
+void ensure_mid(sp_ctx* c, VDev& v) {
+  if (v.mid_cap >= v.idx_cap && v.d_mid != nullptr) return;
+  SP_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->side) SP_CUDA(cudaStreamSynchronize(c->side));
+  if (v.d_mid) cudaFree(v.d_mid);
+  v.d_mid = nullptr;
+  const int64_t cap = std::max<int64_t>(v.idx_cap, 1);
+  SP_CUDA(cudaMalloc(&v.d_mid, 2 * cap * sort_mid_bytes(v.splan)));
+  v.mid_cap = cap;
+}
+
+// The K4a sort plan of a (virtual) device (sort.cu: bucket width and
+// warp-tile size per table from its expected lookups pf * B) and its device
+// copies; re-planned by sp_ctx_set_sort_target.
+void plan_sort(sp_ctx* c, VDev& v) {
+  std::vector<double> est;
+  for (int g : v.tables) est.push_back(std::max(0.0, c->tables[g].pooling_factor) * c->B);
+  v.splan = sort_plan(v.meta_canon, est, c->B, c->sort_target, c->bags16);
+  // the intermediates' width may change with the plan
+  if (v.d_mid) cudaFree(v.d_mid);
+  v.d_mid = nullptr;
+  v.mid_cap = 0;
+  if (v.idx_cap > 0) ensure_mid(c, v);
+  for (void* p : {static_cast<void*>(v.d_stabs), static_cast<void*>(v.d_wtiles),
+                   static_cast<void*>(v.d_bkts), static_cast<void*>(v.d_cnt),
+                   static_cast<void*>(v.d_bstart), static_cast<void*>(v.d_big),
+                   static_cast<void*>(v.d_nbig)})
+    if (p) cudaFree(p);
+  const SortPlan& pl = v.splan;
+  auto up = [](auto*& dst, const auto& vec) {
+    using T = typename std::decay_t<decltype(vec)>::value_type;
+    SP_CUDA(cudaMalloc(&dst, std::max<size_t>(vec.size(), 1) * sizeof(T)));
+    if (!vec.empty())
+      SP_CUDA(cudaMemcpy(dst, vec.data(), vec.size() * sizeof(T), cudaMemcpyHostToDevice));
+  };
+  up(v.d_stabs, pl.tabs);
+  up(v.d_wtiles, pl.wtiles);
+  up(v.d_bkts, pl.bkts);
+  SP_CUDA(cudaMalloc(&v.d_cnt, std::max<int64_t>(pl.n_cnt, 1) * sizeof(int)));
+  SP_CUDA(cudaMalloc(&v.d_bstart, std::max<int32_t>(pl.n_bstart, 1) * sizeof(int)));
+  SP_CUDA(cudaMalloc(&v.d_big, std::max<size_t>(pl.bkts.size(), 1) * sizeof(int2)));
+  SP_CUDA(cudaMalloc(&v.d_nbig, sizeof(int)));
 }
 
 void check_ctx(sp_ctx* c) {
@@ -476,120 +369,26 @@ struct ProfScope {
 
 // The sort runs on the side stream, concurrently with the forward.
 bool overlap_active(const sp_ctx* c) {
-  return c->overlap_sort && c->vdevs.size() == 1 && !c->vdevs[0].bucketed &&
-         c->vdevs[0].nnz > 0;
+  return c->overlap_sort && c->vdevs.size() == 1 && c->vdevs[0].nnz > 0;
 }
 
 void stage_forward(sp_ctx* c, VDev& v) {
-  const bool emit = c->fuse_keys && !v.bucketed && v.nnz > 0 && !overlap_active(c);
   ProfScope prof(c, kProfFwd);
-  static const bool per_table = std::getenv("SP_K1_PER_TABLE") != nullptr;  // diagnostic
-  if (per_table) {
-    for (size_t li = 0; li < v.tables.size(); ++li)
-      launch_tbe_forward(v.d_meta_canon, v.d_tiles_canon + v.tile_start[li],
-                         v.tile_start[li + 1] - v.tile_start[li], c->B, v.d_off, v.d_idx,
-                         c->d_w, c->wt, v.d_pooled, c->d_rowmap, v.W,
-                         emit ? v.d_keys : nullptr, emit ? v.d_bags : nullptr, c->bags16,
-                         c->stream);
-    v.keys_valid = emit;
-    return;
-  }
-  launch_tbe_forward(v.d_meta_canon, v.d_tiles, v.n_tiles, c->B, v.d_off, v.d_idx,
-                     c->d_w, c->wt, v.d_pooled, c->d_rowmap, v.W, emit ? v.d_keys : nullptr,
-                     emit ? v.d_bags : nullptr, c->bags16, c->stream);
-  // every iteration builds its sort pairs once: here, or (when K1 does not
-  // emit them) in the backward's key build
-  v.keys_valid = emit;
+  launch_tbe_forward(v.d_meta_canon, v.d_tiles, v.n_tiles, c->B, v.d_off, v.d_idx, c->d_w, c->wt,
+                     v.d_pooled, c->d_rowmap, v.W, c->stream);
 }
 
-// (keys) -> stable radix sort; leaves sorted keys in d_kb, bags in d_bb.
-void sort_pairs_of(sp_ctx* c, VDev& v, const SortGroup& g, cudaStream_t st,
-                   void* temp = nullptr) {
-  if (g.p1 == g.p0) return;
-  const size_t bb = c->bags16 ? 2 : 4;
-  sort_pairs(temp ? temp : c->d_temp, c->temp_bytes, v.d_keys + g.p0, c->d_kb + g.p0,
-             reinterpret_cast<const char*>(v.d_bags) + g.p0 * bb,
-             reinterpret_cast<char*>(c->d_bb) + g.p0 * bb, c->bags16, g.p1 - g.p0, g.end_bit,
-             st);
-}
-
-// rebuild: derive the keys from the CSR even if K1 emitted them (the
-// overlapped sort does not wait for K1).
-void sort_group(sp_ctx* c, VDev& v, int gi, cudaStream_t st, void* temp = nullptr);
-
-void stage_sort(sp_ctx* c, VDev& v, cudaStream_t st, bool rebuild = false) {
-  const int S = static_cast<int>(c->sort_st.size()) + 1;
-  if (S > 1 && v.groups.size() > 1 && (!v.keys_valid || rebuild) && !c->profiling) {
-    // each group's key build and sort on its own stream: group g's sort
-    // starts as soon as its own keys exist
-    SP_CUDA(cudaEventRecord(c->ev_sfork, st));
-    for (int k = 1; k < S; ++k) SP_CUDA(cudaStreamWaitEvent(c->sort_st[k - 1], c->ev_sfork, 0));
-    for (size_t gi = 0; gi < v.groups.size(); ++gi) {
-      const int k = static_cast<int>(gi % S);
-      if (k == 0) sort_group(c, v, static_cast<int>(gi), st);
-      else sort_group(c, v, static_cast<int>(gi), c->sort_st[k - 1], c->sort_temp[k - 1]);
-    }
-    for (int k = 1; k < S; ++k) {
-      SP_CUDA(cudaEventRecord(c->ev_sjoin[k - 1], c->sort_st[k - 1]));
-      SP_CUDA(cudaStreamWaitEvent(st, c->ev_sjoin[k - 1], 0));
-    }
-    v.keys_valid = true;
-    return;
-  }
-  if (!v.keys_valid || rebuild) {
-    ProfScope prof(c, kProfKeys, st);
-    launch_build_keys(v.d_meta_canon, static_cast<int>(v.tables.size()), c->B, v.d_off,
-                      v.d_idx, v.d_keys, v.d_bags, c->bags16, st);
-    v.keys_valid = true;
-  }
+// K4a: the stable sort of local tables [t0, t1) (their CSR is on the device)
+// into the shared sorted keys / bags.
+void sort_range(sp_ctx* c, VDev& v, int t0, int t1, cudaStream_t st) {
+  if (t1 <= t0) return;
   ProfScope prof(c, kProfSort, st);
-  if (S == 1 || v.groups.size() < 2) {
-    for (const SortGroup& g : v.groups) sort_pairs_of(c, v, g, st);
-    return;
-  }
-  // SP_SORT_STREAMS > 1: groups round-robin over st and the extra sort
-  // streams (each with its own CUB scratch), joined back into st
-  SP_CUDA(cudaEventRecord(c->ev_sfork, st));
-  for (int k = 1; k < S; ++k) SP_CUDA(cudaStreamWaitEvent(c->sort_st[k - 1], c->ev_sfork, 0));
-  for (size_t gi = 0; gi < v.groups.size(); ++gi) {
-    const int k = static_cast<int>(gi % S);
-    if (k == 0) sort_pairs_of(c, v, v.groups[gi], st);
-    else sort_pairs_of(c, v, v.groups[gi], c->sort_st[k - 1], c->sort_temp[k - 1]);
-  }
-  for (int k = 1; k < S; ++k) {
-    SP_CUDA(cudaEventRecord(c->ev_sjoin[k - 1], c->sort_st[k - 1]));
-    SP_CUDA(cudaStreamWaitEvent(st, c->ev_sjoin[k - 1], 0));
-  }
+  launch_sort(v.splan, v.d_stabs, v.d_wtiles, v.d_bkts, t0, t1, c->B, v.d_off, v.d_idx, v.d_cnt,
+              v.d_bstart, v.d_big, v.d_nbig, v.d_mid, v.mid_cap, c->d_kb, c->d_bb, c->bags16, st);
 }
 
-// Keys (from the CSR) and the stable sort of one sort group's lookups.
-void sort_group(sp_ctx* c, VDev& v, int gi, cudaStream_t st, void* temp) {
-  const SortGroup& g = v.groups[gi];
-  {
-    ProfScope prof(c, kProfKeys, st);
-    launch_build_keys(v.d_meta_canon + g.t0, g.t1 - g.t0, c->B, v.d_off, v.d_idx, v.d_keys,
-                      v.d_bags, c->bags16, st);
-  }
-  ProfScope prof(c, kProfSort, st);
-  sort_pairs_of(c, v, g, st, temp);
-}
-
-// Bucketed backward (bwd.cu): partition pairs into row buckets, then one
-// block per bucket sorts by row and applies the SGD. sorted_* non-null also
-// writes the sorted (key, bag) pairs (test API) and do_sgd gates the update.
-void stage_backward_bucketed(sp_ctx* c, VDev& v, uint32_t* sorted_keys, uint32_t* sorted_bags,
-                             bool do_sgd) {
-  const int T = static_cast<int>(v.tables.size());
-  {
-    ProfScope prof(c, kProfSort);
-    launch_bwd_partition(v.d_bm, T, v.n_btiles, v.n_cnt, c->B, v.d_off, v.d_idx, c->d_cnt,
-                         c->d_cpos, c->d_temp, c->temp_bytes, c->d_prow, c->d_pbag, c->stream);
-  }
-  ProfScope prof(c, kProfSgd);
-  launch_bwd_buckets(v.d_meta_canon, v.d_bm, T, v.n_buckets, c->d_cpos, v.nnz, c->d_prow,
-                     c->d_pbag, c->d_scr, v.d_grad, v.W, c->lr, static_cast<float*>(c->d_w),
-                     sorted_keys, sorted_bags,
-                     do_sgd, c->stream);
+void stage_sort(sp_ctx* c, VDev& v, cudaStream_t st) {
+  sort_range(c, v, 0, static_cast<int>(v.tables.size()), st);
 }
 
 // sorted: the overlapped sort already ran (the caller joined its stream).
@@ -598,10 +397,6 @@ void stage_backward_bucketed(sp_ctx* c, VDev& v, uint32_t* sorted_keys, uint32_t
 void stage_backward(sp_ctx* c, VDev& v, bool sorted = false,
                     const int32_t* abort_flag = nullptr) {
   if (v.nnz == 0) return;
-  if (v.bucketed) {
-    stage_backward_bucketed(c, v, nullptr, nullptr, true);
-    return;
-  }
   if (!sorted) stage_sort(c, v, c->stream);
   ProfScope prof(c, kProfSgd);
   launch_sgd(v.d_meta_canon, v.d_sgd_tiles[v.cur], v.sgd_counts, c->d_kb, c->d_bb, c->bags16,
@@ -711,47 +506,20 @@ void barrier(sp_ctx* c) {
 
 bool exchange_needed(const sp_ctx* c) { return c->D > 1; }
 
-// Fork: the side stream builds the sort keys from the CSR and sorts them
-// while the main stream runs the forward and the exchanges.
+// Fork: the side stream sorts the batch's lookups while the main stream runs
+// the forward and the exchanges.
 void fork_sort(sp_ctx* c) {
   SP_CUDA(cudaEventRecord(c->ev_fork, c->stream));
   SP_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-  stage_sort(c, c->vdevs[0], c->side, /*rebuild=*/true);
+  stage_sort(c, c->vdevs[0], c->side);
   SP_CUDA(cudaEventRecord(c->ev_join, c->side));
 }
 
 void join_sort(sp_ctx* c) { SP_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0)); }
 
-// Overlap mode 2: K1 runs sort group by sort group (canonical tile order),
-// emitting the group's sort pairs; each group's radix sort then runs on the
-// side stream under K1 of the next groups.
-void forward_pipelined(sp_ctx* c) {
-  VDev& v = c->vdevs[0];
-  for (size_t gi = 0; gi < v.groups.size(); ++gi) {
-    const SortGroup& g = v.groups[gi];
-    const int64_t k0 = v.tile_start[g.t0], k1 = v.tile_start[g.t1];
-    {
-      ProfScope prof(c, kProfFwd);
-      launch_tbe_forward(v.d_meta_canon, v.d_tiles_canon + k0, k1 - k0, c->B, v.d_off,
-                         v.d_idx, c->d_w, c->wt, v.d_pooled, c->d_rowmap, v.W, v.d_keys, v.d_bags, c->bags16,
-                         c->stream);
-    }
-    SP_CUDA(cudaEventRecord(c->ev_fork, c->stream));
-    SP_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-    ProfScope prof(c, kProfSort, c->side);
-    sort_pairs_of(c, v, g, c->side);
-  }
-  v.keys_valid = true;
-  SP_CUDA(cudaEventRecord(c->ev_join, c->side));
-}
-
 // Stage 1 of an iteration: the forward, with the backward sort forked onto
 // the side stream when the overlap is active.
 void forward_stage(sp_ctx* c, bool ov) {
-  if (ov && c->overlap_mode == 2) {
-    forward_pipelined(c);
-    return;
-  }
   if (ov) fork_sort(c);
   for (auto& v : c->vdevs) stage_forward(c, v);
 }
@@ -796,22 +564,17 @@ namespace {
 std::vector<uint32_t> sorted_keys_host(sp_ctx* c, VDev& v, uint32_t* bags) {
   std::vector<uint32_t> keys(v.nnz);
   if (v.nnz == 0) return keys;
-  if (v.bucketed) stage_backward_bucketed(c, v, c->d_kb, c->d_bb, false);
-  else stage_sort(c, v, c->stream);
+  stage_sort(c, v, c->stream);
   SP_CUDA(cudaMemcpyAsync(keys.data(), c->d_kb, v.nnz * 4, cudaMemcpyDeviceToHost, c->stream));
   std::vector<uint16_t> b16;
-  const bool narrow = c->bags16 && !v.bucketed;  // the CUB path sorts 16-bit bags
-  if (bags && narrow) {
+  if (bags && c->bags16) {
     b16.resize(v.nnz);
     SP_CUDA(cudaMemcpyAsync(b16.data(), c->d_bb, v.nnz * 2, cudaMemcpyDeviceToHost, c->stream));
   } else if (bags) {
     SP_CUDA(cudaMemcpyAsync(bags, c->d_bb, v.nnz * 4, cudaMemcpyDeviceToHost, c->stream));
   }
   SP_CUDA(cudaStreamSynchronize(c->stream));
-  if (bags && narrow) std::copy(b16.begin(), b16.end(), bags);
-  // keys are sort-group relative on the device
-  for (const SortGroup& g : v.groups)
-    for (int64_t p = g.p0; p < g.p1; ++p) keys[p] += static_cast<uint32_t>(g.row_base);
+  if (bags && c->bags16) std::copy(b16.begin(), b16.end(), bags);
   return keys;
 }
 }  // namespace
@@ -908,21 +671,6 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
       int lo = 0, hi = 0;
       SP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
       SP_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi));
-      const char* ss = std::getenv("SP_SORT_STREAMS");
-      // SP_SORT_STREAMS (default 4): sort groups run concurrently; CUB's
-      // onesweep passes are look-back latency-bound at ~22 warps/SM, so
-      // independent groups overlap (cfg3 isolated sort 1.10 -> 0.97 ms)
-      const int extra = std::max(0, std::min(7, (ss ? std::atoi(ss) : 4) - 1));
-      for (int k = 0; k < extra; ++k) {
-        cudaStream_t s2;
-        cudaEvent_t e2;
-        SP_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, hi));
-        SP_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
-        c->sort_st.push_back(s2);
-        c->ev_sjoin.push_back(e2);
-        c->sort_temp.push_back(nullptr);
-      }
-      if (extra > 0) SP_CUDA(cudaEventCreateWithFlags(&c->ev_sfork, cudaEventDisableTiming));
     }
     SP_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     SP_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
@@ -996,32 +744,11 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
       for (int i = 0; i < num_tables; ++i)
         if (placement[i] == d) v.tables.push_back(i);
       const int T = static_cast<int>(v.tables.size());
-      const std::vector<int> group_end =
-          plan_sort_groups(tables, v.tables, batch_size, static_cast<int>(c->sort_st.size()) + 1);
-      size_t next_group = 0;
       int64_t lcol = 0;
-      uint64_t rb = 0;     // row base inside the current sort group
-      int64_t gbase = 0;   // rows of the device before the current group
-      int gstart = 0;
-      auto close_group = [&](int t1) {
-        SortGroup sg;
-        sg.t0 = gstart;
-        sg.t1 = t1;
-        sg.row_base = gbase;
-        sg.end_bit = 1;
-        while (sg.end_bit < 32 && (1ULL << sg.end_bit) < std::max<uint64_t>(rb, 2)) ++sg.end_bit;
-        v.groups.push_back(sg);
-        gbase += static_cast<int64_t>(rb);
-        rb = 0;
-        gstart = t1;
-      };
+      uint64_t rb = 0;  // device-wide row base (sort keys)
       for (int li = 0; li < T; ++li) {
         const int g = v.tables[li];
         const sp_table_spec& t = tables[g];
-        if (li > gstart && li == group_end[next_group]) {
-          close_group(li);
-          ++next_group;
-        }
         TableMeta m{};
         m.woff = c->woff[g];
         m.rows = t.hash_size;
@@ -1037,19 +764,14 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
         rb += static_cast<uint64_t>(t.hash_size);
         if (rb > 0xffffffffULL)
           raise(SP_ERR_BAD_INPUT, "rows per device above 2^32 (32-bit sort keys)");
-        v.rb_end.push_back(static_cast<uint32_t>(rb));
       }
-      if (T > 0) close_group(T);
       v.W = lcol;
-      v.rows_total = gbase;
-      v.end_bit = 1;
-      for (const SortGroup& sg : v.groups) v.end_bit = std::max(v.end_bit, sg.end_bit);
+      v.rows_total = static_cast<int64_t>(rb);
       // K1 grid order, each table a contiguous block range: by weight
       // (pf * dim) interleaved heaviest / lightest / 2nd heaviest / ... so
       // the tables in flight together mix large and small row footprints in
       // L2 (cfg3 iteration 4.13 -> 4.08 ms vs heaviest-first; canonical
-      // order 4.10). SP_FWD_ORDER: 0 heaviest first, 1 canonical, 2 (default)
-      // interleaved, 3 interleaved by rows * dim.
+      // order 4.10; profiles/r01_notes.md).
       std::vector<int> order(T);
       std::iota(order.begin(), order.end(), 0);
       std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
@@ -1058,26 +780,12 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
         return ta.pooling_factor * ta.dim > tb.pooling_factor * tb.dim;
       });
       {
-        const char* fo = std::getenv("SP_FWD_ORDER");  // read per context
-        const int mode = fo ? std::atoi(fo) : 2;
-        auto interleave = [&](std::vector<int> o) {  // o[0], o[n-1], o[1], o[n-2], ...
-          std::vector<int> r;
-          for (size_t i = 0, j = o.size(); i < j;) {
-            r.push_back(o[i++]);
-            if (i < j) r.push_back(o[--j]);
-          }
-          return r;
-        };
-        if (mode == 1) std::iota(order.begin(), order.end(), 0);
-        if (mode == 2) order = interleave(order);
-        if (mode == 3) {
-          std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-            const auto& ta = tables[v.tables[a]];
-            const auto& tb = tables[v.tables[b]];
-            return double(ta.hash_size) * ta.dim > double(tb.hash_size) * tb.dim;
-          });
-          order = interleave(order);
+        std::vector<int> r;  // o[0], o[n-1], o[1], o[n-2], ...
+        for (size_t i = 0, j = order.size(); i < j;) {
+          r.push_back(order[i++]);
+          if (i < j) r.push_back(order[--j]);
         }
+        order = r;
       }
       const std::vector<int4> tiles = make_fwd_tiles(v.meta_canon, order, batch_size);
       v.n_tiles = static_cast<int64_t>(tiles.size());
@@ -1095,16 +803,11 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
         v.tile_start.assign(T + 1, 0);
         for (const int4& tl : ct) ++v.tile_start[tl.x + 1];
         for (int li = 0; li < T; ++li) v.tile_start[li + 1] += v.tile_start[li];
-        v.group_of_table.assign(T, 0);
-        for (size_t gi = 0; gi < v.groups.size(); ++gi)
-          for (int li = v.groups[gi].t0; li < v.groups[gi].t1; ++li) v.group_of_table[li] = gi;
       }
       v.d_meta_canon = dalloc<TableMeta>(T, c->owned, c->dev_bytes);
-      v.d_rb_end = dalloc<uint32_t>(T, c->owned, c->dev_bytes);
       v.d_colmap = dalloc<int32_t>(v.W, c->owned, c->dev_bytes);
       if (T) {
         SP_CUDA(cudaMemcpy(v.d_meta_canon, v.meta_canon.data(), T * sizeof(TableMeta), cudaMemcpyHostToDevice));
-        SP_CUDA(cudaMemcpy(v.d_rb_end, v.rb_end.data(), T * sizeof(uint32_t), cudaMemcpyHostToDevice));
       }
       if (v.W)
         SP_CUDA(cudaMemcpy(v.d_colmap, v.colmap.data(), v.W * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -1127,21 +830,12 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
       c->d_recv = dalloc<float>(c->n_dst * R * c->W_total, c->owned, c->dev_bytes);
       c->d_gin = dalloc<float>(c->n_dst * R * c->W_total, c->owned, c->dev_bytes);
     }
-    c->d_nseg = dalloc<int32_t>(1, c->owned, c->dev_bytes);
     c->d_flag = dalloc<int32_t>(1, c->owned, c->dev_bytes);
     c->d_bd = dalloc<double>(8 * static_cast<int64_t>(num_devices), c->owned, c->dev_bytes);
     c->d_barrier = dalloc<int32_t>(1, c->owned, c->dev_bytes);
     SP_CUDA(cudaMemset(c->d_barrier, 0, sizeof(int32_t)));
     for (auto& e : c->ev_a2a) SP_CUDA(cudaEventCreate(&e));
-    if (const char* f = std::getenv("SP_FUSE_KEYS")) c->fuse_keys = std::atoi(f) != 0;
-    if (const char* f = std::getenv("SP_BWD")) c->use_buckets = std::string(f) == "bucket";
-    if (const char* f = std::getenv("SP_OVERLAP")) {
-      c->overlap_sort = std::atoi(f) != 0;
-      if (std::atoi(f) == 1 || std::atoi(f) == 2) c->overlap_mode = std::atoi(f);
-    }
-    if (const char* f = std::getenv("SP_UPLOAD_CHUNK"))
-      c->upload_chunk = std::max<int64_t>(1, std::atoll(f));
-
+    for (auto& v : c->vdevs) plan_sort(c.get(), v);
     if (world_size > 1) {
       c->plan = make_plan(tables, num_tables, num_devices, placement, batch_size, rank);
       if (nccl_id != nullptr) {
@@ -1228,9 +922,10 @@ int sp_ctx_device_bytes(sp_ctx* ctx, uint64_t* bytes) {
   return guarded([&] {
     check_ctx(ctx);
     uint64_t b = ctx->dev_bytes;
-    b += ctx->sort_cap * 4 * 3 + ctx->temp_bytes * (1 + ctx->sort_temp.size()) +
-         ctx->stage_cap * 8;
-    for (auto& v : ctx->vdevs) b += v.idx_cap * 12;
+    b += ctx->sort_cap * 4 * 2 + ctx->stage_cap * 8;
+    for (auto& v : ctx->vdevs)
+      b += v.idx_cap * 4 + v.mid_cap * 2 * sort_mid_bytes(v.splan) +
+           (v.splan.n_cnt + v.splan.n_bstart) * 4;
     *bytes = b;
   });
 }
@@ -1304,8 +999,7 @@ int sp_get_table(sp_ctx* ctx, int32_t table_id, float* rows) {
   });
 }
 
-// Layout metadata of the current batch (sort-group positions on the host,
-// SGD tiles on the device). The tiles go through the pinned buffer of `slot`
+// Layout metadata of the current batch (SGD tiles on the device). The tiles go through the pinned buffer of `slot`
 // on the copy stream, ahead of the batch's H2D and into the slot's own
 // device buffer, so a step's upload never queues behind the previous step's
 // compute (a pageable or compute-stream copy would).
@@ -1338,12 +1032,6 @@ static void finish_batch(sp_ctx* c, int slot = 0, bool pipelined = false) {
   for (size_t vi = 0; vi < c->vdevs.size(); ++vi) {
     VDev& v = c->vdevs[vi];
     max_nnz = std::max(max_nnz, v.nnz);
-    int64_t p = 0;  // positions of each sort group in the device CSR
-    for (SortGroup& g : v.groups) {
-      g.p0 = p;
-      for (int t = g.t0; t < g.t1; ++t) p += v.table_nnz[t];
-      g.p1 = p;
-    }
     const std::vector<int>& tl = tiles[vi];
     v.n_sgd_tiles = static_cast<int64_t>(tl.size()) / kSgdTileInts;
     const int64_t wide = v.sgd_counts[1];
@@ -1377,7 +1065,6 @@ static void finish_batch(sp_ctx* c, int slot = 0, bool pipelined = false) {
   SP_CUDA(cudaEventRecord(c->meta_ready, c->copy_stream));
   SP_CUDA(cudaStreamWaitEvent(c->stream, c->meta_ready, 0));
   ensure_sort_capacity(c, max_nnz);
-  plan_buckets(c);
   c->has_batch = true;
   if (c->graph_exec) {
     cudaGraphExecDestroy(c->graph_exec);
@@ -1390,19 +1077,15 @@ static void alloc_indices(sp_ctx* c, VDev& v, int64_t nnz) {
     raise(SP_ERR_BAD_INPUT, "more than 2^31-1 lookups on one device (int32 CSR)");
   if (nnz > v.idx_cap || v.d_idx == nullptr) {
     SP_CUDA(cudaStreamSynchronize(c->stream));
-    for (void* p : {static_cast<void*>(v.d_idx), static_cast<void*>(v.d_keys),
-                     static_cast<void*>(v.d_bags)})
-      if (p) cudaFree(p);
+    if (c->side) SP_CUDA(cudaStreamSynchronize(c->side));
+    if (v.d_idx) cudaFree(v.d_idx);
     v.d_idx = nullptr;
-    v.d_keys = v.d_bags = nullptr;
     const int64_t cap = std::max<int64_t>(nnz, 1);
     SP_CUDA(cudaMalloc(&v.d_idx, cap * sizeof(int32_t)));
-    SP_CUDA(cudaMalloc(&v.d_keys, cap * sizeof(uint32_t)));
-    SP_CUDA(cudaMalloc(&v.d_bags, cap * sizeof(uint32_t)));
     v.idx_cap = cap;
   }
+  ensure_mid(c, v);
   v.nnz = nnz;
-  v.keys_valid = false;
 }
 
 }  // extern "C"
@@ -1471,7 +1154,7 @@ cudaEvent_t upload_event(sp_ctx* c, size_t& n_ev) {
 // Coalesced, pipelined H2D of a host LookupBatch: local tables with
 // consecutive global ids are adjacent in the reference CSR, so each such run
 // is copied with two large memcpys, cut into chunks of <= kUploadChunk
-// indices (never straddling a sort group) on the copy stream while the
+// indices on the copy stream while the
 // compute stream narrows the previous chunk to the int32 device CSR (and
 // flags malformed data in d_flag, clamping it so later kernels stay in
 // bounds). chunk_done(v, t0, t1) runs after the narrows of local tables
@@ -1503,8 +1186,7 @@ void enqueue_upload_from(sp_ctx* c, const int64_t* offsets, CopyIdx&& copy_idx, 
       while (c0 < run_end) {
         int c1 = c0 + 1;
         int64_t acc = v.table_nnz[c0];
-        while (c1 < run_end && acc + v.table_nnz[c1] <= kUploadChunk &&
-               v.group_of_table[c1] == v.group_of_table[c0])
+        while (c1 < run_end && acc + v.table_nnz[c1] <= kUploadChunk)
           acc += v.table_nnz[c1++];
         const int64_t g0 = v.tables[c0], g1 = v.tables[c1 - 1] + 1;
         const int64_t n_off = (g1 - g0) * B + 1;
@@ -2013,7 +1695,7 @@ namespace sp {
 namespace {
 
 // One host-buffer step, enqueued: upload (slot, flag) pipelined with K1 per
-// chunk and the per-group backward sorts, then stages 2-4 with the SGD
+// chunk and each chunk's backward sort, then stages 2-4 with the SGD
 // guarded by the step's validation flag. Events ev[0..7] time its stages.
 void enqueue_batch_step(sp_ctx* c, const int64_t* offsets, const int64_t* indices,
                         int32_t* flag, int slot, bool pipelined = false) {
@@ -2026,31 +1708,19 @@ void enqueue_batch_step(sp_ctx* c, const int64_t* offsets, const int64_t* indice
       c, offsets, indices,
       [&](VDev& v, int t0, int t1) {
         const int64_t k0 = v.tile_start[t0], k1 = v.tile_start[t1];
-        const bool emit = ov ? c->overlap_mode == 2 : (c->fuse_keys && !v.bucketed);
         {
           ProfScope prof(c, kProfFwd);
           launch_tbe_forward(v.d_meta_canon, v.d_tiles_canon + k0, k1 - k0, c->B, v.d_off,
-                             v.d_idx, c->d_w, c->wt, v.d_pooled, c->d_rowmap, v.W,
-                             emit ? v.d_keys : nullptr, emit ? v.d_bags : nullptr, c->bags16,
-                             st);
+                             v.d_idx, c->d_w, c->wt, v.d_pooled, c->d_rowmap, v.W, st);
         }
-        if (t1 == static_cast<int>(v.tables.size())) {
-          v.keys_valid = emit;
-          SP_CUDA(cudaEventRecord(v.ev[1], st));
-        }
-        const int g = v.group_of_table[t1 - 1];
-        if (ov && v.groups[g].t1 == t1) {
-          // the group's CSR is on the device: sort it on the side stream
+        const bool last = t1 == static_cast<int>(v.tables.size());
+        if (last) SP_CUDA(cudaEventRecord(v.ev[1], st));
+        if (ov) {
+          // the chunk's CSR is on the device: sort its tables on the side stream
           SP_CUDA(cudaEventRecord(c->ev_fork, st));
           SP_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-          if (c->overlap_mode == 2) {
-            ProfScope prof(c, kProfSort, c->side);
-            sort_pairs_of(c, v, v.groups[g], c->side);
-          } else {
-            sort_group(c, v, g, c->side);
-          }
-          if (g + 1 == static_cast<int>(v.groups.size()))
-            SP_CUDA(cudaEventRecord(c->ev_join, c->side));
+          sort_range(c, v, t0, t1, c->side);
+          if (last) SP_CUDA(cudaEventRecord(c->ev_join, c->side));
         }
       },
       flag, slot);
@@ -2069,7 +1739,7 @@ extern "C" {
 // The reference-facing step with host buffers: the LookupBatch's H2D is
 // pipelined with the forward (K1 runs on each uploaded chunk of tables while
 // the next chunk is in flight) and, with one (virtual) device, with the
-// backward sort of every completed sort group; the device-side validation
+// backward sort of every uploaded chunk; the device-side validation
 // (offsets monotone inside a table, indices in range) is checked at the end
 // and, if it failed, the SGD never touched the tables (device-side abort
 // flag) and the call raises like sp_upload_batch.
@@ -2227,6 +1897,29 @@ int sp_ctx_set_overlap(sp_ctx* ctx, int32_t on) {
   });
 }
 
+int sp_ctx_set_sort_target(sp_ctx* ctx, int64_t lookups) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (lookups < 0) raise(SP_ERR_BAD_INPUT, "sort target must be >= 0");
+    SP_CUDA(cudaStreamSynchronize(ctx->stream));
+    SP_CUDA(cudaStreamSynchronize(ctx->side));
+    ctx->sort_target = lookups;
+    for (auto& v : ctx->vdevs) plan_sort(ctx, v);
+    if (ctx->graph_exec) {
+      cudaGraphExecDestroy(ctx->graph_exec);
+      ctx->graph_exec = nullptr;
+    }
+  });
+}
+
+int sp_ctx_set_upload_chunk(sp_ctx* ctx, int64_t indices) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (indices < 1) raise(SP_ERR_BAD_INPUT, "upload chunk must be >= 1 index");
+    ctx->upload_chunk = indices;
+  });
+}
+
 int sp_ctx_set_profiling(sp_ctx* ctx, int32_t on) {
   return guarded([&] {
     check_ctx(ctx);
@@ -2258,14 +1951,13 @@ int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]) {
     sp_ctx* c = ctx;
     // Max over the (virtual) devices held here; SURVEY §8d formulas, 4-byte
     // ids, per launch of each kernel as this build runs it:
-    //  [0] K1: offsets + ids + gathered rows + pooled out (+ 8 B/lookup of
-    //      sort pairs when K1 emits them for the CUB path)
+    //  [0] K1: offsets + ids + gathered rows + pooled out
     //  [1] exchange sent per direction
-    //  [2] K4 SGD kernel: gradient 4*B*W + touched rows read+write
-    //      8*sum_unique dim + the pairs it reads (8 B/lookup, the bucketed
-    //      kernel also re-reads rows for its histogram: +4 B)
-    //  [3] sort / partition: CUB 16 B/lookup/pass; bucketed: ids twice +
-    //      pair write (8+8 B/lookup) + offsets
+    //  [2] K4b SGD kernel: gradient 4*B*W + touched rows read+write
+    //      8*sum_unique dim (2 B/param tables: 4*) + the sorted pairs it reads
+    //  [3] K4a sort: ids read twice (8 B/lookup), packed pairs written and
+    //      read (4 B each, 8 B when wide), sorted key + bag written, offsets
+    //      read twice, count matrix written, scanned (read + write) and read
     // (row bytes use the storage type: 2 B/param for fp16 tables)
     double fwd = 0, a2a = 0, sgd = 0, sort = 0;
     const double eb = elem_bytes(c->wt);
@@ -2277,16 +1969,15 @@ int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]) {
       const double offs = 4.0 * (static_cast<double>(T) * c->B + 1);
       const double csr = offs + 4.0 * v.nnz;
       const double outb = 4.0 * c->B * v.W;
-      const bool emit = overlap_active(c) ? c->overlap_mode == 2 : (c->fuse_keys && !v.bucketed);
-      const double pair = c->bags16 ? 6.0 : 8.0;  // sort key + bag payload bytes
-      fwd = std::max(fwd, csr + rows_bytes + outb + (emit ? pair * v.nnz : 0.0));
+      const double pair = c->bags16 ? 6.0 : 8.0;  // sorted key + bag payload bytes
+      const double mid = static_cast<double>(sort_mid_bytes(v.splan));
+      fwd = std::max(fwd, csr + rows_bytes + outb);
       a2a = std::max(a2a, 4.0 * c->B * v.W * (c->D - 1) / c->D);
       double uniq_dim = 0;
       {
         const std::vector<uint32_t> keys = sorted_keys_host(c, v, nullptr);
         std::vector<uint64_t> row_end;  // device-wide end row of each local table
-        for (const SortGroup& g : v.groups)
-          for (int t = g.t0; t < g.t1; ++t) row_end.push_back(g.row_base + v.rb_end[t]);
+        for (const TableMeta& m : v.meta_canon) row_end.push_back(m.rowbase + m.rows);
         for (size_t p = 0; p < keys.size(); ++p)
           if (p == 0 || keys[p] != keys[p - 1]) {
             const int li = static_cast<int>(
@@ -2294,13 +1985,9 @@ int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]) {
             uniq_dim += c->tables[v.tables[li]].dim;
           }
       }
-      sgd = std::max(sgd, outb + 2.0 * eb * uniq_dim + (v.bucketed ? 12.0 : pair) * v.nnz);
-      double sort_dev = 0;
-      if (v.bucketed)
-        sort_dev = 2.0 * csr + 8.0 * v.nnz + 8.0 * v.n_cnt;
-      else
-        for (const SortGroup& g : v.groups)
-          sort_dev += 2.0 * pair * (g.p1 - g.p0) * ((g.end_bit + 7) / 8);
+      sgd = std::max(sgd, outb + 2.0 * eb * uniq_dim + pair * v.nnz);
+      const double sort_dev = 2.0 * csr + 2.0 * mid * v.nnz + pair * v.nnz +
+                              4.0 * 4.0 * static_cast<double>(v.splan.n_cnt);
       sort = std::max(sort, sort_dev);
     }
     out[0] = fwd;

@@ -351,26 +351,17 @@ __device__ __forceinline__ void fwd_tile_warp_generic(
   }
 }
 
-// BagT: the sort payload — uint16_t when the batch fits 16 bits (6-byte
-// pairs through the radix sort instead of 8), else uint32_t.
 #ifndef SP_FWD_STAGED
 #define SP_FWD_STAGED 1
 #endif
-#ifdef SP_FWD_MIN_BLOCKS  // A/B builds; default: ptxas' own choice (32 registers)
-#define SP_FWD_BOUNDS __launch_bounds__(kBlockThreads, SP_FWD_MIN_BLOCKS)
-#else
-#define SP_FWD_BOUNDS __launch_bounds__(kBlockThreads)
-#endif
-template <bool kEmitKeys, class BagT, bool kPeer, class T>
-__global__ void SP_FWD_BOUNDS
+template <bool kPeer, class T>
+__global__ void __launch_bounds__(kBlockThreads)
     tbe_forward_kernel(const TableMeta* __restrict__ meta,
                        const FwdTile* __restrict__ tiles, int batch,
                        const int32_t* __restrict__ off,
                        const int32_t* __restrict__ idx,
                        const T* __restrict__ w, float* __restrict__ out,
-                       const RowMap* __restrict__ peer,
-                       int64_t ldo, uint32_t* __restrict__ keys,
-                       BagT* __restrict__ bags) {
+                       const RowMap* __restrict__ peer, int64_t ldo) {
   __shared__ int32_t s_off[kFwdTileBags + 1];
   __shared__ int32_t s_idx[kIdxCap];
   const FwdTile tile = tiles[blockIdx.x];
@@ -380,20 +371,7 @@ __global__ void SP_FWD_BOUNDS
   __syncthreads();
   const int p0 = s_off[0];
   const int np = s_off[tile.nb] - p0;
-  for (int i = threadIdx.x; i < np; i += kBlockThreads) {
-    const int32_t v = __ldg(idx + p0 + i);
-    if (i < kIdxCap) s_idx[i] = v;
-    if (kEmitKeys) {
-      // bag of position i: last j with s_off[j] <= p0 + i
-      int lo = 0, hi = tile.nb - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_off[mid] <= p0 + i) lo = mid; else hi = mid - 1;
-      }
-      __stcs(keys + p0 + i, m.rowbase + static_cast<uint32_t>(v));
-      bags[p0 + i] = static_cast<BagT>(tile.b0 + lo);
-    }
-  }
+  for (int i = threadIdx.x; i < min(np, kIdxCap); i += kBlockThreads) s_idx[i] = __ldg(idx + p0 + i);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   switch (m.cls) {
@@ -422,44 +400,6 @@ __global__ void SP_FWD_BOUNDS
   // against the receivers' reads
   if (kPeer) __threadfence_system();
 }
-
-// ---------------------------------------------------------------------------
-// K4 step 1 (only when K1 did not emit them): keys[p] = rowbase + idx[p],
-// bags[p] = bag of p. A block takes 256 bags of one table.
-
-template <class BagT>
-__global__ void __launch_bounds__(kTileBags)
-    build_keys_kernel(const TableMeta* __restrict__ meta, int batch,
-                      int tiles_per_table, const int32_t* __restrict__ off,
-                      const int32_t* __restrict__ idx,
-                      uint32_t* __restrict__ keys, BagT* __restrict__ bags) {
-  __shared__ int32_t s_off[kTileBags + 1];
-  const int t = blockIdx.x / tiles_per_table;
-  const int tile = blockIdx.x % tiles_per_table;
-  const int b0 = tile * kTileBags;
-  const int nb = min(kTileBags, batch - b0);
-  const TableMeta m = meta[t];
-  const int64_t base = static_cast<int64_t>(m.local) * batch + b0;
-  for (int i = threadIdx.x; i <= nb; i += blockDim.x) s_off[i] = off[base + i];
-  __syncthreads();
-  const int p0 = s_off[0], p1 = s_off[nb];
-  for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-    int lo = 0, hi = nb - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_off[mid] <= p) lo = mid; else hi = mid - 1;
-    }
-    keys[p] = m.rowbase + static_cast<uint32_t>(__ldg(idx + p));
-    bags[p] = static_cast<BagT>(b0 + lo);
-  }
-}
-
-struct HeadFlag {
-  const uint32_t* keys;
-  __device__ __forceinline__ bool operator()(const uint32_t& k) const {
-    return k == 0 || keys[k] != keys[k - 1];
-  }
-};
 
 // ---------------------------------------------------------------------------
 // K4 step 3: row-wise SGD over the sorted (key, bag) pairs.
@@ -1241,26 +1181,15 @@ std::vector<int4> make_fwd_tiles(const std::vector<TableMeta>& canon,
 void launch_tbe_forward(const TableMeta* d_meta_canon, const int4* d_tiles,
                         int64_t n_tiles, int batch, const int32_t* d_off,
                         const int32_t* d_idx, const void* d_w, WeightType wt, float* d_out,
-                        const RowMap* d_peer, int64_t ldo, uint32_t* d_keys, void* d_bags,
-                        bool bags16, cudaStream_t st) {
+                        const RowMap* d_peer, int64_t ldo, cudaStream_t st) {
   if (n_tiles <= 0) return;
   const FwdTile* tiles = reinterpret_cast<const FwdTile*>(d_tiles);
   const unsigned g = static_cast<unsigned>(n_tiles);
   auto go = [&](auto peer, auto elem) {
     constexpr bool kPeer = decltype(peer)::value;
     using T = typename decltype(elem)::type;
-    const T* w = static_cast<const T*>(d_w);
-    if (!d_keys)
-      tbe_forward_kernel<false, uint32_t, kPeer, T><<<g, kBlockThreads, 0, st>>>(
-          d_meta_canon, tiles, batch, d_off, d_idx, w, d_out, d_peer, ldo, nullptr, nullptr);
-    else if (bags16)
-      tbe_forward_kernel<true, uint16_t, kPeer, T><<<g, kBlockThreads, 0, st>>>(
-          d_meta_canon, tiles, batch, d_off, d_idx, w, d_out, d_peer, ldo, d_keys,
-          static_cast<uint16_t*>(d_bags));
-    else
-      tbe_forward_kernel<true, uint32_t, kPeer, T><<<g, kBlockThreads, 0, st>>>(
-          d_meta_canon, tiles, batch, d_off, d_idx, w, d_out, d_peer, ldo, d_keys,
-          static_cast<uint32_t*>(d_bags));
+    tbe_forward_kernel<kPeer, T><<<g, kBlockThreads, 0, st>>>(
+        d_meta_canon, tiles, batch, d_off, d_idx, static_cast<const T*>(d_w), d_out, d_peer, ldo);
   };
   using F32 = TypeTag<float>;
   using F16 = TypeTag<__half>;
@@ -1272,45 +1201,6 @@ void launch_tbe_forward(const TableMeta* d_meta_canon, const int4* d_tiles,
     else go(std::false_type{}, F32{});
   }
   SP_LAUNCHED();
-}
-
-void launch_build_keys(const TableMeta* d_meta_canon, int n_tables, int batch,
-                       const int32_t* d_off, const int32_t* d_idx,
-                       uint32_t* d_keys, void* d_bags, bool bags16, cudaStream_t st) {
-  if (n_tables <= 0) return;
-  const int tiles = (batch + kTileBags - 1) / kTileBags;
-  if (bags16)
-    build_keys_kernel<uint16_t><<<n_tables * tiles, kTileBags, 0, st>>>(
-        d_meta_canon, batch, tiles, d_off, d_idx, d_keys, static_cast<uint16_t*>(d_bags));
-  else
-    build_keys_kernel<uint32_t><<<n_tables * tiles, kTileBags, 0, st>>>(
-        d_meta_canon, batch, tiles, d_off, d_idx, d_keys, static_cast<uint32_t*>(d_bags));
-  SP_LAUNCHED();
-}
-
-size_t sort_pairs(void* temp, size_t temp_bytes, const uint32_t* keys_in,
-                  uint32_t* keys_out, const void* vals_in, void* vals_out, bool bags16,
-                  int64_t n, int end_bit, cudaStream_t st) {
-  size_t bytes = temp_bytes;
-  if (bags16)
-    SP_CUDA(cub::DeviceRadixSort::SortPairs(temp, bytes, keys_in, keys_out,
-                                            static_cast<const uint16_t*>(vals_in),
-                                            static_cast<uint16_t*>(vals_out), n, 0, end_bit, st));
-  else
-    SP_CUDA(cub::DeviceRadixSort::SortPairs(temp, bytes, keys_in, keys_out,
-                                            static_cast<const uint32_t*>(vals_in),
-                                            static_cast<uint32_t*>(vals_out), n, 0, end_bit, st));
-  return bytes;
-}
-
-size_t select_heads(void* temp, size_t temp_bytes, const uint32_t* d_keys,
-                    int64_t n, uint32_t* d_seg, int32_t* d_nseg,
-                    cudaStream_t st) {
-  size_t bytes = temp_bytes;
-  cub::CountingInputIterator<uint32_t> it(0);
-  SP_CUDA(cub::DeviceSelect::If(temp, bytes, it, d_seg, d_nseg, n,
-                                HeadFlag{d_keys}, st));
-  return bytes;
 }
 
 size_t exclusive_scan_i32(void* temp, size_t temp_bytes, const int32_t* in,

@@ -17,7 +17,7 @@ struct TableMeta {
   int64_t reserved;
   int32_t dim;
   int32_t lcol;         // first column in the local pooled [B, W_local]
-  uint32_t rowbase;     // K4 key base: sum of rows of earlier local tables
+  uint32_t rowbase;     // K4 key base: rows of the earlier local tables (device-wide)
   int32_t cls;          // dim class, see dim_class(); -1 = generic path
   int32_t local;        // canonical local index (ascending global id)
   int32_t gid;          // global table id
@@ -66,8 +66,6 @@ constexpr int kBlockThreads = 32 * kWarpsPerBlock;
 // One launch over all local tables; a block per tile of <= 256 bags of one
 // table: out[b, lcol_t : lcol_t + dim_t] =
 //   sum_{p in [off[i*B+b], off[i*B+b+1])} W_t[idx[p], :]   (int32 CSR).
-// With d_keys != nullptr also writes the backward's sort pairs
-// keys[p] = rowbase_i + idx[p], bags[p] = b.
 // Tiles (x = canonical table, y = first bag, z = bag count) in launch order.
 //
 // Where the pooled rows go: d_peer == nullptr -> the local pooled buffer
@@ -87,26 +85,52 @@ std::vector<int4> make_fwd_tiles(const std::vector<TableMeta>& canon,
 void launch_tbe_forward(const TableMeta* d_meta_canon, const int4* d_tiles,
                         int64_t n_tiles, int batch, const int32_t* d_off,
                         const int32_t* d_idx, const void* d_w, WeightType wt, float* d_out,
-                        const RowMap* d_peer, int64_t ldo, uint32_t* d_keys, void* d_bags,
-                        bool bags16, cudaStream_t st);
+                        const RowMap* d_peer, int64_t ldo, cudaStream_t st);
 
-// ---- K4: backward = keys -> stable radix sort -> runs -> SGD -------------
-void launch_build_keys(const TableMeta* d_meta_canon, int n_tables, int batch,
-                       const int32_t* d_off, const int32_t* d_idx,
-                       uint32_t* d_keys, void* d_bags, bool bags16, cudaStream_t st);
-// Run heads of sorted keys (test/diagnostic path; the SGD kernel finds the
-// heads itself): seg[u] = first position of the u-th run, *d_nseg = runs.
-size_t select_heads(void* temp, size_t temp_bytes, const uint32_t* d_keys,
-                    int64_t n, uint32_t* d_seg, int32_t* d_nseg,
-                    cudaStream_t st);
-// vals are uint16_t (bags16: batch <= 65536) or uint32_t bag ids.
-size_t sort_pairs(void* temp, size_t temp_bytes, const uint32_t* keys_in,
-                  uint32_t* keys_out, const void* vals_in, void* vals_out, bool bags16,
-                  int64_t n, int end_bit, cudaStream_t st);
+// ---- K4a: stable sort of a device's lookups by (table, row) (sort.cu) ----
+// Per local table: rows split into nb buckets of 2^lo rows, bags into nwt
+// tiles of wb bags; cnt[cbase + tile*nb + bucket] is the count matrix,
+// bstart[bkbase + bucket] the bucket starts (+ one table-end slot).
+struct SortTable {
+  int32_t lo;        // row bits inside a bucket
+  int32_t nb;        // buckets: ceil(rows / 2^lo) (<= 1024)
+  int32_t wb;        // bags per tile
+  int32_t nwt;       // tiles: ceil(B / wb)
+  int64_t cbase;     // first count of the table
+  int32_t bkbase;    // first bucket-start slot of the table
+  uint32_t rowbase;  // key base of the table (device-wide)
+  int32_t db;        // digit bits per pass of the in-bucket sort (<= 10)
+  int32_t pad;
+};
+struct SortPlan {
+  std::vector<SortTable> tabs;
+  std::vector<int2> wtiles;            // (table, tile), tables in order
+  std::vector<int2> bkts;              // (table, bucket), tables in order
+  std::vector<int64_t> wt_start, bk_start;  // per table (+ end)
+  int64_t n_cnt = 0;
+  int32_t n_bstart = 0;
+  bool wide_mid = false;  // 8-byte packed intermediates (32-bit bags or > 16 low row bits)
+};
+// est_nnz: expected lookups per table; target > 0 forces the bucket and
+// tile size in lookups (tests), 0 = the default plan.
+SortPlan sort_plan(const std::vector<TableMeta>& canon, const std::vector<double>& est_nnz,
+                   int batch, int64_t target, bool bags16);
+// Bytes of one packed intermediate (d_mid holds 2 * mid_cap of them: the
+// pairs, then the scratch of buckets too large for shared memory).
+size_t sort_mid_bytes(const SortPlan& pl);
+// Sorts the lookups of local tables [t0, t1) into keys/bags at their CSR
+// positions (keys = rowbase + row, ties in position order: std::stable_sort).
+// d_big / d_nbig: scratch list of the large buckets (bkts.size() entries).
+void launch_sort(const SortPlan& pl, const SortTable* d_tabs, const int2* d_tiles,
+                 const int2* d_bkts, int t0, int t1, int batch, const int32_t* d_off,
+                 const int32_t* d_idx, int* d_cnt, int* d_bstart, int2* d_big, int* d_nbig,
+                 void* d_mid, int64_t mid_cap, uint32_t* d_keys, void* d_bags, bool bags16,
+                 cudaStream_t st);
+
+// ---- K4b: row-wise SGD over the sorted pairs -------------------------------
 // Row-wise SGD over the sorted pairs:
 // W[row] -= lr * sum_{k in run, sorted order} grad[bags[k], lcol..].
-// Keys are relative to their sort group (the table's rowbase is too); the
-// sorted lookups of local table t occupy its CSR position range, so the
+// Keys are device-wide (rowbase + row); the sorted lookups of local table t occupy its CSR position range, so the
 // launch runs over per-table tiles (make_sgd_tiles: kSgdTileInts ints each,
 // from the per-table lookup counts in canonical order).
 constexpr int kSgdTileInts = 8;

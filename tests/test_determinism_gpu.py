@@ -1,8 +1,8 @@
-"""Scheduling knobs never change results: the K1 launch order of tables
-(SP_FWD_ORDER), the number of concurrent sort streams (SP_SORT_STREAMS) and
-the sort-group split, and the overlapped vs serial sort (SP_OVERLAP) all give
-bit-identical pooled rows, sorted pairs and updated tables — every reduction
-has a fixed order that does not depend on which block or stream runs it."""
+"""Scheduling choices never change results: the K4a sort plan (bucket width
+and warp-tile size, sp_ctx_set_sort_target), the overlapped vs serial sort
+(sp_ctx_set_overlap) and repeated runs all give bit-identical pooled rows,
+sorted pairs and updated tables — every reduction has a fixed order that does
+not depend on which block or stream runs it."""
 import numpy as np
 import pytest
 
@@ -16,14 +16,14 @@ B = 128
 DIMS = [16, 32, 64, 128, 16, 64, 8, 128, 32, 4]
 
 
-def _run(monkeypatch, env, D=1):
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+def _run(cfg, D=1):
     task, placement = random_task(404 + D, DIMS, D, B, rows_range=(50, 5000))
     weights = random_weights(17, task.tables)
     off, idx = orc.synth_batch(as_dicts(task.tables), B, seed=23)
     grad = np.random.default_rng(8).uniform(-1, 1, size=(B, sum(DIMS))).astype(np.float32)
     sh = EmbeddingShard(task, placement, lr=0.02)
+    sh.set_sort_target(cfg.get("target", 0))
+    sh.set_overlap(cfg.get("overlap", True))
     for i, w in enumerate(weights):
         sh.set_table(i, w)
     sh.upload_batch(LookupBatch(idx, off, len(DIMS), B))
@@ -32,8 +32,6 @@ def _run(monkeypatch, env, D=1):
     out = {"pooled": sh.pooled(), "tables": [sh.get_table(i) for i in range(len(DIMS))],
            "sorted": [sh.sorted(d) for d in range(D)]}
     sh.close()
-    for k in env:
-        monkeypatch.delenv(k, raising=False)
     return out
 
 
@@ -47,13 +45,12 @@ def _same(a, b):
 
 
 @pytest.mark.parametrize("D", [1, 4])
-def test_schedules_are_bit_identical(monkeypatch, D):
-    ref = _run(monkeypatch, {"SP_FWD_ORDER": "0", "SP_SORT_STREAMS": "1", "SP_OVERLAP": "0"}, D)
-    for env in ({},  # defaults: interleaved K1 order, 4 sort streams, overlap on
-                {"SP_FWD_ORDER": "1"}, {"SP_FWD_ORDER": "3", "SP_SORT_STREAMS": "8"},
-                {"SP_SORT_GROUP_ROWS": "3000", "SP_SORT_STREAMS": "4"},
-                {"SP_SORT_GROUP_ROWS": "3000", "SP_SORT_STREAMS": "1"}):
-        _same(ref, _run(monkeypatch, env, D))
+def test_schedules_are_bit_identical(D):
+    ref = _run({"overlap": False}, D)
+    for cfg in ({},  # defaults: planned buckets / tiles, overlap on
+                {}, {"target": 1}, {"target": 5, "overlap": False}, {"target": 40},
+                {"target": 100000}):
+        _same(ref, _run(cfg, D))
 
 
 def test_run_local_equals_stage_calls(monkeypatch):

@@ -51,8 +51,7 @@ def _shard(task, placement, weights, lr):
 
 
 @pytest.mark.parametrize("D", [1, 3])
-def test_upload_file_equals_upload_batch(tmp_path, D, monkeypatch):
-    monkeypatch.setenv("SP_UPLOAD_CHUNK", "500")  # many chunks / ring refills
+def test_upload_file_equals_upload_batch(tmp_path, D):
     B = 96
     dims = [16, 32, 64, 128, 16, 64, 12, 4]
     task, placement = random_task(50 + D, dims, D, B)
@@ -63,6 +62,7 @@ def test_upload_file_equals_upload_batch(tmp_path, D, monkeypatch):
     grad = np.random.default_rng(2).uniform(-1, 1, size=(B, sum(dims))).astype(np.float32)
     a = _shard(task, placement, weights, 0.03)
     b = _shard(task, placement, weights, 0.03)
+    a.set_upload_chunk(500)  # many chunks / ring refills
     a.upload_batch_file(path)
     b.upload_batch(LookupBatch(idx, off, len(dims), B))
     assert a.nnz == b.nnz == len(idx)

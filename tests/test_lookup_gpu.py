@@ -80,17 +80,16 @@ def test_forward_hand_case():
     np.testing.assert_array_equal(got, want)
 
 
-@pytest.fixture(params=["cub", "bucket"])
-def bwd_path(request, monkeypatch):
-    """Both backward implementations: CUB radix sort + tiled SGD (default)
-    and the bucketed counting sort fused with the SGD (SP_BWD=bucket)."""
-    monkeypatch.setenv("SP_BWD", request.param)
+@pytest.fixture(params=[0, 7])
+def sort_target(request):
+    """The default K4a sort plan, and one forced to buckets / warp-tiles of ~7
+    lookups (many buckets and tiles per table even at B = 64)."""
     return request.param
 
 
 @pytest.mark.parametrize("dims", list(DIM_SETS))
 @pytest.mark.parametrize("D", [1, 2])
-def test_backward_matches_oracle(dims, D, bwd_path):
+def test_backward_matches_oracle(dims, D, sort_target):
     B = 64
     task, placement = random_task(19 + D, DIM_SETS[dims], D, B, rows_range=(1, 200))
     weights = random_weights(3, task.tables)
@@ -99,6 +98,7 @@ def test_backward_matches_oracle(dims, D, bwd_path):
     grad = np.random.default_rng(4).uniform(-1, 1, size=(B, W)).astype(np.float32)
     lr = 0.05
     sh = _shard(task, placement, weights, lr=lr)
+    sh.set_sort_target(sort_target)
     sh.upload_batch(LookupBatch(idx, off, len(task.tables), B))
     sh.set_grad(grad)
     sh.a2a_backward()
@@ -119,13 +119,14 @@ def test_backward_matches_oracle(dims, D, bwd_path):
         np.testing.assert_allclose(sh.get_table(i), want[i], rtol=RTOL, atol=ATOL)
 
 
-def test_device_generator_matches_oracle(bwd_path):
+def test_device_generator_matches_oracle(sort_target):
     """sp_synth_batch / sp_init_tables / sp_synth_grad are bit-identical to the
     oracle generator: same sorted keys, same pooled sums, same update."""
     B = 128
     task, placement = random_task(23, [16, 32, 64, 128, 8], 2, B, rows_range=(500, 5000))
     seed = 2210
     sh = EmbeddingShard(task, placement, lr=0.01)
+    sh.set_sort_target(sort_target)
     sh.init_tables(seed)
     sh.synth_batch(seed)
     off, idx = orc.synth_batch(as_dicts(task.tables), B, seed)
@@ -206,7 +207,7 @@ def test_memory_cap_enforced():
     assert e.value.kind == "memory_violation" and e.value.exit_code == 2
 
 
-def test_hot_rows_and_empty_tables(bwd_path):
+def test_hot_rows_and_empty_tables(sort_target):
     """All-hot table (long duplicate runs), a never-accessed table (pf 0)."""
     B = 512
     tables = make_tables([32, 16, 128], [5000, 300, 70], [20.0, 0.0, 3.0], hot=[1.0, 0.0, 0.9])
@@ -217,6 +218,7 @@ def test_hot_rows_and_empty_tables(bwd_path):
     W = sum(t.dim for t in tables)
     grad = np.random.default_rng(2).uniform(-1, 1, size=(B, W)).astype(np.float32)
     sh = _shard(task, placement, weights, lr=0.001)
+    sh.set_sort_target(sort_target)
     sh.upload_batch(LookupBatch(idx, off, 3, B))
     sh.forward()
     sh.a2a_forward()
@@ -231,7 +233,7 @@ def test_hot_rows_and_empty_tables(bwd_path):
         np.testing.assert_allclose(sh.get_table(i), want[i], rtol=RTOL, atol=1e-4)
 
 
-def test_runs_spanning_many_sgd_tiles(bwd_path):
+def test_runs_spanning_many_sgd_tiles(sort_target):
     """Tables of 1-3 rows at B = 4096: every row's run covers thousands of
     sorted positions, i.e. dozens of segmented-SGD tiles (1024 positions),
     so the per-chunk partials and the cross-tile carries are all exercised;
@@ -244,6 +246,7 @@ def test_runs_spanning_many_sgd_tiles(bwd_path):
     off, idx = orc.synth_batch(as_dicts(tables), B, seed=31)
     grad = np.random.default_rng(5).uniform(-1, 1, size=(B, sum(dims))).astype(np.float32)
     sh = _shard(task, [0] * len(dims), weights, lr=0.001)
+    sh.set_sort_target(sort_target)
     sh.upload_batch(LookupBatch(idx, off, len(dims), B))
     sh.set_grad(grad)
     sh.run_iteration()

@@ -1,7 +1,7 @@
 """sp_run_batch — the pipelined upload + iteration with host buffers (the e2e
 path of bench.py) — against the CPU oracle and against the unpipelined
-upload_batch + run_iteration, including many upload chunks and sort groups
-(SP_UPLOAD_CHUNK / SP_SORT_GROUP_ROWS), and its deferred validation: a bad
+upload_batch + run_iteration, including many upload chunks, each sorted on its own
+(sp_ctx_set_upload_chunk) with many small sort buckets (sp_ctx_set_sort_target), and its deferred validation: a bad
 batch raises like upload_batch and leaves every table untouched."""
 import os
 
@@ -18,24 +18,24 @@ RTOL = 1e-5
 
 
 @pytest.fixture(params=["default", "chunked"])
-def chunking(request, monkeypatch):
-    if request.param == "chunked":
-        monkeypatch.setenv("SP_UPLOAD_CHUNK", "700")
-        monkeypatch.setenv("SP_SORT_GROUP_ROWS", "3000")
+def chunking(request):
     return request.param
 
 
-def _shard(task, placement, weights, lr):
+def _shard(task, placement, weights, lr, chunking="default", overlap=True):
     sh = EmbeddingShard(task, placement, lr=lr)
+    if chunking == "chunked":
+        sh.set_upload_chunk(700)
+        sh.set_sort_target(9)
+    sh.set_overlap(overlap)
     for i, w in enumerate(weights):
         sh.set_table(i, w)
     return sh
 
 
 @pytest.mark.parametrize("D", [1, 3])
-@pytest.mark.parametrize("overlap", ["1", "0"])
-def test_run_batch_matches_oracle(D, overlap, chunking, monkeypatch):
-    monkeypatch.setenv("SP_OVERLAP", overlap)
+@pytest.mark.parametrize("overlap", [True, False])
+def test_run_batch_matches_oracle(D, overlap, chunking):
     B = 96
     dims = [16, 32, 64, 128, 16, 64, 12, 4]
     task, placement = random_task(31 + D, dims, D, B)
@@ -44,7 +44,7 @@ def test_run_batch_matches_oracle(D, overlap, chunking, monkeypatch):
     W = sum(dims)
     grad = np.random.default_rng(4).uniform(-1, 1, size=(B, W)).astype(np.float32)
     lr = 0.02
-    sh = _shard(task, placement, weights, lr)
+    sh = _shard(task, placement, weights, lr, chunking, overlap)
     sh.set_grad(grad)
     bd = sh.run_batch(LookupBatch(idx, off, len(dims), B))
     assert bd.overall_ms > 0 and len(bd.fwd_ms) == D
@@ -75,7 +75,7 @@ def test_run_batch_rejects_bad_batch_without_update(chunking):
     task, placement = random_task(5, dims, 1, B)
     weights = random_weights(3, task.tables)
     off, idx = orc.synth_batch(as_dicts(task.tables), B, seed=2)
-    sh = _shard(task, placement, weights, 0.1)
+    sh = _shard(task, placement, weights, 0.1, chunking)
     sh.set_grad(np.ones((B, sum(dims)), dtype=np.float32))
     bad = idx.copy()
     bad[len(bad) // 2] = task.tables[1].hash_size + 5  # out of range in table 1
@@ -111,11 +111,11 @@ def test_run_batches_equals_sequential_steps(chunking):
         off, idx = orc.synth_batch(as_dicts(task.tables), B, seed=seed)
         batches.append(LookupBatch(idx, off, len(dims), B))
     grad = np.random.default_rng(8).uniform(-1, 1, size=(B, sum(dims))).astype(np.float32)
-    a = _shard(task, placement, weights, 0.02)
+    a = _shard(task, placement, weights, 0.02, chunking)
     a.set_grad(grad)
     ms = a.run_batches(batches)
     assert len(ms) == 3 and all(m > 0 for m in ms)
-    b = _shard(task, placement, weights, 0.02)
+    b = _shard(task, placement, weights, 0.02, chunking)
     b.set_grad(grad)
     for bt in batches:
         b.run_batch(bt)
@@ -125,12 +125,12 @@ def test_run_batches_equals_sequential_steps(chunking):
     bad_idx = batches[1].indices.copy()
     bad_idx[0] = -1
     bad = LookupBatch(bad_idx, batches[1].offsets, len(dims), B)
-    c = _shard(task, placement, weights, 0.02)
+    c = _shard(task, placement, weights, 0.02, chunking)
     c.set_grad(grad)
     with pytest.raises(ShardplanError) as e:
         c.run_batches([batches[0], bad, batches[2]])
     assert e.value.kind == "bad_input" and "step 1" in str(e.value)
-    d = _shard(task, placement, weights, 0.02)
+    d = _shard(task, placement, weights, 0.02, chunking)
     d.set_grad(grad)
     d.run_batch(batches[0])
     d.run_batch(batches[2])

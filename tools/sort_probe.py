@@ -1,0 +1,28 @@
+"""Runs the K4a sort of the cfg3 batch (D = 1) a few times: a target for
+ncu (`-k regex:sort_`) and a quick CUDA-event timing of the sort alone."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from bench import SEED, load_task  # noqa: E402
+from paper_2210_02023_b200 import api  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+task = load_task(cfg, 1)
+sh = api.EmbeddingShard(task, [0] * len(task.tables), lr=0.01)
+sh.init_tables(SEED)
+sh.synth_batch(SEED)
+sh.synth_grad(SEED)
+sh.set_overlap(False)
+sh.set_profiling(True)
+for _ in range(reps):
+    sh.enqueue_iteration()
+k = sh.kernel_ms()
+print(json.dumps({n: round(v[0] / max(1, v[1]), 4) for n, v in k.items()}))
+sh.close()
