@@ -70,6 +70,25 @@ def make_placement(task, how: str, device: int, ckpt_path: str = CKPT):
     return api.expert_placement(task, how)
 
 
+def make_placement_cpu(task, how: str, ckpt_path: str = CKPT):
+    """The same placement as make_placement, computed on the host by the
+    reference's own code (oracle/_ref: harness.hpp:332 infer for DreamShard,
+    baselines.hpp expert placements) — for the reference arm, which must not
+    run our kernels. tests/test_evaluator_gpu.py pins infer() on the GPU to it."""
+    if task.num_devices == 1:
+        return np.zeros(len(task.tables), dtype=np.int32)
+    from paper_2210_02023_b200 import api
+    if how == "dreamshard":
+        from oracle import ref
+        tables = [t.to_dict() for t in task.tables]
+        p, _, _ = ref.infer(ckpt_path, tables, task.num_devices, task.mem_cap_gb,
+                            task.batch_size)
+        return np.asarray(p, dtype=np.int32)
+    if how == "random":
+        return api.random_placement(task, SEED)
+    return api.expert_placement(task, how)
+
+
 def bench_placements(args, device: int):
     """Paper Fig. 1 on B200: DreamShard vs random vs greedy (size, lookup)
     placements of cfg2 (50 tables, D=4, the m50_d4 checkpoint) and cfg3
@@ -231,16 +250,43 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def dist_setup():
+def dist_setup(args):
+    """One process per GPU. Under torchrun WORLD_SIZE/RANK/LOCAL_RANK come
+    from the environment and must agree with --gpus; NCCL's INIT lines stay
+    on (NCCL_DEBUG=INFO, subsystem INIT) so every rank's communicator shows
+    in the log. --dry-dist uses gloo (no GPU) and stops after the rendezvous.
+    The reference arm needs no process group: rank 0 runs it alone."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one "
+                         f"process per GPU (bench.py self-launches when WORLD_SIZE is unset)")
+    if world > 1 and args.impl == "ours":
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dry_dist:
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
+
+
+def self_launch(args) -> int:
+    """`python bench.py --gpus N` without torchrun: re-run this script as N
+    ranks (torch.distributed.run, one process per GPU, rendezvous on
+    127.0.0.1) and return its exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def allreduce_max(x: float, world: int) -> float:
@@ -262,55 +308,139 @@ def barrier(world: int):
 # ---------------------------------------------------------------------------
 # CPU legs (oracle port; the only place bench.py touches oracle/)
 
-def cpu_sample(task, sample_bags: int, threads: int, steps: int = 1, warmup: int = 0):
-    """The oracle port (oracle/lookup_oracle.cpp, OpenMP) on bags [0, Bs) of
-    every table: fwd sum-pooling + per-table stable sort/segment/SGD. Returns
-    per-step ms extrapolated to the full batch, and the sample description."""
-    from oracle import lookup as orc
-    tables = [t.to_dict() for t in task.tables]
-    Bs = sample_bags
-    off, idx = orc.synth_batch(tables, Bs, SEED, nthreads=threads)
-    dims = [t.dim for t in task.tables]
-    rows = [t.hash_size for t in task.tables]
-    weights = [np.full((t.hash_size, t.dim), 0.75, dtype=np.float32) for t in task.tables]
-    W = sum(dims)
-    grad = np.random.default_rng(0).uniform(-1, 1, size=(Bs, W)).astype(np.float32)
-    lst = list(range(len(tables)))
-    times = []
-    for i in range(warmup + steps):
-        t0 = time.perf_counter()
-        orc.tbe_forward(dims, rows, weights, off, idx, Bs, nthreads=threads)
-        orc.tbe_backward_sgd_inplace(dims, rows, weights, off, idx, Bs, grad, 0.01, lst,
-                                     nthreads=threads)
-        dt = time.perf_counter() - t0
-        if i >= warmup:
-            times.append(dt * 1e3 * (task.batch_size / Bs))
-    sample = (f"oracle port (fp64-accumulate fwd + stable-sort SGD) on bags [0,{Bs}) of all "
-              f"{len(tables)} tables ({len(idx)} lookups), x{task.batch_size // Bs} to the "
-              f"full batch; D=1 layout (no exchange)")
-    return times, sample
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class CpuIteration:
+    """The oracle port (oracle/lookup_oracle.cpp, OpenMP) running the FULL
+    workload iteration on the host cores: fp64-accumulated sum-pooling of
+    every table's bags -> (D > 1) the forward all-to-all as the host
+    re-layout of pooled rows from owner-major to receiver-major -> the
+    backward all-to-all (the mirror) -> per-table stable sort / segment /
+    row-wise SGD. Same tables, batch, placement and D as the GPU arm."""
+
+    def __init__(self, task, placement):
+        from oracle import lookup as orc
+        self.orc = orc
+        self.task = task
+        tables = [t.to_dict() for t in task.tables]
+        self.B = task.batch_size
+        self.off, self.idx = orc.synth_batch(tables, self.B, SEED)
+        self.dims = [t.dim for t in task.tables]
+        self.rows = [t.hash_size for t in task.tables]
+        self.weights = [np.full((t.hash_size, t.dim), 0.75, dtype=np.float32)
+                        for t in task.tables]
+        W = sum(self.dims)
+        self.grad = np.random.default_rng(0).uniform(-1, 1, size=(self.B, W)).astype(np.float32)
+        self.lst = list(range(len(tables)))
+        D = task.num_devices
+        self.D = D
+        gcol = np.concatenate([[0], np.cumsum(self.dims)])
+        # owner-major column order: device 0's tables' columns, then device 1's ...
+        # owner-major column blocks: (global column range, receiver column start)
+        self.blocks, c = [], 0
+        for d in range(D):
+            for t in self.lst:
+                if placement[t] == d:
+                    self.blocks.append((int(gcol[t]), int(gcol[t + 1]), c))
+                    c += self.dims[t]
+        if D > 1:
+            # each receiver's gradient slice [B/D, W] in its owner-major layout;
+            # receive / send-back buffers allocated once, like the GPU arm's
+            s = self.B // D
+            self.recv = [np.empty((s, W), dtype=np.float32) for _ in range(D)]
+            self.back = np.empty_like(self.grad)
+            self.grad_recv = [np.empty((s, W), dtype=np.float32) for _ in range(D)]
+            for j in range(D):
+                self._to_receiver(self.grad, j, self.grad_recv[j])
+            from concurrent.futures import ThreadPoolExecutor
+            self.pool = ThreadPoolExecutor(max_workers=D)  # numpy copies drop the GIL
+
+    def _to_receiver(self, src, j, out):
+        s = self.B // self.D
+        for g0, g1, c in self.blocks:
+            out[:, c:c + g1 - g0] = src[j * s:(j + 1) * s, g0:g1]
+
+    def _to_owner(self, j):
+        s = self.B // self.D
+        for g0, g1, c in self.blocks:
+            self.back[j * s:(j + 1) * s, g0:g1] = self.grad_recv[j][:, c:c + g1 - g0]
+
+    def step(self, threads: int):
+        orc = self.orc
+        pooled = orc.tbe_forward(self.dims, self.rows, self.weights, self.off, self.idx, self.B,
+                                 nthreads=threads)
+        grad = self.grad
+        if self.D > 1:
+            # fwd a2a: receiver j gets rows [j s, (j+1) s) of every owner's block
+            list(self.pool.map(lambda j: self._to_receiver(pooled, j, self.recv[j]),
+                               range(self.D)))
+            # bwd a2a: each receiver's gradient slice back to the owners
+            list(self.pool.map(self._to_owner, range(self.D)))
+            grad = self.back
+        orc.tbe_backward_sgd_inplace(self.dims, self.rows, self.weights, self.off, self.idx,
+                                     self.B, grad, 0.01, self.lst, nthreads=threads)
+
+    def time(self, threads: int, steps: int, warmup: int):
+        times = []
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            self.step(threads)
+            if i >= warmup:
+                times.append((time.perf_counter() - t0) * 1e3)
+        return times
+
+    def describe(self, threads: int, steps: int, warmup: int) -> str:
+        ex = ("the a2a re-layouts as host copies" if self.D > 1 else "D=1 (no exchange)")
+        return (f"oracle port on the FULL batch: {len(self.lst)} tables, B={self.B}, "
+                f"{len(self.idx)} lookups; fp64-accumulate fwd + stable-sort SGD, {ex}; "
+                f"{threads} thread(s), median of {steps} after {warmup} warm-up")
+
+
+def cpu_baseline(task, placement, steps: int, warmup: int, single: bool = True):
+    """Full-batch CPU iteration: all host threads (median of `steps`) and,
+    when `single`, one thread (one timed step after none: ~15-20 s)."""
+    threads = os.cpu_count() or 1
+    it = CpuIteration(task, placement)
+    times = it.time(threads, steps, warmup)
+    out = {"value": round(statistics.median(times), 3), "unit": UNIT, "cores": threads,
+           "kind": "port", "sample": it.describe(threads, steps, warmup),
+           "times_ms": [round(t, 2) for t in times], "cpu_model": cpu_model(),
+           "method": "PAPER.md:673 (warm-up, then median)"}
+    if single:
+        t1 = it.time(1, 1, 0)
+        out["single_thread"] = {"value": round(t1[0], 3), "unit": UNIT, "cores": 1,
+                                "sample": it.describe(1, 1, 0)}
+    return out
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the reference path on the host cores (the reference
-    has no lookup code, so this is the oracle port, kind "port")."""
+    """--impl reference: the reference path on the host cores. The reference
+    has no lookup code (its cost is a model, oracle.hpp:140-185), so this is
+    the oracle port (kind "port") running the full iteration of the same
+    config as the GPU arm: same tables, batch, D and placement."""
     if rank != 0:
         return
-    task = load_task(args.config, max(args.gpus, 1))
-    threads = os.cpu_count() or 1
-    times, sample = cpu_sample(task, args.cpu_sample_bags, threads, steps=args.steps,
-                               warmup=args.warmup)
-    v = statistics.median(times)
+    task = load_task(args.config, args.gpus)
+    placement = make_placement_cpu(task, args.placement)
+    bl = cpu_baseline(task, placement, args.steps, args.warmup, single=not args.no_cpu_single)
+    v = bl["value"]
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT,
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(v, 3), "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "ms_per_step": v, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (SURVEY §8d generator, seed 2210)",
         "config": config_dict(args, task),
-        "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
-        "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "cpu_baseline": bl,
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -466,6 +596,59 @@ def bench_reference_evaluator(n_eval: int = 1024, n_sampled: int = 8):
 
 # ---------------------------------------------------------------------------
 
+NVLINK_GBS = 900.0
+
+
+def load_traffic(key: str):
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum)
+    of a kernel from the ncu capture committed for this code
+    (profiles/traffic.json, written by profiles/summarize.py with the HEAD
+    it was captured at)."""
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(tpath):
+        return None, None
+    with open(tpath) as f:
+        t = json.load(f)
+    v = t.get(key)
+    if isinstance(v, dict):
+        return v.get("dram_bytes"), v.get("head")
+    return v, t.get("_head")
+
+
+def roofline_block(args, D, kernels, per_launch, alg, dominant, ab):
+    """Roofline of the dominant kernel on algorithmic bytes (SURVEY §8d per
+    launch / CUDA-event time) and, per hot kernel, on DRAM bytes from ncu.
+    K1's algorithmic bytes count every lookup's row read; the hot rows are
+    served by L2, so its algorithmic rate exceeds the copy peak — it is
+    reported as `l2_inclusive_gbs` with no fraction, beside the DRAM rate and
+    the unique-row floor (each touched row read once)."""
+    peak, peak_kind = load_peaks()
+    ach = alg[dominant] / (per_launch[dominant] * 1e6)
+    out = {"bound": "hbm", "kernel": dominant, "achieved": round(ach, 1), "peak": peak,
+           "unit": "GB/s", "frac": round(ach / peak, 3), "traffic": None,
+           "peak_kind": peak_kind}
+    for k in ("fwd", "sgd"):
+        t = per_launch.get(k, 0.0)
+        dram, head = load_traffic(f"{args.config}/D{D}/{k}")
+        e = {"ms": round(t, 4)}
+        if dram and t > 0:
+            e.update({"dram_bytes": dram, "dram_gbs": round(dram / (t * 1e6), 1),
+                      "dram_frac": round(dram / (t * 1e6) / peak, 3),
+                      "dram_source": f"ncu --set full, profiles/traffic.json (HEAD {head})"})
+        if k == "fwd" and t > 0:
+            e["l2_inclusive_gbs"] = kernels["fwd"]["alg_gbs"]
+            e["unique_floor_bytes"] = ab["fwd_unique"]
+            e["unique_floor_gbs"] = round(ab["fwd_unique"] / (t * 1e6), 1)
+            e["unique_floor_frac"] = round(ab["fwd_unique"] / (t * 1e6) / peak, 3)
+        if k == "sgd" and t > 0:
+            e["alg_gbs"] = kernels["sgd"]["alg_gbs"]
+            e["alg_frac"] = round(kernels["sgd"]["alg_gbs"] / peak, 3)
+        out["lookup_fwd" if k == "fwd" else "sgd"] = e
+        if k == dominant:
+            out["traffic"] = dram
+    return out
+
+
 def run_ours(args, world, rank, local):
     import torch
     from paper_2210_02023_b200 import api
@@ -546,18 +729,18 @@ def run_ours(args, world, rank, local):
                       "alg_bytes": alg[k],
                       "alg_gbs": round(alg[k] / (t * 1e6), 1) if t > 0 else None}
     dominant = max(("fwd", "sgd"), key=lambda k: kms[k][0])
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            traffic = json.load(f).get(f"{args.config}/D{D}/{dominant}")
-    ach = alg[dominant] / (per_launch[dominant] * 1e6)
-    roofline = {"bound": "hbm", "kernel": dominant, "achieved": round(ach, 1),
-                "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 3),
-                "traffic": traffic, "peak_kind": peak_kind,
-                "lookup_fwd": {"achieved": kernels["fwd"]["alg_gbs"],
-                               "frac": round(kernels["fwd"]["alg_gbs"] / peak, 3)
-                               if kernels["fwd"]["alg_gbs"] else None}}
+    roofline = roofline_block(args, D, kernels, per_launch, alg, dominant, ab)
+
+    # NVLink GB/s of the two exchange stages (N > 1): bytes this rank sends
+    # per direction (sp_ctx_algorithmic_bytes[1], max over ranks) / stage ms
+    if world > 1:
+        for name, st in (("fwd_a2a", bd.fwd_comm_stage_ms), ("bwd_a2a", bd.bwd_comm_stage_ms)):
+            gbs = ab["a2a"] / (st * 1e6) if st > 0 else None
+            roofline[name] = {"bytes_sent_per_rank": ab["a2a"], "stage_ms": round(st, 4),
+                              "achieved": round(gbs, 1) if gbs else None,
+                              "peak": NVLINK_GBS, "unit": "GB/s",
+                              "frac": round(gbs / NVLINK_GBS, 3) if gbs else None,
+                              "bound": "nvlink (900 GB/s per direction per GPU)"}
 
     # e2e through the public API with host buffers: H2D LookupBatch (pinned
     # int64, the reference layout) -> measured iteration -> breakdown to host
@@ -599,13 +782,10 @@ def run_ours(args, world, rank, local):
                 ROOT, "oracle", "_ref", "libshardplan_ref.so")):
             evaluator["reference_cpu"] = bench_reference_evaluator()
 
-    # CPU baseline (rank 0, N = 1 only)
+    # CPU baseline (rank 0, N = 1 only): the full iteration on the host cores
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        times, sample = cpu_sample(task, args.cpu_sample_bags, threads, steps=1, warmup=0)
-        cpu = {"value": round(times[0], 3), "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": sample}
+        cpu = cpu_baseline(task, placement, steps=3, warmup=1, single=not args.no_cpu_single)
 
     # D=8 DreamShard placement emulated on this GPU (N = 1 only)
     emulated = None
@@ -673,8 +853,8 @@ def run_ours(args, world, rank, local):
             "gpu_launches_detail": {"per_iter_graph_kernel_nodes": kernels_per_iter,
                                     "own_launch_sites_counted": int(own_launches),
                                     "note": "per-iteration kernel nodes of the captured "
-                                            "iteration (K1, CUB radix-sort kernels compiled "
-                                            "into our library, K4 SGD)"},
+                                            "iteration (K1, the K4a sort passes, K4 SGD "
+                                            "and carry; all in _shardplan_b200.so)"},
             "clocks": clk.summary(),
             "emulated_d8": emulated,
             "fp16_tables": fp16,
@@ -687,7 +867,7 @@ def run_ours(args, world, rank, local):
     shard.close()
 
 
-def main():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
@@ -696,22 +876,36 @@ def main():
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--placement", default="dreamshard",
                     choices=["dreamshard", "size", "dim", "lookup", "size-lookup"])
-    ap.add_argument("--cpu-sample-bags", type=int, default=2048)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cpu-single", action="store_true",
+                    help="skip the single-thread full-batch CPU step (~15-20 s)")
     ap.add_argument("--no-emulation", action="store_true")
     ap.add_argument("--no-evaluator", action="store_true")
     ap.add_argument("--no-fp16", action="store_true")
     ap.add_argument("--no-studies", action="store_true",
                     help="skip the placement study (cfg2/cfg3) and the cfg4 per-rank shards")
-    args = ap.parse_args()
+    ap.add_argument("--dry-dist", action="store_true",
+                    help="rendezvous only (gloo), print {world, rank} per rank and exit")
+    args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
-    world, rank, local = dist_setup()
-    if args.impl == "reference":
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    return args
+
+
+def main():
+    args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
+    world, rank, local = dist_setup(args)
+    if args.dry_dist:
+        print(json.dumps({"dry_dist": True, "world": world, "rank": rank}), flush=True)
+    elif args.impl == "reference":
         run_reference(args, world, rank)
     else:
         run_ours(args, world, rank, local)
-    if world > 1:
+    if world > 1 and args.impl == "ours":
         import torch.distributed as dist
         dist.destroy_process_group()
 

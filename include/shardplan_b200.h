@@ -289,8 +289,9 @@ int sp_ctx_kernel_ms(sp_ctx* ctx, double ms[5], int64_t counts[5]);
 
 /* Algorithmic bytes of one launch of each stage on this rank:
  * [0]=fwd (K1) [1]=a2a send per direction [2]=bwd floor (K4, sort
- * excluded) [3]=sort traffic estimate. */
-int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]);
+ * excluded) [3]=sort traffic estimate [4]=K1's unique-row floor (every
+ * touched row read once: K1's DRAM bytes with perfect L2 reuse). */
+int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[5]);
 
 /* ------------------------------------------------------------------ */
 /* Ingest — ingest_lookup_batch (table.hpp:188-232) on the GPU.         */

@@ -609,9 +609,10 @@ class EmbeddingShard:
         return {k: (ms[i], n[i]) for i, k in enumerate(self.KERNELS)}
 
     def algorithmic_bytes(self) -> dict:
-        out = (ctypes.c_double * 4)()
+        out = (ctypes.c_double * 5)()
         check(lib().sp_ctx_algorithmic_bytes(self._h, out))
-        return {"fwd": out[0], "a2a": out[1], "bwd": out[2], "sort": out[3]}
+        return {"fwd": out[0], "a2a": out[1], "bwd": out[2], "sort": out[3],
+                "fwd_unique": out[4]}
 
 
 # ---------------------------------------------------------------------------

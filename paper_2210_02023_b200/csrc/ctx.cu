@@ -1944,7 +1944,7 @@ int sp_ctx_kernel_ms(sp_ctx* ctx, double ms[5], int64_t counts[5]) {
   });
 }
 
-int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]) {
+int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[5]) {
   return guarded([&] {
     check_ctx(ctx);
     require_batch(ctx);
@@ -1958,8 +1958,10 @@ int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]) {
     //  [3] K4a sort: ids read twice (8 B/lookup), packed pairs written and
     //      read (4 B each, 8 B when wide), sorted key + bag written, offsets
     //      read twice, count matrix written, scanned (read + write) and read
+    //  [4] K1's unique-row floor: [0] with every touched row read once (the
+    //      DRAM bytes K1 would move if L2 kept every reused row)
     // (row bytes use the storage type: 2 B/param for fp16 tables)
-    double fwd = 0, a2a = 0, sgd = 0, sort = 0;
+    double fwd = 0, a2a = 0, sgd = 0, sort = 0, fwd_u = 0;
     const double eb = elem_bytes(c->wt);
     for (auto& v : c->vdevs) {
       const int T = static_cast<int>(v.tables.size());
@@ -1986,6 +1988,7 @@ int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]) {
           }
       }
       sgd = std::max(sgd, outb + 2.0 * eb * uniq_dim + pair * v.nnz);
+      fwd_u = std::max(fwd_u, csr + eb * uniq_dim + outb);
       const double sort_dev = 2.0 * csr + 2.0 * mid * v.nnz + pair * v.nnz +
                               4.0 * 4.0 * static_cast<double>(v.splan.n_cnt);
       sort = std::max(sort, sort_dev);
@@ -1994,6 +1997,7 @@ int sp_ctx_algorithmic_bytes(sp_ctx* ctx, double out[4]) {
     out[1] = a2a;
     out[2] = sgd;
     out[3] = sort;
+    out[4] = fwd_u;
   });
 }
 

@@ -1,0 +1,64 @@
+"""bench.py's host-side contract (CPU): both arms describe the same config
+for every N, `python bench.py --gpus N` self-launches N ranks, and the CPU
+iteration the reference arm times is the oracle's arithmetic with the
+exchange as a pure re-layout."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+@pytest.mark.parametrize("gpus", [1, 2, 4, 8])
+def test_arms_share_config(gpus):
+    """run_ours sizes the task by the world (= --gpus, enforced by
+    dist_setup); run_reference by --gpus: the config objects are equal."""
+    args = bench.parse_args(["--gpus", str(gpus)])
+    ours = bench.config_dict(args, bench.load_task(args.config, gpus))
+    ref_args = bench.parse_args(["--gpus", str(gpus), "--impl", "reference"])
+    ref = bench.config_dict(ref_args, bench.load_task(ref_args.config, ref_args.gpus))
+    assert ours == ref
+    assert ours["devices"] == gpus
+
+
+def test_world_must_match_gpus(monkeypatch):
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    with pytest.raises(SystemExit):
+        bench.dist_setup(bench.parse_args(["--gpus", "4"]))
+
+
+def test_self_launch_reaches_world_2():
+    """`python bench.py --gpus 2` with no WORLD_SIZE re-runs itself under
+    torch.distributed.run; --dry-dist stops each rank after the rendezvous."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--dry-dist"], capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert sorted(x["rank"] for x in lines) == [0, 1]
+    assert all(x["world"] == 2 for x in lines)
+
+
+def test_cpu_iteration_exchange_is_a_relayout():
+    """The D > 1 CPU step: the backward all-to-all hands every owner exactly
+    the gradient columns of its tables (the mirror of the forward re-layout),
+    so the SGD result equals the D = 1 step's."""
+    from paper_2210_02023_b200.api import PlacementTask, TableDesc
+    dims = [8, 16, 4, 8]
+    tabs = [TableDesc(i, d, 50 + 10 * i, 3.0, 0.0, [0.5] + [0.0] * 11 + [0.5] + [0.0] * 4)
+            for i, d in enumerate(dims)]
+    res = []
+    for D, pl in ((1, [0, 0, 0, 0]), (2, [1, 0, 1, 0])):
+        it = bench.CpuIteration(PlacementTask(tabs, D, 0.0, 64), pl)
+        it.step(1)
+        res.append([w.copy() for w in it.weights])
+    for a, b in zip(*res):
+        np.testing.assert_array_equal(a, b)
