@@ -17,8 +17,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def short(name):
-    for k in ("tbe_forward", "sgd_seg_kernel", "sgd_carry_kernel", "sgd_kernel", "build_keys", "Onesweep", "Histogram",
-              "ExclusiveSum", "rollout", "eval_kernel"):
+    for k in ("tbe_forward", "sgd_seg_kernel", "sgd_carry_kernel", "sgd_kernel", "sort_count",
+              "sort_scan", "sort_scatter", "sort_bucket", "sort_big", "narrow_table",
+              "rollout", "eval_kernel"):
         if k in name:
             return k
     return name[:40]
@@ -66,6 +67,9 @@ def to_bytes(val, unit):
 def main():
     rnd, lpath = sys.argv[1], sys.argv[2]
     rep = sys.argv[3] if len(sys.argv) > 3 else None
+    # the commit the capture ran (gpurun snapshots the committed tree)
+    head = subprocess.run(["git", "rev-parse", "--short=12", "HEAD"], capture_output=True,
+                          text=True, cwd=HERE).stdout.strip()
     shutil.copy(lpath, os.path.join(HERE, f"{rnd}_launches.csv"))
     L = launches(lpath)
     lines = [f"# {rnd}: ncu summary (cfg3, D=1, one iteration = the launches below)", "",
@@ -93,11 +97,14 @@ def main():
                 d.get("launch__registers_per_thread", ""),
                 d.get("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", ""),
                 d.get("lts__throughput.avg.pct_of_peak_sustained_elapsed", "")]) + " |")
-            k = {"tbe_forward": "fwd", "sgd_kernel": "sgd", "sgd_seg_kernel": "sgd"}.get(short(d.get("Kernel Name", "")))
+            k = {"tbe_forward": "fwd", "sgd_kernel": "sgd", "sgd_seg_kernel": "sgd",
+                 "sort_scatter": "sort_scatter", "sort_big": "sort_big"}.get(
+                     short(d.get("Kernel Name", "")))
             if k:
-                traffic[f"cfg3/D1/{k}"] = (
-                    to_bytes(d["dram__bytes_read.sum"], u["dram__bytes_read.sum"]) +
-                    to_bytes(d["dram__bytes_write.sum"], u["dram__bytes_write.sum"]))
+                traffic[f"cfg3/D1/{k}"] = {
+                    "dram_bytes": to_bytes(d["dram__bytes_read.sum"], u["dram__bytes_read.sum"]) +
+                    to_bytes(d["dram__bytes_write.sum"], u["dram__bytes_write.sum"]),
+                    "head": head, "capture": os.path.basename(rep)}
         json.dump(traffic, open(traffic_path, "w"), indent=1)
     open(os.path.join(HERE, f"{rnd}_summary.md"), "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))

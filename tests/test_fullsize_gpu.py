@@ -4,9 +4,9 @@ weights on the GPU and in the CPU oracle (generator-defined weights, so the
 oracle never materialises the tables).
   - the backward's sorted (key, bag) pairs and run heads == std::stable_sort
     over the whole batch, bit for bit;
-  - pooled rows of the first and last 512 bags of every table == the oracle's
+  - all pooled rows (every bag of every table) == the oracle's
     fp64-accumulated forward (rtol 1e-5);
-  - three whole tables (the heaviest, a dim-16 and a dim-128 one) after one
+  - ten whole tables (the heaviest, a dim-16, a dim-128 one and every 14th) after one
     SGD step == the oracle's row-wise SGD over all of their lookups (rtol 1e-5).
 """
 import json
@@ -17,6 +17,7 @@ import pytest
 
 from oracle import lookup as orc
 from paper_2210_02023_b200.api import EmbeddingShard, PlacementTask, TableDesc
+from tests.helpers import grad_cols
 
 pytestmark = pytest.mark.gpu
 
@@ -51,7 +52,8 @@ def test_fullsize_sort_bit_exact(cfg3):
     np.testing.assert_array_equal(heads, wh)
 
 
-def test_fullsize_forward_sampled_bags(cfg3):
+def test_fullsize_forward_all_bags(cfg3):
+    """Every pooled row of the 65536 x 6224 output (1.6 GB), in bag chunks."""
     task, sh, off, idx = cfg3
     B = task.batch_size
     dims = [t.dim for t in task.tables]
@@ -59,25 +61,10 @@ def test_fullsize_forward_sampled_bags(cfg3):
     sh.forward()
     sh.a2a_forward()
     pooled = sh.pooled()
-    for lo, hi in ((0, 512), (B - 512, B)):
+    for lo in range(0, B, 8192):
+        hi = lo + 8192
         want = orc.tbe_forward(dims, rows, None, off, idx, B, wseed=SEED, bag_lo=lo, bag_hi=hi)
         np.testing.assert_allclose(pooled[lo:hi], want, rtol=1e-5, atol=1e-5)
-
-
-def _grad_cols(seed, B, cols):
-    """The SURVEY 8d gradient generator (synth.cuh grad_value), vectorised:
-    columns `cols` of dL/dpooled for every bag."""
-    def mix64(x):
-        x = x + np.uint64(0x9e3779b97f4a7c15)
-        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xbf58476d1ce4e5b9)
-        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94d049bb133111eb)
-        return x ^ (x >> np.uint64(31))
-    tag = np.uint64(0x6772616469656e74)
-    with np.errstate(over="ignore"):
-        s = mix64(np.array([np.uint64(seed) ^ tag], dtype=np.uint64))
-        hb = mix64(s ^ np.arange(B, dtype=np.uint64))[:, None]
-        h = mix64(hb ^ np.asarray(cols, dtype=np.uint64)[None, :])
-    return (h >> np.uint64(40)).astype(np.float32) * np.float32(2.0 ** -23) - np.float32(1.0)
 
 
 def test_fullsize_sgd_whole_tables(cfg3):
@@ -89,7 +76,7 @@ def test_fullsize_sgd_whole_tables(cfg3):
     heavy = int(np.argmax(nnz * np.array(dims)))
     d16 = next(i for i in range(T) if dims[i] == 16 and i != heavy)
     d128 = next(i for i in range(T) if dims[i] == 128 and i != heavy)
-    picks = [heavy, d16, d128]
+    picks = sorted({heavy, d16, d128} | set(range(0, T, 14)))
     before = {t: sh.get_table(t) for t in picks}
     gcol = np.concatenate([[0], np.cumsum(dims)[:-1]])
     sh.synth_grad(SEED)
@@ -106,10 +93,10 @@ def test_fullsize_sgd_whole_tables(cfg3):
     sub_off = np.concatenate(sub_off)
     sub_idx = np.concatenate(sub_idx)
     cols = np.concatenate([np.arange(gcol[t], gcol[t] + dims[t]) for t in picks])
-    grad = _grad_cols(SEED, B, cols)
+    grad = grad_cols(SEED, B, cols)
     sub_dims = [dims[t] for t in picks]
     sub_rows = [task.tables[t].hash_size for t in picks]
     want = orc.tbe_backward_sgd(sub_dims, sub_rows, [before[t] for t in picks], sub_off,
-                                sub_idx, B, grad, LR, [0, 1, 2])
+                                sub_idx, B, grad, LR, list(range(len(picks))))
     for k, t in enumerate(picks):
         np.testing.assert_allclose(sh.get_table(t), want[k], rtol=1e-5, atol=1e-6)

@@ -255,3 +255,43 @@ def test_runs_spanning_many_sgd_tiles(sort_target):
     for i in range(len(dims)):
         np.testing.assert_allclose(sh.get_table(i), want[i], rtol=RTOL, atol=1e-5)
     sh.close()
+
+
+def _golden_cases():
+    import json
+    import os
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "lookup_cases.json")
+    with open(p) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("case", _golden_cases(), ids=lambda c: c["name"])
+def test_golden_cases_bit_exact(case, sort_target):
+    """K1, the K4a sort and the SGD against the hand-worked golden cases
+    (tests/golden/gen_lookup_cases.py; integer data: exact)."""
+    dims, rows, B = case["dims"], case["rows"], case["B"]
+    placement = case["placement"]
+    D = max(placement) + 1
+    tables = make_tables(dims, rows, [1.0] * len(dims))
+    task = PlacementTask(tables, D, 0.0, B)
+    w = [np.array(x, dtype=np.float32).reshape(r, d) for x, r, d in
+         zip(case["weights"], rows, dims)]
+    sh = _shard(task, placement, w, lr=case["lr"])
+    sh.set_sort_target(sort_target)
+    off = np.array(case["offsets"], dtype=np.int64)
+    idx = np.array(case["indices"], dtype=np.int64)
+    sh.upload_batch(LookupBatch(idx, off, len(dims), B))
+    sh.forward()
+    sh.a2a_forward()
+    np.testing.assert_array_equal(sh.pooled(), np.array(case["pooled"], dtype=np.float32))
+    for d, want in enumerate(case["sorted"]):
+        k, b, h = sh.sorted(d)
+        assert k.tolist() == want["keys"] and b.tolist() == want["bags"]
+        assert h.tolist() == want["heads"]
+    sh.set_grad(np.array(case["grad"], dtype=np.float32))
+    sh.a2a_backward()
+    sh.backward_sgd()
+    for t, (x, r, d) in enumerate(zip(case["updated"], rows, dims)):
+        np.testing.assert_array_equal(sh.get_table(t),
+                                      np.array(x, dtype=np.float32).reshape(r, d))
+    sh.close()

@@ -224,3 +224,28 @@ def test_live_reference_agrees_with_oracle_ingest():
     rc, pf, dist = orc.ingest(off, idx, T, B)
     for i, t in enumerate(tables):
         assert t["pooling_factor"] == pf[i] and t["dist"] == dist[i].tolist()
+
+
+# ---- lookup path: hand-worked golden cases (tests/golden/gen_lookup_cases.py)
+
+@pytest.mark.parametrize("case", _load("lookup_cases.json"), ids=lambda c: c["name"])
+def test_oracle_lookup_golden_cases(case):
+    """The oracle's forward, stable sort and row-wise SGD against outputs
+    worked out from the definitions (integer data, lr 0.5: exact)."""
+    dims, rows, B = case["dims"], case["rows"], case["B"]
+    w = [np.array(x, dtype=np.float32).reshape(r, d) for x, r, d in
+         zip(case["weights"], rows, dims)]
+    off = np.array(case["offsets"], dtype=np.int64)
+    idx = np.array(case["indices"], dtype=np.int64)
+    np.testing.assert_array_equal(orc.tbe_forward(dims, rows, w, off, idx, B),
+                                  np.array(case["pooled"], dtype=np.float32))
+    for d, want in enumerate(case["sorted"]):
+        lst = [t for t in range(len(dims)) if case["placement"][t] == d]
+        k, b, h = orc.sorted_keys(rows, off, idx, B, lst)
+        assert k.tolist() == want["keys"] and b.tolist() == want["bags"]
+        assert h.tolist() == want["heads"]
+    grad = np.array(case["grad"], dtype=np.float32)
+    got = orc.tbe_backward_sgd(dims, rows, w, off, idx, B, grad, case["lr"],
+                               list(range(len(dims))))
+    for g, x, r, d in zip(got, case["updated"], rows, dims):
+        np.testing.assert_array_equal(g, np.array(x, dtype=np.float32).reshape(r, d))

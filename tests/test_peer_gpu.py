@@ -25,8 +25,19 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _case():
+def _case(name="random"):
     from tests.helpers import random_task, random_weights
+    if name == "cfg1":
+        # BASELINE.json cfg1: 10 x dim 16, 1e5 rows, pf 8, D = 2, B = 512
+        import json
+        from paper_2210_02023_b200.api import PlacementTask, TableDesc
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        with open(os.path.join(root, "paper_2210_02023_b200", "data", "pools.json")) as f:
+            pool = json.load(f)["cfg1"]
+        tables = [TableDesc.from_dict(t) for t in pool["tables"]]
+        task = PlacementTask(tables, WORLD, 0.0, int(pool["batch_size"]))
+        placement = (np.arange(len(tables)) % WORLD).astype(np.int32)
+        return task, placement, random_weights(17, task.tables)
     dims = [16, 64, 32, 128, 12, 16, 64]
     task, placement = random_task(101, dims, WORLD, B)
     placement[0], placement[1] = 0, 1  # both ranks own tables
@@ -34,7 +45,7 @@ def _case():
     return task, placement, weights
 
 
-def _worker(rank, port, q):
+def _worker(rank, port, q, name="random"):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -43,7 +54,8 @@ def _worker(rank, port, q):
         from oracle import lookup as orc
         from paper_2210_02023_b200.api import EmbeddingShard, LookupBatch
         from tests.helpers import as_dicts
-        task, placement, weights = _case()
+        task, placement, weights = _case(name)
+        B = task.batch_size
         dims = [t.dim for t in task.tables]
         rows = [t.hash_size for t in task.tables]
         off, idx = orc.synth_batch(as_dicts(task.tables), B, seed=23)
@@ -93,12 +105,13 @@ def _worker(rank, port, q):
         q.put((rank, traceback.format_exc()))
 
 
-def test_peer_exchange_two_processes_one_gpu():
+@pytest.mark.parametrize("name", ["random", "cfg1"])
+def test_peer_exchange_two_processes_one_gpu(name):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(WORLD)]
+    procs = [ctx.Process(target=_worker, args=(r, port, q, name)) for r in range(WORLD)]
     for p in procs:
         p.start()
     results = {}
