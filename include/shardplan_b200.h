@@ -120,7 +120,11 @@ int sp_nccl_unique_id(uint8_t out_id[SP_NCCL_ID_BYTES]);
  *    the same layout (reported, not NVLink).
  * batch_size must be divisible by num_devices. Validates the
  * placement like evaluate_placement (oracle.hpp:190-204) against
- * mem_cap_gb (<= 0 disables the cap). */
+ * mem_cap_gb. Divergence from check_memory (oracle.hpp:329-341), which
+ * enforces mem > cap + 1e-9 for every cap: here mem_cap_gb <= 0 disables
+ * the cap (an unbounded device), so tasks built with PlacementTask's default
+ * cap of 0 are measurable; pass the task's real cap to get the reference's
+ * memory_violation. */
 int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
                   int32_t num_devices, const int32_t* placement,
                   int32_t batch_size, double mem_cap_gb, float lr,
@@ -137,7 +141,11 @@ int sp_ctx_device_bytes(sp_ctx* ctx, uint64_t* bytes);
 int sp_ctx_local_tables(sp_ctx* ctx, int32_t* ids, int32_t* n_out);
 
 /* Table weights. Deterministic init w = 0.5 + 0.5*u(seed, table, row, col)
- * (SURVEY §8d), or explicit fp32 rows [hash_size, dim] row-major. */
+ * (SURVEY §8d), or explicit fp32 rows [hash_size, dim] row-major. The
+ * generators (weights here, bags and indices in sp_synth_batch /
+ * sp_synth_lookup_batch) are keyed by sp_table_spec.id, not by the table's
+ * position in the context, so a table keeps its synthetic data in any
+ * sub-task; the gradient generator is keyed by (bag, global column). */
 int sp_init_tables(sp_ctx* ctx, uint64_t seed);
 int sp_set_table(sp_ctx* ctx, int32_t table_id, const float* rows);
 int sp_get_table(sp_ctx* ctx, int32_t table_id, float* rows);
@@ -272,6 +280,20 @@ int sp_graph_replay(sp_ctx* ctx, int32_t iters, int32_t* kernels_per_iter);
  * with the forward and the exchanges. on = 0 serialises it behind K1
  * (per-kernel timing in isolation). */
 int sp_ctx_set_overlap(sp_ctx* ctx, int32_t on);
+
+/* The exchange of one GPU emulating D devices is a device-local copy, not
+ * NVLink. on = 1 makes the breakdown's comm terms (comm_ms, both stage
+ * times, overall) a MODEL of the NVLink 5 all-to-all instead — the B200
+ * counterpart of device_comm (oracle.hpp:178-185), see sp_comm_model.
+ * Rejected for one-process-per-GPU contexts (their exchange is measured). */
+#define SP_NVLINK_PEER_GBS 770.0  /* measured peer copy per direction, B200_PROFILING.md */
+#define SP_A2A_LATENCY_MS 0.010   /* grouped send/recv fixed cost (assumed, not measured) */
+int sp_ctx_set_comm_model(sp_ctx* ctx, int32_t on);
+/* Modelled ms of one all-to-all direction for a device holding width_dev
+ * pooled columns of width_total: SP_A2A_LATENCY_MS + max(4 B w_d (D-1)/D,
+ * 4 (B/D)(W - w_d)) / SP_NVLINK_PEER_GBS. width_total < 0 counts the send
+ * side only (a function of the device's own tables, like device_comm). */
+int sp_comm_model(int32_t batch, int64_t width_dev, int64_t width_total, int32_t D, double* ms);
 /* K4a sort plan override: buckets and warp-tiles of about `lookups` lookups
  * per table (0 = the default ~sqrt(64 n) rule). The sorted result does not
  * depend on it; tests use small targets to cover many buckets and tiles. */

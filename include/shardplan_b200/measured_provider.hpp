@@ -123,6 +123,9 @@ struct MeasureOptions {
   int iters = 5;              // median of these
   float lr = 0.01f;
   int cuda_device = 0;
+  // one GPU emulating D devices: comm terms from the NVLink 5 model
+  // (sp_comm_model) instead of the device-local copy's time
+  bool comm_model = true;
 };
 
 // One (emulated, world 1) shard of a placement on this GPU; RAII over sp_ctx.
@@ -138,6 +141,7 @@ class Shard {
     check(sp_ctx_create(specs.data(), static_cast<int32_t>(specs.size()), D_, p.data(),
                         task.batch_size, task.mem_cap_gb, o.lr, 0, 1, nullptr, o.cuda_device,
                         &ctx_));
+    check(sp_ctx_set_comm_model(ctx_, o.comm_model ? 1 : 0));
   }
   ~Shard() { sp_ctx_destroy(ctx_); }
   Shard(const Shard&) = delete;
@@ -219,16 +223,23 @@ class MeasuredCostProvider : public CostProvider {
       for (int id : assignment[d]) {
         if (id < 0 || static_cast<std::size_t>(id) >= task_.tables.size())
           throw Error(ErrorKind::unknown_table, "table id " + std::to_string(id));
-        TableDesc t = task_.tables[id];
-        t.id = static_cast<int>(sub.tables.size());
-        sub.tables.push_back(t);
+        // the table keeps its id: the synthetic data is keyed by it
+        sub.tables.push_back(task_.tables[id]);
         p.push_back(d);
       }
     std::vector<std::array<double, 3>> q(D, {0.0, 0.0, 0.0});
     if (sub.tables.empty()) return q;
     const CostBreakdown cb = measure_placement(sub, p, o_);
-    for (int d = 0; d < D; ++d)
-      if (!assignment[d].empty()) q[d] = {cb.fwd_ms[d], cb.bwd_ms[d], cb.comm_ms[d]};
+    for (int d = 0; d < D; ++d) {
+      if (assignment[d].empty()) continue;
+      double comm = cb.comm_ms[d];
+      if (o_.comm_model) {  // the send side of the device's own tables
+        int64_t w = 0;
+        for (int id : assignment[d]) w += task_.tables[id].dim;
+        check(sp_comm_model(task_.batch_size, w, -1, D, &comm));
+      }
+      q[d] = {cb.fwd_ms[d], cb.bwd_ms[d], comm};
+    }
     return q;
   }
 

@@ -57,6 +57,8 @@ SIGNATURES = {
     "sp_enqueue_iteration": (c_i32, [c_vp]),
     "sp_graph_replay": (c_i32, [c_vp, c_i32, P(c_i32)]),
     "sp_ctx_algorithmic_bytes": (c_i32, [c_vp, P(c_f64)]),
+    "sp_ctx_set_comm_model": (c_i32, [c_vp, c_i32]),
+    "sp_comm_model": (c_i32, [c_i32, c_i64, c_i64, c_i32, P(c_f64)]),
     "sp_ctx_set_profiling": (c_i32, [c_vp, c_i32]),
     "sp_ctx_set_overlap": (c_i32, [c_vp, c_i32]),
     "sp_ctx_set_sort_target": (c_i32, [c_vp, c_i64]),

@@ -307,6 +307,19 @@ class CostBreakdown:
                 "events": [e.__dict__ for e in self.events]}
 
 
+NVLINK_PEER_GBS = 770.0   # SP_NVLINK_PEER_GBS
+A2A_LATENCY_MS = 0.010    # SP_A2A_LATENCY_MS
+
+
+def comm_model_ms(batch: int, width_dev: int, width_total: int, D: int) -> float:
+    """Modelled ms of one all-to-all direction on NVLink 5 for a device with
+    width_dev pooled columns (sp_comm_model; width_total < 0: send side only)."""
+    ms = ctypes.c_double()
+    check(lib().sp_comm_model(int(batch), int(width_dev), int(width_total), int(D),
+                              ctypes.byref(ms)))
+    return ms.value
+
+
 def nccl_unique_id() -> bytes:
     buf = (ctypes.c_uint8 * 128)()
     check(lib().sp_nccl_unique_id(buf))
@@ -342,9 +355,9 @@ class HostBuffer:
         try:
             if getattr(self, "_p", None) and self._p.value:
                 lib().sp_host_free(self._p)
+                self._p = ctypes.c_void_p()
         except Exception:  # interpreter shutdown: the library binding is gone
             pass
-            self._p = ctypes.c_void_p()
 
 
 # ---------------------------------------------------------------------------
@@ -579,6 +592,12 @@ class EmbeddingShard:
     def synchronize(self):
         check(lib().sp_ctx_synchronize(self._h))
 
+    def set_comm_model(self, on: bool):
+        """One GPU emulating D devices: report the exchange terms of the
+        breakdown as the modelled NVLink 5 all-to-all (sp_ctx_set_comm_model)
+        instead of the device-local copy's time."""
+        check(lib().sp_ctx_set_comm_model(self._h, 1 if on else 0))
+
     def set_overlap(self, on: bool):
         """Backward sort on the side stream concurrently with the forward
         (default) or serialised behind it (sp_ctx_set_overlap)."""
@@ -636,15 +655,24 @@ class MeasuredCostProvider(CostProvider):
     GPU — all D virtual devices, real K1/K4 kernels on the synthetic batch of
     the task — and returns median stage times over `iters` iterations after
     `warmup`. cost_features returns per device (fwd_ms, bwd_ms, comm_ms);
-    a device with no tables reports (0, 0, 0) like oracle.hpp:242-269."""
+    a device with no tables reports (0, 0, 0) like oracle.hpp:242-269.
+
+    One GPU cannot time NVLink, so with comm_model (default) the comm terms
+    are the modelled NVLink 5 all-to-all (sp_comm_model: the B200
+    counterpart of device_comm, oracle.hpp:178-185) instead of the
+    emulation's device-local copy: comm_ms of a device = its send side
+    (its own tables only, like device_comm); overall = max fwd + the two
+    modelled stages + max bwd. Synthetic data is keyed by table id, so a
+    table brings the same batch to every partial assignment."""
 
     def __init__(self, task: PlacementTask, seed: int = 2210, iters: int = 5, warmup: int = 2,
-                 device: int = 0):
+                 device: int = 0, comm_model: bool = True):
         self.task = task
         self.seed = seed
         self.iters = iters
         self.warmup = warmup
         self.device = device
+        self.comm_model = comm_model
         self.calls = 0
 
     def _measure(self, placement: np.ndarray, subset: np.ndarray) -> CostBreakdown:
@@ -653,6 +681,7 @@ class MeasuredCostProvider(CostProvider):
                                  self.task.batch_size)
         shard = EmbeddingShard(sub_task, placement[subset], device=self.device)
         try:
+            shard.set_comm_model(self.comm_model)
             shard.init_tables(self.seed)
             shard.synth_batch(self.seed)
             shard.synth_grad(self.seed)
@@ -681,8 +710,17 @@ class MeasuredCostProvider(CostProvider):
         if len(subset) == 0:
             return [(0.0, 0.0, 0.0)] * D
         bd = self._measure(placement, subset)
-        return [(bd.fwd_ms[d], bd.bwd_ms[d], bd.comm_ms[d]) if len(assignment[d]) else
-                (0.0, 0.0, 0.0) for d in range(D)]
+        out = []
+        for d in range(D):
+            if not len(assignment[d]):
+                out.append((0.0, 0.0, 0.0))
+                continue
+            comm = bd.comm_ms[d]
+            if self.comm_model:
+                w = sum(self.task.tables[i].dim for i in assignment[d])
+                comm = comm_model_ms(self.task.batch_size, w, -1, D)
+            out.append((bd.fwd_ms[d], bd.bwd_ms[d], comm))
+        return out
 
     def overall(self, placement):
         self.calls += 1

@@ -195,6 +195,7 @@ struct sp_ctx {
   cudaGraphExec_t graph_exec = nullptr;
   int graph_kernels = 0;
   bool profiling = false;            // per-kernel events (sp_ctx_set_profiling)
+  bool comm_model = false;           // emulation: modelled NVLink exchange (sp_ctx_set_comm_model)
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   struct Mark { int cls; size_t a, b; };
@@ -950,7 +951,7 @@ int sp_init_tables(sp_ctx* ctx, uint64_t seed) {
     for (auto& v : ctx->vdevs)
       for (int g : v.tables)
         launch_init_weights(wptr(ctx, g), ctx->wt, ctx->tables[g].hash_size,
-                            ctx->tables[g].dim, g, seed, ctx->stream);
+                            ctx->tables[g].dim, ctx->tables[g].id, seed, ctx->stream);
     SP_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -1317,7 +1318,7 @@ int sp_synth_batch(sp_ctx* ctx, uint64_t seed) {
       std::vector<uint64_t> thr(T);
       for (int li = 0; li < T; ++li) {
         const auto& t = c->tables[v.tables[li]];
-        gid[li] = v.tables[li];
+        gid[li] = t.id;  // the generator is keyed by the table's id
         lmax[li] = static_cast<int64_t>(std::floor(2.0 * t.pooling_factor));
         rows[li] = t.hash_size;
         double h = 0.0;  // hot_mass (oracle.hpp:119-123)
@@ -1583,6 +1584,22 @@ void timed_exchange_and_backward(sp_ctx* c, bool ov, const int32_t* abort_flag) 
 // Per-stage device times of the iteration just synchronised (events ev[0..7]
 // of every (virtual) device, ev_a2a in NCCL mode), gathered over ranks and
 // composed like CostOracle::evaluate_placement (oracle.hpp:222-227).
+// The B200 counterpart of device_comm (oracle.hpp:178-185) for one GPU
+// emulating D: a MODEL, not a measurement. One direction of the
+// all-to-all moves, per device, 4 B W_d (D-1)/D bytes out and
+// 4 (B/D) (W_tot - W_d) bytes in over full-duplex NVLink 5 through
+// NVSwitch (every peer at full rate), so the device's stage time is the
+// larger of the two at the measured per-direction peer bandwidth of this
+// pool's B200s (770 GB/s, B200_PROFILING.md; 900 nominal) plus a fixed
+// grouped send/recv latency. width_total < 0: the send side only (a device's
+// own tables alone, as device_comm and partial_cost_features use it).
+double comm_model_ms(int64_t B, int64_t width_dev, int64_t width_total, int D) {
+  if (D <= 1 || width_dev <= 0) return 0.0;
+  const double sent = 4.0 * B * width_dev * (D - 1) / D;
+  const double recv = width_total < 0 ? 0.0 : 4.0 * (B / D) * (width_total - width_dev);
+  return SP_A2A_LATENCY_MS + std::max(sent, recv) / (SP_NVLINK_PEER_GBS * 1e6);
+}
+
 void collect_breakdown(sp_ctx* c, sp_breakdown* out) {
   const int D = c->D;
   cudaStream_t st = c->stream;
@@ -1594,6 +1611,8 @@ void collect_breakdown(sp_ctx* c, sp_breakdown* out) {
       if (multi_rank(c)) {
         cf[v.vid] = elapsed(c->ev_a2a[0], c->ev_a2a[1]);
         cb[v.vid] = elapsed(c->ev_a2a[2], c->ev_a2a[3]);
+      } else if (c->comm_model) {
+        cf[v.vid] = cb[v.vid] = comm_model_ms(c->B, v.W, c->W_total, D);
       } else {
         cf[v.vid] = elapsed(v.ev[2], v.ev[3]);
         cb[v.vid] = elapsed(v.ev[4], v.ev[5]);
@@ -1703,11 +1722,16 @@ void enqueue_batch_step(sp_ctx* c, const int64_t* offsets, const int64_t* indice
   c->has_batch = false;
   cudaStream_t st = c->stream;
   const bool ov = overlap_active(c);
-  for (auto& v : c->vdevs) SP_CUDA(cudaEventRecord(v.ev[0], st));
+  // a device's forward stage starts at its first chunk's K1 (after that
+  // chunk's upload), so in emulation no device is charged for the uploads
+  // and kernels of the devices before it
+  for (auto& v : c->vdevs)
+    if (v.tables.empty()) SP_CUDA(cudaEventRecord(v.ev[0], st));
   enqueue_upload(
       c, offsets, indices,
       [&](VDev& v, int t0, int t1) {
         const int64_t k0 = v.tile_start[t0], k1 = v.tile_start[t1];
+        if (t0 == 0) SP_CUDA(cudaEventRecord(v.ev[0], st));
         {
           ProfScope prof(c, kProfFwd);
           launch_tbe_forward(v.d_meta_canon, v.d_tiles_canon + k0, k1 - k0, c->B, v.d_off,
@@ -1884,6 +1908,24 @@ int sp_exchange_plan(const sp_table_spec* tables, int32_t num_tables, int32_t nu
   });
 }
 
+int sp_ctx_set_comm_model(sp_ctx* ctx, int32_t on) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (on && multi_rank(ctx))
+      raise(SP_ERR_BAD_INPUT, "one process per GPU measures its exchange; the model is for "
+                              "one GPU emulating D devices");
+    ctx->comm_model = on != 0;
+  });
+}
+
+int sp_comm_model(int32_t batch, int64_t width_dev, int64_t width_total, int32_t D,
+                  double* ms) {
+  return guarded([&] {
+    if (!ms || batch < 1 || D < 1 || width_dev < 0) raise(SP_ERR_BAD_INPUT, "bad comm model args");
+    *ms = comm_model_ms(batch, width_dev, width_total, D);
+  });
+}
+
 int sp_ctx_set_overlap(sp_ctx* ctx, int32_t on) {
   return guarded([&] {
     check_ctx(ctx);
@@ -2018,7 +2060,7 @@ extern "C" int sp_synth_lookup_batch(const sp_table_spec* tables, int32_t num_ta
     std::vector<uint64_t> thr(T);
     for (int i = 0; i < T; ++i) {
       const auto& t = tables[i];
-      gid[i] = i;
+      gid[i] = t.id;
       lmax[i] = static_cast<int64_t>(std::floor(2.0 * t.pooling_factor));
       rows[i] = t.hash_size;
       double h = 0.0;

@@ -95,3 +95,17 @@ def test_ingest_argument_errors_before_gpu():
     with pytest.raises(ShardplanError) as e:
         ingest_lookup_batch(LookupBatch(np.array([1, 2]), np.array([1, 2, 2]), 1, 2), [4], [10])
     assert e.value.kind == "malformed_batch"
+
+
+def test_comm_model_is_host_only_and_matches_formula():
+    """sp_comm_model (the NVLink 5 all-to-all model used when one GPU
+    emulates D devices) needs no GPU; send side vs receive side."""
+    from paper_2210_02023_b200 import api
+    B, D = 65536, 8
+    lat, bw = api.A2A_LATENCY_MS, api.NVLINK_PEER_GBS
+    sent = 4.0 * B * 800 * (D - 1) / D
+    assert abs(api.comm_model_ms(B, 800, -1, D) - (lat + sent / (bw * 1e6))) < 1e-12
+    recv = 4.0 * (B // D) * (6224 - 800)
+    assert abs(api.comm_model_ms(B, 800, 6224, D) - (lat + max(sent, recv) / (bw * 1e6))) < 1e-12
+    assert api.comm_model_ms(B, 800, 6224, 1) == 0.0
+    assert api.comm_model_ms(B, 0, 6224, 8) == 0.0
