@@ -130,6 +130,21 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
                   int32_t batch_size, double mem_cap_gb, float lr,
                   int32_t rank, int32_t world_size, const uint8_t* nccl_id,
                   int32_t cuda_device, sp_ctx** out);
+/* sp_ctx_create with an explicit table storage type. SP_STORAGE_AUTO
+ * (what sp_ctx_create does) follows the tables' sizing: 2 B/param -> fp16,
+ * 4 B/param (or unsized) -> fp32. SP_STORAGE_BF16 stores 2 B/param tables
+ * as bfloat16 (same bytes, fp32's exponent range). Pooled outputs,
+ * gradients and every sum stay fp32; a sizing that disagrees with the type
+ * is SP_ERR_BAD_INPUT. */
+#define SP_STORAGE_AUTO 0
+#define SP_STORAGE_F32 1
+#define SP_STORAGE_F16 2
+#define SP_STORAGE_BF16 3
+int sp_ctx_create_ex(const sp_table_spec* tables, int32_t num_tables,
+                     int32_t num_devices, const int32_t* placement,
+                     int32_t batch_size, double mem_cap_gb, float lr,
+                     int32_t rank, int32_t world_size, const uint8_t* nccl_id,
+                     int32_t cuda_device, int32_t storage, sp_ctx** out);
 void sp_ctx_destroy(sp_ctx* ctx);
 
 /* cudaStream_t the context launches on (as void*). */

@@ -27,6 +27,8 @@ SIGNATURES = {
     "sp_nccl_unique_id": (c_i32, [c_vp]),
     "sp_ctx_create": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_i32, c_f64, c_f32, c_i32,
                               c_i32, c_vp, c_i32, P(c_vp)]),
+    "sp_ctx_create_ex": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_i32, c_f64, c_f32, c_i32,
+                                 c_i32, c_vp, c_i32, c_i32, P(c_vp)]),
     "sp_ctx_destroy": (None, [c_vp]),
     "sp_ctx_stream": (c_i32, [c_vp, P(c_vp)]),
     "sp_ctx_device_bytes": (c_i32, [c_vp, P(c_u64)]),

@@ -368,11 +368,15 @@ class EmbeddingShard:
 
     world_size == num_devices: one process per GPU, exchanges over NCCL.
     world_size == 1 < num_devices: emulation, all virtual devices on this GPU
-    (compute measured per device; exchange is a device-local copy)."""
+    (compute measured per device; exchange is a device-local copy).
+    storage: "auto" (2 B/param tables -> fp16, else fp32), "fp32", "fp16",
+    "bf16" (sp_ctx_create_ex)."""
+
+    STORAGE = {"auto": 0, "fp32": 1, "fp16": 2, "bf16": 3}  # SP_STORAGE_*
 
     def __init__(self, task: PlacementTask, placement: Sequence[int], lr: float = 0.01,
                  rank: int = 0, world_size: int = 1, nccl_id: Optional[bytes] = None,
-                 device: int = 0):
+                 device: int = 0, storage: str = "auto"):
         self.task = task
         self.placement = np.ascontiguousarray(placement, dtype=np.int32)
         if len(self.placement) != len(task.tables):
@@ -388,9 +392,12 @@ class EmbeddingShard:
         idb = None
         if nccl_id is not None:
             idb = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
-        check(lib().sp_ctx_create(self._specs, len(task.tables), self.D, _ptr(self.placement),
-                                  self.B, float(task.mem_cap_gb), float(lr), rank, world_size,
-                                  idb, device, ctypes.byref(h)))
+        if storage not in self.STORAGE:
+            raise ShardplanError(10, f"storage must be one of {sorted(self.STORAGE)}")
+        check(lib().sp_ctx_create_ex(self._specs, len(task.tables), self.D,
+                                     _ptr(self.placement), self.B, float(task.mem_cap_gb),
+                                     float(lr), rank, world_size, idb, device,
+                                     self.STORAGE[storage], ctypes.byref(h)))
         self._h = h
 
     def close(self):

@@ -613,6 +613,15 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
                   int32_t batch_size, double mem_cap_gb, float lr,
                   int32_t rank, int32_t world_size, const uint8_t* nccl_id,
                   int32_t cuda_device, sp_ctx** out) {
+  return sp_ctx_create_ex(tables, num_tables, num_devices, placement, batch_size, mem_cap_gb,
+                          lr, rank, world_size, nccl_id, cuda_device, SP_STORAGE_AUTO, out);
+}
+
+int sp_ctx_create_ex(const sp_table_spec* tables, int32_t num_tables,
+                     int32_t num_devices, const int32_t* placement,
+                     int32_t batch_size, double mem_cap_gb, float lr,
+                     int32_t rank, int32_t world_size, const uint8_t* nccl_id,
+                     int32_t cuda_device, int32_t storage, sp_ctx** out) {
   return guarded([&] {
     if (out == nullptr) raise(SP_ERR_BAD_INPUT, "null output handle");
     *out = nullptr;
@@ -701,8 +710,10 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
 
     // Storage type from the tables' own sizing: table_size_gb =
     // rows * dim * bytes_per_param / 2^30 (table_memory_gb, table.hpp:55-63):
-    // 2 B/param (the reference's default, the paper's fp16 tables) -> fp16,
-    // 4 B/param -> fp32; one type per context.
+    // 2 B/param (the reference's default, the paper's fp16 tables) -> fp16
+    // (or bf16 when asked for), 4 B/param -> fp32; one type per context.
+    if (storage < SP_STORAGE_AUTO || storage > SP_STORAGE_BF16)
+      raise(SP_ERR_BAD_INPUT, "unknown storage type");
     {
       int bpp_all = 0;
       for (int i = 0; i < num_tables; ++i) {
@@ -719,7 +730,17 @@ int sp_ctx_create(const sp_table_spec* tables, int32_t num_tables,
           raise(SP_ERR_BAD_INPUT, "tables mix 2 and 4 bytes/param");
         bpp_all = b;
       }
-      c->wt = bpp_all == 2 ? WeightType::kF16 : WeightType::kF32;
+      if (storage == SP_STORAGE_AUTO)
+        c->wt = bpp_all == 2 ? WeightType::kF16 : WeightType::kF32;
+      else if (storage == SP_STORAGE_F32)
+        c->wt = WeightType::kF32;
+      else
+        c->wt = storage == SP_STORAGE_F16 ? WeightType::kF16 : WeightType::kBF16;
+      const int want_b = c->wt == WeightType::kF32 ? 4 : 2;
+      if (bpp_all != 0 && bpp_all != want_b)
+        raise(SP_ERR_BAD_INPUT, "tables are sized at " + std::to_string(bpp_all) +
+                                    " bytes/param but the storage type has " +
+                                    std::to_string(want_b));
     }
     // Weight slab.
     const int64_t eb = elem_bytes(c->wt);

@@ -241,6 +241,35 @@ template <> struct Slice<__half> {
     atomicAdd(p, __float2half_rn(d));
   }
 };
+// bf16 tables (2 B/param like fp16, fp32's exponent range): widening is a
+// 16-bit shift; the update is REDG.ADD.BF16x8 (round-to-nearest at L2)
+template <> struct Slice<__nv_bfloat16> {
+  static constexpr int E = 8;
+  __device__ static __forceinline__ void load(const __nv_bfloat16* p, float (&v)[8]) {
+    const uint4 x = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[2 * k] = __uint_as_float(w4[k] << 16);
+      v[2 * k + 1] = __uint_as_float(w4[k] & 0xffff0000u);
+    }
+  }
+  __device__ static __forceinline__ void red_add(__nv_bfloat16* p, const float (&d)[8]) {
+    uint32_t u[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const __nv_bfloat162 h = __floats2bfloat162_rn(d[2 * k], d[2 * k + 1]);
+      u[k] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    asm volatile("red.global.add.noftz.v4.bf16x2 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(u[0]),
+                 "r"(u[1]), "r"(u[2]), "r"(u[3])
+                 : "memory");
+  }
+  __device__ static __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+  __device__ static __forceinline__ void red_add1(__nv_bfloat16* p, float d) {
+    atomicAdd(p, __float2bfloat16_rn(d));
+  }
+};
 
 // kPeer: a compile-time path, so the local store path stays exactly the
 // plain `out + b * ld` (a runtime branch on a by-value row-map parameter cost
@@ -1058,6 +1087,10 @@ __global__ void sgd_carry_kernel(const TableMeta* __restrict__ meta,
 
 __device__ __forceinline__ void store_w(float* p, float v) { *p = v; }
 __device__ __forceinline__ void store_w(__half* p, float v) { *p = __float2half_rn(v); }
+__device__ __forceinline__ void store_w(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+__device__ __forceinline__ float load_w(float x) { return x; }
+__device__ __forceinline__ float load_w(__half x) { return __half2float(x); }
+__device__ __forceinline__ float load_w(__nv_bfloat16 x) { return __bfloat162float(x); }
 
 template <class T>
 __global__ void init_weights_kernel(T* __restrict__ w, int64_t rows,
@@ -1072,18 +1105,18 @@ __global__ void init_weights_kernel(T* __restrict__ w, int64_t rows,
   }
 }
 
-// fp32 host rows <-> fp16 device rows (set_table / get_table)
-__global__ void f32_to_f16_kernel(const float* __restrict__ src, __half* __restrict__ dst,
-                                  int64_t n) {
+// fp32 host rows <-> 2-byte device rows (set_table / get_table)
+template <class T>
+__global__ void f32_to_w_kernel(const float* __restrict__ src, T* __restrict__ dst, int64_t n) {
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    dst[e] = __float2half_rn(src[e]);
+    store_w(dst + e, src[e]);
 }
-__global__ void f16_to_f32_kernel(const __half* __restrict__ src, float* __restrict__ dst,
-                                  int64_t n) {
+template <class T>
+__global__ void w_to_f32_kernel(const T* __restrict__ src, float* __restrict__ dst, int64_t n) {
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    dst[e] = __half2float(src[e]);
+    dst[e] = load_w(src[e]);
 }
 
 __global__ void synth_lengths_kernel(const int32_t* __restrict__ gid,
@@ -1193,9 +1226,13 @@ void launch_tbe_forward(const TableMeta* d_meta_canon, const int4* d_tiles,
   };
   using F32 = TypeTag<float>;
   using F16 = TypeTag<__half>;
+  using BF16 = TypeTag<__nv_bfloat16>;
   if (wt == WeightType::kF16) {
     if (d_peer) go(std::true_type{}, F16{});
     else go(std::false_type{}, F16{});
+  } else if (wt == WeightType::kBF16) {
+    if (d_peer) go(std::true_type{}, BF16{});
+    else go(std::false_type{}, BF16{});
   } else {
     if (d_peer) go(std::true_type{}, F32{});
     else go(std::false_type{}, F32{});
@@ -1270,6 +1307,9 @@ void launch_sgd(const TableMeta* d_meta_canon, const int* d_tiles, const int64_t
   if (wt == WeightType::kF16) {
     if (bags16) go(TypeTag<__half>{}, TypeTag<uint16_t>{});
     else go(TypeTag<__half>{}, TypeTag<uint32_t>{});
+  } else if (wt == WeightType::kBF16) {
+    if (bags16) go(TypeTag<__nv_bfloat16>{}, TypeTag<uint16_t>{});
+    else go(TypeTag<__nv_bfloat16>{}, TypeTag<uint32_t>{});
   } else {
     if (bags16) go(TypeTag<float>{}, TypeTag<uint16_t>{});
     else go(TypeTag<float>{}, TypeTag<uint32_t>{});
@@ -1283,6 +1323,9 @@ void launch_init_weights(void* d_w, WeightType wt, int64_t rows, int dim, int32_
   if (wt == WeightType::kF16)
     init_weights_kernel<__half><<<grid_for(rows * dim, 256), 256, 0, st>>>(
         static_cast<__half*>(d_w), rows, dim, gid, seed);
+  else if (wt == WeightType::kBF16)
+    init_weights_kernel<__nv_bfloat16><<<grid_for(rows * dim, 256), 256, 0, st>>>(
+        static_cast<__nv_bfloat16*>(d_w), rows, dim, gid, seed);
   else
     init_weights_kernel<float><<<grid_for(rows * dim, 256), 256, 0, st>>>(
         static_cast<float*>(d_w), rows, dim, gid, seed);
@@ -1293,7 +1336,11 @@ void launch_f32_to_weights(const float* d_src, void* d_dst, WeightType wt, int64
                            cudaStream_t st) {
   if (n <= 0) return;
   if (wt == WeightType::kF16) {
-    f32_to_f16_kernel<<<grid_for(n, 256), 256, 0, st>>>(d_src, static_cast<__half*>(d_dst), n);
+    f32_to_w_kernel<<<grid_for(n, 256), 256, 0, st>>>(d_src, static_cast<__half*>(d_dst), n);
+    SP_LAUNCHED();
+  } else if (wt == WeightType::kBF16) {
+    f32_to_w_kernel<<<grid_for(n, 256), 256, 0, st>>>(d_src, static_cast<__nv_bfloat16*>(d_dst),
+                                                      n);
     SP_LAUNCHED();
   } else {
     SP_CUDA(cudaMemcpyAsync(d_dst, d_src, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
@@ -1304,8 +1351,11 @@ void launch_weights_to_f32(const void* d_src, WeightType wt, float* d_dst, int64
                            cudaStream_t st) {
   if (n <= 0) return;
   if (wt == WeightType::kF16) {
-    f16_to_f32_kernel<<<grid_for(n, 256), 256, 0, st>>>(static_cast<const __half*>(d_src),
-                                                        d_dst, n);
+    w_to_f32_kernel<<<grid_for(n, 256), 256, 0, st>>>(static_cast<const __half*>(d_src), d_dst, n);
+    SP_LAUNCHED();
+  } else if (wt == WeightType::kBF16) {
+    w_to_f32_kernel<<<grid_for(n, 256), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(d_src),
+                                                      d_dst, n);
     SP_LAUNCHED();
   } else {
     SP_CUDA(cudaMemcpyAsync(d_dst, d_src, n * sizeof(float), cudaMemcpyDeviceToDevice, st));

@@ -2,6 +2,7 @@
 // the launchers of the hot kernels (K1 forward, K4 backward).
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -26,8 +27,8 @@ struct TableMeta {
 // Storage type of the embedding rows: fp32 (4 B/param) or fp16 (2 B/param,
 // the paper's tables, and table_memory_gb's default,
 // table.hpp:30). Pooled outputs, gradients and all sums stay fp32.
-enum class WeightType : int32_t { kF32 = 0, kF16 = 1 };
-inline int elem_bytes(WeightType t) { return t == WeightType::kF16 ? 2 : 4; }
+enum class WeightType : int32_t { kF32 = 0, kF16 = 1, kBF16 = 2 };
+inline int elem_bytes(WeightType t) { return t == WeightType::kF32 ? 4 : 2; }
 
 // Row class by row bytes: 0..5 for 16, 32, ..., 512-byte rows (whole 16-byte
 // slices: fp32 dims 4..128, fp16 dims 8..256), -1 = the generic path.
