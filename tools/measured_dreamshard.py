@@ -39,14 +39,18 @@ def load(config, D):
 
 
 def measure(task, placement, device=0):
+    """(max-over-device fwd + bwd compute, the metric with the exchange
+    stages from the NVLink 5 model): median of 5 after one warm-up."""
     sh = api.EmbeddingShard(task, placement, lr=0.01, device=device)
+    sh.set_comm_model(True)
     sh.init_tables(2210)
     sh.synth_batch(2210)
     sh.synth_grad(2210)
     runs = sorted((sh.run_iteration() for _ in range(6)), key=lambda b: b.overall_ms)[1:]
     bd = runs[2]
     sh.close()
-    return round(max(bd.fwd_ms) + max(bd.bwd_ms), 4)
+    return {"compute_ms": round(max(bd.fwd_ms) + max(bd.bwd_ms), 4),
+            "overall_ms": round(bd.overall_ms, 4)}
 
 
 def main():
@@ -90,9 +94,13 @@ def main():
     out = {"train_seconds": round(train_s, 1), "iterations": args.iterations,
            "train_tables": args.tables, "train_devices": args.devices,
            "oracle_checkpoint": os.path.basename(oracle_ckpt),
-           "train_metrics": metrics, "max_device_compute_ms": results,
-           "note": "placements measured on one B200 with every device emulated: max over "
-                   "devices of the measured fwd + bwd compute (exchange excluded), median of 5"}
+           "train_metrics": metrics, "placements": results,
+           "note": "placements measured on one B200 with every device emulated: compute_ms = "
+                   "max over devices of the measured fwd + bwd compute; overall_ms = that plus "
+                   "the two all-to-all stages from the NVLink 5 model (sp_comm_model: 770 GB/s "
+                   "per direction + 10 us; a model, not a measurement), median of 5. The "
+                   "measured checkpoint is trained with the same comm term "
+                   "(MeasuredCostProvider comm_model)"}
     name = f"measured_dreamshard_m{args.tables}_d{args.devices}.json"
     with open(os.path.join(args.out, name), "w") as f:
         json.dump(out, f, indent=1)
