@@ -97,6 +97,14 @@ struct Geo {
 #define SP_FWD_G4 16, 1, 2, 8
 #define SP_FWD_G5 32, 1, 1, 8
 #endif
+// K1 fp32 with 32-byte slices (Slice256F): half the lanes per row of the
+// 16-byte geometry and half the rows in flight (the same bytes per lane).
+// Only the 64 B class (dim 16) gains at cfg3 (K1 1.418 -> 1.405 ms); the
+// 128 B class alone -0.8 %, both together 0, and the 256 / 512 B classes
+// raise K1 to 43-48 registers (40 warps/SM) and lose 6-19 %.
+constexpr unsigned kFwd256Classes = 1u << 2;
+template <int CLS> struct FwdGeo256 : Geo<1, 1, 8, 4> {};  // classes not in kFwd256Classes
+template <> struct FwdGeo256<2> : Geo<2, 1, 4, 2> {};
 template <int CLS> struct FwdGeo;
 template <> struct FwdGeo<0> : Geo<SP_FWD_G0> {};
 template <> struct FwdGeo<1> : Geo<SP_FWD_G1> {};
@@ -271,6 +279,21 @@ template <> struct Slice<__nv_bfloat16> {
   }
 };
 
+// fp32 rows gathered in 32-byte lane slices (LDG.E.256, new on sm_100):
+// the same bytes in flight with half the load instructions. Isolated random
+// rows (profiles/microbench/rows256.cu): 128 B 4.65 -> 5.56 TB/s, 256-512 B
+// +2-4 %, 64 B +4 %; inside K1 see kFwd256Classes. K1 only: vector
+// reductions stop at 128 bits.
+struct Slice256F {
+  static constexpr int E = 8;
+  __device__ static __forceinline__ void load(const float* p, float (&v)[8]) {
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+          "=f"(v[7])
+        : "l"(p));
+  }
+};
+
 // kPeer: a compile-time path, so the local store path stays exactly the
 // plain `out + b * ld` (a runtime branch on a by-value row-map parameter cost
 // K1 6% at cfg3). The peer map lives in device memory.
@@ -284,7 +307,7 @@ __device__ __forceinline__ float* out_row(float* out, const RowMap* __restrict__
 
 // kStaged: every position of the tile is in s_idx (np <= kIdxCap), so the
 // index fetch has no per-slot bound check against the staging capacity.
-template <class G, bool kPeer, class T, bool kStaged = false>
+template <class G, bool kPeer, class T, bool kStaged = false, class SL = Slice<T>>
 __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb,
                                               int p0, int warp, int lane,
                                               const int32_t* s_off,
@@ -295,7 +318,7 @@ __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb
                                               const RowMap* __restrict__ peer,
                                               int64_t ldo) {
   constexpr int L = G::L, V = G::V, P = G::P, U = G::U, S = G::S, GB = G::GB;
-  constexpr int E = Slice<T>::E;
+  constexpr int E = SL::E;
   const int span = lane / S, ls = lane % S, g = ls / L, s = ls % L;
   const T* wt = w + m.woff + E * s;  // lane s moves slices s, s+L, s+2L, ... (coalesced)
   const int dim = m.dim;
@@ -328,7 +351,7 @@ __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb
 #pragma unroll
         for (int j = 0; j < V; ++j) {
           if (r[u] >= 0) {
-            Slice<T>::load(wt + static_cast<int64_t>(r[u]) * dim + E * L * j, v[u][j]);
+            SL::load(wt + static_cast<int64_t>(r[u]) * dim + E * L * j, v[u][j]);
           } else {
 #pragma unroll
             for (int e = 0; e < E; ++e) v[u][j][e] = 0.f;
@@ -406,12 +429,21 @@ __global__ void __launch_bounds__(kBlockThreads)
   switch (m.cls) {
 #define SP_FWD_CASE(C)                                                                    \
   case C:                                                                                 \
-    if (SP_FWD_STAGED && np <= kIdxCap)                                                   \
-      fwd_tile_warp<FwdG<C, T>, kPeer, T, true>(m, tile.b0, tile.nb, p0, warp, lane, s_off, \
-                                                s_idx, idx, w, out, peer, ldo);           \
-    else                                                                                  \
-      fwd_tile_warp<FwdG<C, T>, kPeer, T>(m, tile.b0, tile.nb, p0, warp, lane, s_off,      \
-                                          s_idx, idx, w, out, peer, ldo);                 \
+    if constexpr (std::is_same<T, float>::value && ((kFwd256Classes >> C) & 1)) {        \
+      if (np <= kIdxCap)                                                                  \
+        fwd_tile_warp<FwdGeo256<C>, kPeer, T, true, Slice256F>(                           \
+            m, tile.b0, tile.nb, p0, warp, lane, s_off, s_idx, idx, w, out, peer, ldo);   \
+      else                                                                                \
+        fwd_tile_warp<FwdGeo256<C>, kPeer, T, false, Slice256F>(                          \
+            m, tile.b0, tile.nb, p0, warp, lane, s_off, s_idx, idx, w, out, peer, ldo);   \
+    } else {                                                                              \
+      if (SP_FWD_STAGED && np <= kIdxCap)                                                 \
+        fwd_tile_warp<FwdG<C, T>, kPeer, T, true>(m, tile.b0, tile.nb, p0, warp, lane,      \
+                                                  s_off, s_idx, idx, w, out, peer, ldo);  \
+      else                                                                                \
+        fwd_tile_warp<FwdG<C, T>, kPeer, T>(m, tile.b0, tile.nb, p0, warp, lane, s_off,    \
+                                            s_idx, idx, w, out, peer, ldo);               \
+    }                                                                                     \
     break;
     SP_FWD_CASE(0)
     SP_FWD_CASE(1)

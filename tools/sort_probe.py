@@ -1,5 +1,8 @@
 """Runs the K4a sort of the cfg3 batch (D = 1) a few times: a target for
-ncu (`-k regex:sort_`) and a quick CUDA-event timing of the sort alone."""
+ncu (`-k regex:sort_`) and a quick CUDA-event timing of the sort alone
+(kernels serialised: K1, then the sort, then the SGD), after two warm-up
+iterations. SP_LIBRARY selects an A/B build of the library.
+    python tools/sort_probe.py [config] [reps]"""
 import json
 import os
 import sys
@@ -21,8 +24,13 @@ sh.synth_batch(SEED)
 sh.synth_grad(SEED)
 sh.set_overlap(False)
 sh.set_profiling(True)
+for _ in range(2):
+    sh.enqueue_iteration()
+sh.kernel_ms()
 for _ in range(reps):
     sh.enqueue_iteration()
 k = sh.kernel_ms()
-print(json.dumps({n: round(v[0] / max(1, v[1]), 4) for n, v in k.items()}))
+out = {n: round(v[0] / max(1, v[1]), 4) for n, v in k.items()}
+out["lib"] = os.path.basename(os.environ.get("SP_LIBRARY", "_shardplan_b200.so"))
+print(json.dumps(out))
 sh.close()
