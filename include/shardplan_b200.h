@@ -257,11 +257,13 @@ int sp_get_sorted(sp_ctx* ctx, int32_t dev, uint32_t* keys, uint32_t* bags,
  * arrays hold every rank's numbers (gathered), identical on all ranks. */
 int sp_run_iteration(sp_ctx* ctx, sp_breakdown* out);
 /* This context's compute of one iteration without the exchanges: ms[0] =
- * the forward stage (K1 with the backward's key build and sort overlapped,
- * as in sp_run_iteration), ms[1] = the backward stage (SGD on the resident
- * gradient). Measures one rank of a multi-GPU placement on its own (no NCCL
- * id or peers needed) — the compute part of that rank's CostBreakdown. */
-int sp_run_local(sp_ctx* ctx, double ms[2]);
+ * the forward stage (K1), ms[1] = the backward stage (SGD on the resident
+ * gradient, after waiting for the sort), ms[2] = the backward sort alone
+ * (side stream, forked after K1 as in sp_run_iteration, where it runs
+ * under the exchanges; 0 when the overlap is off and the sort is inside
+ * ms[1]). Measures one rank of a multi-GPU placement on its own (no NCCL id
+ * or peers needed) — the compute part of that rank's CostBreakdown. */
+int sp_run_local(sp_ctx* ctx, double ms[3]);
 /* sp_upload_batch + sp_run_iteration in one call, pipelined: the H2D of the
  * host LookupBatch overlaps the forward of the tables already on the device
  * (and, with one device per context, their backward sort). The device-side

@@ -531,11 +531,15 @@ class EmbeddingShard:
         return CostBreakdown(list(f), list(b), list(c), bd.fwd_comm_stage_ms,
                              bd.bwd_comm_stage_ms, bd.overall_ms)
 
-    def run_local(self):
+    def run_local(self, with_sort: bool = False):
         """This shard's compute of one iteration, exchanges left out:
-        (forward-stage ms, backward-stage ms) (sp_run_local)."""
-        ms = np.zeros(2)
+        (forward-stage ms, backward-stage ms[, sort ms]) (sp_run_local). The
+        backward stage waits for the sort, which in a multi-GPU iteration
+        runs under the exchanges."""
+        ms = np.zeros(3)
         check(lib().sp_run_local(self._h, _ptr(ms)))
+        if with_sort:
+            return float(ms[0]), float(ms[1]), float(ms[2])
         return float(ms[0]), float(ms[1])
 
     def run_batch(self, b: LookupBatch) -> CostBreakdown:

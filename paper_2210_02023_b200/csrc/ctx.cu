@@ -507,8 +507,12 @@ void barrier(sp_ctx* c) {
 
 bool exchange_needed(const sp_ctx* c) { return c->D > 1; }
 
-// Fork: the side stream sorts the batch's lookups while the main stream runs
-// the forward and the exchanges.
+// Fork, after K1: the side stream sorts the batch's lookups while the main
+// stream runs the exchanges (NVLink-bound, a few SMs), joined before the SGD.
+// Not concurrently with K1: both fill every SM, and at cfg3 D=1 the
+// concurrent sort slowed the iteration 3.87 -> 4.02 ms (K1 loses resident
+// warps and L2 to it); with no exchange (one device) the sort simply
+// follows K1.
 void fork_sort(sp_ctx* c) {
   SP_CUDA(cudaEventRecord(c->ev_fork, c->stream));
   SP_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
@@ -518,11 +522,11 @@ void fork_sort(sp_ctx* c) {
 
 void join_sort(sp_ctx* c) { SP_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0)); }
 
-// Stage 1 of an iteration: the forward, with the backward sort forked onto
+// Stage 1 of an iteration: the forward, then the backward sort forked onto
 // the side stream when the overlap is active.
 void forward_stage(sp_ctx* c, bool ov) {
-  if (ov) fork_sort(c);
   for (auto& v : c->vdevs) stage_forward(c, v);
+  if (ov) fork_sort(c);
 }
 
 void enqueue_iteration(sp_ctx* c) {
@@ -1677,11 +1681,12 @@ void collect_breakdown(sp_ctx* c, sp_breakdown* out) {
 extern "C" {
 
 // This context's compute of one iteration with the exchanges left out: the
-// forward stage (K1, with the backward's key build and sort overlapped on
-// the side streams exactly as in sp_run_iteration) and the backward stage
-// (join + SGD on the resident gradient). One rank of a multi-GPU placement
-// can be measured alone this way (no NCCL id or peers needed).
-int sp_run_local(sp_ctx* ctx, double ms[2]) {
+// forward stage (K1), the backward stage (join + SGD on the resident
+// gradient) and the sort (forked after K1 as in sp_run_iteration; with no
+// exchange to run under, the backward stage waits for it). One rank of a
+// multi-GPU placement can be measured alone this way (no NCCL id or peers
+// needed).
+int sp_run_local(sp_ctx* ctx, double ms[3]) {
   return guarded([&] {
     check_ctx(ctx);
     require_batch(ctx);
@@ -1697,6 +1702,8 @@ int sp_run_local(sp_ctx* ctx, double ms[2]) {
     for (auto& v : c->vdevs) stage_backward(c, v, ov);
     SP_CUDA(cudaEventRecord(v0.ev[7], st));
     SP_CUDA(cudaStreamSynchronize(st));
+    if (c->side) SP_CUDA(cudaStreamSynchronize(c->side));
+    ms[2] = ov ? elapsed(c->ev_fork, c->ev_join) : 0.0;
     ms[0] = elapsed(v0.ev[0], v0.ev[1]);
     ms[1] = elapsed(v0.ev[1], v0.ev[7]);
   });

@@ -2,16 +2,16 @@
 //
 //   K1 tbe_forward_kernel — fused multi-table sum-pooled EmbeddingBag
 //      forward (the reference's fused_kernel stage, oracle.hpp:163-174,
-//      executed for real). Optionally emits the backward's sort pairs; with
-//      peer memory its stores land at the receiving ranks (the forward
-//      all-to-all fused into the lookup).
-//   K4 build_keys (when K1 did not emit them) -> CUB stable radix sort per
-//      sort group -> sgd_kernel — the backward (oracle.hpp:149 bwd_comp):
-//      duplicate rows are reduced in the sorted (= original) order and every
-//      unique row gets one L2 vector-reduction update.
+//      executed for real). With peer memory its stores land at the
+//      receiving ranks (the forward all-to-all fused into the lookup).
+//   K4 the backward (oracle.hpp:149 bwd_comp): the stable sort of sort.cu
+//      (K4a), then sgd_seg_kernel / sgd_kernel (K4b): duplicate rows are
+//      reduced in the sorted (= original) order and every unique row gets
+//      one L2 vector-reduction update.
 //
-// Both are HBM-bound random row gathers / updates over fp32 or fp16 tables
-// (16-byte row slices, Slice<T>). K1: a block owns a tile of consecutive bags
+// Both are HBM-bound random row gathers / updates over fp32, fp16 or bf16
+// tables (16-byte row slices, Slice<T>; 32-byte for K1's fp32 64 B rows,
+// Slice256F). K1: a block owns a tile of consecutive bags
 // of one table, its offsets/indices staged in shared memory with coalesced
 // loads; a warp is split into P spans (one bag each), a span into GB groups
 // of L lanes, each lane moving one 16-byte slice with U rows in flight.
@@ -193,7 +193,6 @@ struct FwdTile {
   int32_t pad;
 };
 
-constexpr int kTileBags = 256;  // build_keys block (bags per block)
 #ifndef SP_FWD_TILE_BAGS
 #define SP_FWD_TILE_BAGS 128  // 256: 1.634 ms, 128: 1.607, 64: 1.630 (K1 at cfg3)
 #endif
