@@ -464,9 +464,10 @@ def config_dict(args, task):
 
 def bench_evaluator_sweep(device: int, n: int = 4096):
     """BASELINE cfg5: the generalisation sweep, M in {20, 50, 100, 200} tables x
-    D in {1, 2, 4, 8} devices, 4096 greedy rollouts and 4096 cost-net scorings of
-    random placements per task on the GPU evaluator (m100_d8 checkpoint;
-    tables from the cfg3 pool, repeated for M = 200)."""
+    D in {1, 2, 4, 8} devices on the GPU evaluator (m100_d8 checkpoint; tables
+    from the cfg3 pool, repeated for M = 200): 4096 cost-net scorings of
+    distinct random placements, 4096 sampled policy rollouts (distinct
+    uniforms: distinct candidates), and the greedy rollout (Alg. 2 infer)."""
     import torch
     from paper_2210_02023_b200 import api
     ckpt = api.load_checkpoint(CKPT)
@@ -481,9 +482,12 @@ def bench_evaluator_sweep(device: int, n: int = 4096):
             ev = api.Evaluator(ckpt, task, device=device)
             rng = np.random.default_rng(M * 10 + D)
             placements = rng.integers(0, D, size=(n, M)).astype(np.int32)
+            uniforms = rng.random((n, M))
             r = {"tables": M, "devices": D}
             for name, fn in (("eval_batch_ms", lambda: ev.eval_batch(placements)),
-                             ("greedy_rollouts_ms", lambda: ev.rollout(n, "greedy"))):
+                             ("sampled_rollouts_ms", lambda: ev.rollout(n, "sample",
+                                                                        uniforms=uniforms)),
+                             ("greedy_rollout_ms", lambda: ev.rollout(1, "greedy"))):
                 fn()
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
@@ -493,7 +497,8 @@ def bench_evaluator_sweep(device: int, n: int = 4096):
             ev.close()
             rows.append(r)
     return {"candidates": n, "rows": rows,
-            "note": "host wall ms per call (4096 candidates) incl. H2D/D2H"}
+            "note": "host wall ms per call incl. H2D/D2H: 4096 distinct placements scored, "
+                    "4096 distinct sampled rollouts, one greedy rollout"}
 
 
 def bench_fp16(args, task, placement, device: int):
@@ -565,7 +570,18 @@ def bench_evaluator(args, device: int, n: int = 4096):
         out[name] = round((time.perf_counter() - t0) * 1e3, 3)
         if name != "eval_batch_ms":
             out[name.replace("_ms", "_refined")] = int(r[3])
-    out["note"] = ("host wall time per call incl. H2D/D2H; the reference's own CPU code for "
+    # K6 roofline (fp32 CUDA cores, no tensor cores: the MLPs are tiny):
+    # per candidate, each device's three 32-64-1 cost heads (2 x 3 x
+    # (32*64 + 64) FLOP) + the device reduction of M 32-wide table reprs +
+    # the overall head; the per-task table MLPs (2 x 13568 x M) run once
+    fl = n * (8 * 2 * 3 * (32 * 64 + 64) + 32 * M + 2 * (32 * 64 + 64)) + 2 * 13568 * M
+    peak_fp32 = 148 * 128 * 2 * 1.965e9
+    out["eval_batch_flop"] = fl
+    out["eval_batch_gflops"] = round(fl / (out["eval_batch_ms"] * 1e6), 1)
+    out["eval_batch_fp32_frac"] = round(fl / (out["eval_batch_ms"] * 1e-3) / peak_fp32, 4)
+    out["note"] = ("host wall time per call incl. H2D/D2H (eval_batch is latency-bound: "
+                   "4096 candidates are ~0.45 GFLOP against a 74 TFLOP/s fp32 CUDA-core "
+                   "peak); the reference's own CPU code for "
                    "the same calls, timed on this host: reference_cpu")
     ev.close()
     return out
