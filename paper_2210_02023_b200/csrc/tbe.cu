@@ -53,9 +53,6 @@ __device__ __forceinline__ float4 ldg_f4_policy(const float* ptr, uint64_t pol) 
   return v;
 }
 
-#ifndef SP_SGD_RED  // 1: apply the row update as red.global.add.v4.f32 (no W load)
-#define SP_SGD_RED 1
-#endif
 // Vector reduction at L2: fire-and-forget, the SM never waits for the row
 // (each unique row has exactly one update per launch, so the result is
 // deterministic: W + fp32(-lr * sum), round-to-nearest at L2). Measured on
@@ -127,9 +124,6 @@ template <int CLS> struct SgdGeo;
 #define SP_SGD_G4 4, 4, 8, 1
 #define SP_SGD_G5 8, 4, 4, 1
 #endif
-#ifndef SP_SGD_INTERLEAVE  // lane float4 slices: 1 interleaved (s, s+L, ..), 0 blocked
-#define SP_SGD_INTERLEAVE 1
-#endif
 template <> struct SgdGeo<0> : Geo<SP_SGD_G0> {};
 template <> struct SgdGeo<1> : Geo<SP_SGD_G1> {};
 template <> struct SgdGeo<2> : Geo<SP_SGD_G2> {};
@@ -193,10 +187,8 @@ struct FwdTile {
   int32_t pad;
 };
 
-#ifndef SP_FWD_TILE_BAGS
-#define SP_FWD_TILE_BAGS 128  // 256: 1.634 ms, 128: 1.607, 64: 1.630 (K1 at cfg3)
-#endif
-constexpr int kFwdTileBags = SP_FWD_TILE_BAGS;  // K1 tile (bags per block)
+// K1 tile (bags per block): 256: 1.634 ms, 128: 1.607, 64: 1.630 (K1 at cfg3)
+constexpr int kFwdTileBags = 128;
 constexpr int kIdxCap = 4096;  // staged indices per tile (16 KB)
 
 // 16-byte slices of a table row of element type T, widened to fp32 (K1) and
@@ -402,9 +394,6 @@ __device__ __forceinline__ void fwd_tile_warp_generic(
   }
 }
 
-#ifndef SP_FWD_STAGED
-#define SP_FWD_STAGED 1
-#endif
 template <bool kPeer, class T>
 __global__ void __launch_bounds__(kBlockThreads)
     tbe_forward_kernel(const TableMeta* __restrict__ meta,
@@ -436,7 +425,7 @@ __global__ void __launch_bounds__(kBlockThreads)
         fwd_tile_warp<FwdGeo256<C>, kPeer, T, false, Slice256F>(                          \
             m, tile.b0, tile.nb, p0, warp, lane, s_off, s_idx, idx, w, out, peer, ldo);   \
     } else {                                                                              \
-      if (SP_FWD_STAGED && np <= kIdxCap)                                                 \
+      if (np <= kIdxCap)                                                                  \
         fwd_tile_warp<FwdG<C, T>, kPeer, T, true>(m, tile.b0, tile.nb, p0, warp, lane,      \
                                                   s_off, s_idx, idx, w, out, peer, ldo);  \
       else                                                                                \
@@ -480,19 +469,10 @@ __global__ void __launch_bounds__(kBlockThreads)
 // (red.global.add.v4.f32): each unique row has exactly one writer per
 // launch, so it is deterministic, and no SM register waits for the old row.
 
-#ifndef SP_SGD_TILE
-#define SP_SGD_TILE 2048
-#endif
-#ifndef SP_SGD_LONG
-#define SP_SGD_LONG 32
-#endif
-constexpr int kTilePos = SP_SGD_TILE;  // <= 2048 (11-bit run starts)
-#ifndef SP_SEG_TILE
-#define SP_SEG_TILE 1024
-#endif
-constexpr int kSegTilePos = SP_SEG_TILE;  // segmented SGD tile (positions)
+constexpr int kTilePos = 2048;  // run-based SGD tile (positions, <= 2048: 11-bit run starts)
+constexpr int kSegTilePos = 1024;  // segmented SGD tile (positions; 2048 re-read more gradient)
 constexpr int kPosPerThread = kTilePos / kBlockThreads;
-constexpr int kLongRun = SP_SGD_LONG;  // runs at least this long are block-cooperative
+constexpr int kLongRun = 32;  // runs at least this long are block-cooperative
 constexpr int kRunChunk = 16;  // short runs claimed per warp at a time (>= max P)
 constexpr int kMaxLong = kTilePos / kLongRun + 1;
 
@@ -736,11 +716,9 @@ __device__ void sgd_tile_generic(const TableMeta& m, const SgdTile& tile, SgdSha
   }
 }
 
-#ifndef SP_SGD_MIN_BLOCKS
-#define SP_SGD_MIN_BLOCKS 4  // 4 x 256 threads per SM: <= 64 registers
-#endif
+constexpr int kSgdMinBlocks = 4;  // 4 x 256 threads per SM: <= 64 registers
 template <class BagT, class T>
-__global__ void __launch_bounds__(kBlockThreads, SP_SGD_MIN_BLOCKS)
+__global__ void __launch_bounds__(kBlockThreads, kSgdMinBlocks)
     sgd_kernel(const TableMeta* __restrict__ meta, const SgdTile* __restrict__ tiles,
                const uint32_t* __restrict__ keys, const BagT* __restrict__ bags,
                const float* __restrict__ grad, int64_t ldg, float lr,
@@ -876,10 +854,7 @@ __device__ __forceinline__ void sgd_seg_tile(const TableMeta& m, const SgdTile& 
                                              float* __restrict__ carry_f,
                                              int32_t* __restrict__ carry_i, int64_t slot) {
   constexpr int E = Slice<T>::E;     // fp32 values per slice
-#ifndef SP_SEG_ROWS
-#define SP_SEG_ROWS 32
-#endif
-  constexpr int kSegU = SP_SEG_ROWS / E;  // gradient rows in flight per group
+  constexpr int kSegU = 32 / E;  // gradient rows in flight per group (32 fp32 values per lane)
   constexpr int G = 32 / R;          // groups per warp
   constexpr int C = kWarpsPerBlock * G;
   constexpr int W = R * E;           // floats per partial row
@@ -1019,11 +994,9 @@ __device__ __forceinline__ void sgd_seg_tile(const TableMeta& m, const SgdTile& 
   }
 }
 
-#ifndef SP_SEG_MIN_BLOCKS
-#define SP_SEG_MIN_BLOCKS 4  // <= 64 registers; 3 or 5 blocks per SM measured slower
-#endif
+constexpr int kSegMinBlocks = 4;  // <= 64 registers; 3 or 5 blocks per SM measured slower
 template <class BagT, class T>
-__global__ void __launch_bounds__(kBlockThreads, SP_SEG_MIN_BLOCKS)
+__global__ void __launch_bounds__(kBlockThreads, kSegMinBlocks)
     sgd_seg_kernel(const TableMeta* __restrict__ meta, const SgdTile* __restrict__ tiles,
                    const uint32_t* __restrict__ keys, const BagT* __restrict__ bags,
                    const float* __restrict__ grad, int64_t ldg, float lr, T* __restrict__ w,
