@@ -37,22 +37,6 @@ __device__ __forceinline__ float4 ldg_f4(const float* p) {
   return __ldg(reinterpret_cast<const float4*>(p));
 }
 
-// L2 eviction-priority policies (createpolicy) for loads that should stay
-// resident (the per-table gradient slice in K4) or stream through.
-__device__ __forceinline__ uint64_t l2_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-
-__device__ __forceinline__ float4 ldg_f4_policy(const float* ptr, uint64_t pol) {
-  float4 v;
-  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(ptr), "l"(pol));
-  return v;
-}
-
 // Vector reduction at L2: fire-and-forget, the SM never waits for the row
 // (each unique row has exactly one update per launch, so the result is
 // deterministic: W + fp32(-lr * sum), round-to-nearest at L2). Measured on
