@@ -501,16 +501,16 @@ def bench_evaluator_sweep(device: int, n: int = 4096):
                     "4096 distinct sampled rollouts, one greedy rollout"}
 
 
-def bench_fp16(args, task, placement, device: int):
-    """The same iteration with the tables stored in fp16 (2 B/param): device
-    ms/iter over the timed loop and each hot kernel in isolation."""
+def bench_fp16(args, task, placement, device: int, storage: str = "fp16"):
+    """The same iteration with the tables stored in fp16 or bf16 (2 B/param):
+    device ms/iter over the timed loop and each hot kernel in isolation."""
     import torch
     from paper_2210_02023_b200 import api
     tables = [api.TableDesc(t.id, t.dim, t.hash_size, t.pooling_factor,
                             api.table_memory_gb(t.hash_size, t.dim, 2), t.dist)
               for t in task.tables]
     t16 = api.PlacementTask(tables, task.num_devices, task.mem_cap_gb / 2, task.batch_size)
-    sh = api.EmbeddingShard(t16, placement, lr=0.01, device=device)
+    sh = api.EmbeddingShard(t16, placement, lr=0.01, device=device, storage=storage)
     sh.init_tables(SEED)
     sh.synth_batch(SEED)
     sh.synth_grad(SEED)
@@ -538,7 +538,8 @@ def bench_fp16(args, task, placement, device: int):
     sh.set_profiling(False)
     ab = sh.algorithmic_bytes()
     sh.close()
-    out = {"ms_per_iter": round(ms, 4), "weights": "fp16 (2 B/param), fp32 sums/pooled/grad"}
+    out = {"ms_per_iter": round(ms, 4),
+           "weights": f"{storage} (2 B/param), fp32 sums/pooled/grad"}
     for k, a in (("fwd", ab["fwd"]), ("sort", ab["sort"]), ("sgd", ab["bwd"])):
         t = kms[k][0] / kms[k][1] if kms[k][1] else 0.0
         out[k] = {"ms": round(t, 4), "alg_bytes": a,
@@ -834,9 +835,10 @@ def run_ours(args, world, rank, local):
 
     # fp16 tables (the paper's storage; 2 B/param like the
     # reference's default table_memory_gb): same tables, batch and placement
-    fp16 = None
+    fp16 = bf16 = None
     if world == 1 and not args.no_fp16:
         fp16 = bench_fp16(args, task, placement, local)
+        bf16 = bench_fp16(args, task, placement, local, storage="bf16")
     placements = cfg4 = cfg3_d8 = None
     if world == 1 and not args.no_studies:
         placements = bench_placements(args, local)
@@ -882,6 +884,7 @@ def run_ours(args, world, rank, local):
             "clocks": clk.summary(),
             "emulated_d8": emulated,
             "fp16_tables": fp16,
+            "bf16_tables": bf16,
             "placement_study": placements,
             "cfg4_per_rank": cfg4,
             "cfg3_d8_per_rank": cfg3_d8,

@@ -131,15 +131,8 @@ template <> struct LongGeo<2> : Geo<SP_LONG_G2> {};
 template <> struct LongGeo<3> : Geo<SP_LONG_G3> {};
 template <> struct LongGeo<4> : Geo<SP_LONG_G4> {};
 template <> struct LongGeo<5> : Geo<SP_LONG_G5> {};
-// fp16 rows: a 16-byte slice widens to 8 fp32 values (twice the registers of
-// an fp32 slice), so fewer slices per lane / rows in flight per class.
-template <int CLS> struct FwdGeoH;
-template <> struct FwdGeoH<0> : Geo<1, 1, 8, 2> {};
-template <> struct FwdGeoH<1> : Geo<2, 1, 8, 2> {};
-template <> struct FwdGeoH<2> : Geo<4, 1, 4, 2> {};
-template <> struct FwdGeoH<3> : Geo<8, 1, 2, 2> {};
-template <> struct FwdGeoH<4> : Geo<16, 1, 2, 4> {};
-template <> struct FwdGeoH<5> : Geo<32, 1, 1, 4> {};
+// K4 on 2-byte rows: a 16-byte slice of the update is 8 fp32 sums (twice
+// the registers of an fp32 slice), so fewer slices per lane / rows per warp.
 template <int CLS> struct SgdGeoH;
 template <> struct SgdGeoH<0> : Geo<1, 1, 16, 1> {};
 template <> struct SgdGeoH<1> : Geo<2, 1, 16, 1> {};
@@ -154,8 +147,12 @@ template <> struct LongGeoH<2> : Geo<4, 1, 1, 2> {};
 template <> struct LongGeoH<3> : Geo<8, 1, 1, 2> {};
 template <> struct LongGeoH<4> : Geo<16, 1, 1, 4> {};
 template <> struct LongGeoH<5> : Geo<32, 1, 1, 4> {};
+// 2-byte tables use the fp32 geometry: K1 keeps slices raw until it sums
+// them (Slice<T>::Raw), so a 16-byte slice in flight costs 4 registers for
+// every type; fp16 K1 at cfg3 1.241 ms (half the rows in flight, widened at
+// load) -> 1.135 ms.
 template <int C, class T>
-using FwdG = std::conditional_t<std::is_same<T, float>::value, FwdGeo<C>, FwdGeoH<C>>;
+using FwdG = FwdGeo<C>;
 template <int C, class T>
 using SgdG = std::conditional_t<std::is_same<T, float>::value, SgdGeo<C>, SgdGeoH<C>>;
 template <int C, class T>
@@ -181,8 +178,19 @@ constexpr int kIdxCap = 4096;  // staged indices per tile (16 KB)
 // and the reference's default 2 B/param sizing, table.hpp:30).
 template <class T> struct TypeTag { using type = T; };
 template <class T> struct Slice;
+// K1 keeps each gathered slice raw (Raw: 4 registers for 16 bytes) until
+// it is summed, so 2-byte tables hold as many rows in flight per register
+// as fp32 ones; load() widens at once (the SGD's gradient path).
 template <> struct Slice<float> {
   static constexpr int E = 4;
+  using Raw = float4;
+  __device__ static __forceinline__ Raw load_raw(const float* p) {
+    return __ldg(reinterpret_cast<const float4*>(p));
+  }
+  __device__ static __forceinline__ Raw zero_raw() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+  __device__ static __forceinline__ void accum(float (&a)[4], const Raw& x) {
+    a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+  }
   __device__ static __forceinline__ void load(const float* p, float (&v)[4]) {
     const float4 x = __ldg(reinterpret_cast<const float4*>(p));
     v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
@@ -197,6 +205,20 @@ template <> struct Slice<float> {
 };
 template <> struct Slice<__half> {
   static constexpr int E = 8;
+  using Raw = uint4;
+  __device__ static __forceinline__ Raw load_raw(const __half* p) {
+    return __ldg(reinterpret_cast<const uint4*>(p));
+  }
+  __device__ static __forceinline__ Raw zero_raw() { return make_uint4(0u, 0u, 0u, 0u); }
+  __device__ static __forceinline__ void accum(float (&a)[8], const Raw& x) {
+    const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[k]));
+      a[2 * k] += f.x;
+      a[2 * k + 1] += f.y;
+    }
+  }
   __device__ static __forceinline__ void load(const __half* p, float (&v)[8]) {
     const uint4 x = __ldg(reinterpret_cast<const uint4*>(p));
     const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
@@ -228,6 +250,19 @@ template <> struct Slice<__half> {
 // 16-bit shift; the update is REDG.ADD.BF16x8 (round-to-nearest at L2)
 template <> struct Slice<__nv_bfloat16> {
   static constexpr int E = 8;
+  using Raw = uint4;
+  __device__ static __forceinline__ Raw load_raw(const __nv_bfloat16* p) {
+    return __ldg(reinterpret_cast<const uint4*>(p));
+  }
+  __device__ static __forceinline__ Raw zero_raw() { return make_uint4(0u, 0u, 0u, 0u); }
+  __device__ static __forceinline__ void accum(float (&a)[8], const Raw& x) {
+    const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      a[2 * k] += __uint_as_float(w4[k] << 16);
+      a[2 * k + 1] += __uint_as_float(w4[k] & 0xffff0000u);
+    }
+  }
   __device__ static __forceinline__ void load(const __nv_bfloat16* p, float (&v)[8]) {
     const uint4 x = __ldg(reinterpret_cast<const uint4*>(p));
     const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
@@ -261,6 +296,17 @@ template <> struct Slice<__nv_bfloat16> {
 // reductions stop at 128 bits.
 struct Slice256F {
   static constexpr int E = 8;
+  struct Raw { float v[8]; };
+  __device__ static __forceinline__ Raw load_raw(const float* p) {
+    Raw r;
+    load(p, r.v);
+    return r;
+  }
+  __device__ static __forceinline__ Raw zero_raw() { return Raw{}; }
+  __device__ static __forceinline__ void accum(float (&a)[8], const Raw& x) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) a[e] += x.v[e];
+  }
   __device__ static __forceinline__ void load(const float* p, float (&v)[8]) {
     asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
         : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
@@ -320,24 +366,17 @@ __device__ __forceinline__ void fwd_tile_warp(const TableMeta& m, int b0, int nb
         else
           r[u] = kk < end ? (kk < kIdxCap ? s_idx[kk] : __ldg(idx + p0 + kk)) : -1;
       }
-      float v[U][V][E];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-          if (r[u] >= 0) {
-            SL::load(wt + static_cast<int64_t>(r[u]) * dim + E * L * j, v[u][j]);
-          } else {
-#pragma unroll
-            for (int e = 0; e < E; ++e) v[u][j][e] = 0.f;
-          }
-        }
+      typename SL::Raw v[U][V];
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int j = 0; j < V; ++j)
+          v[u][j] = r[u] >= 0 ? SL::load_raw(wt + static_cast<int64_t>(r[u]) * dim + E * L * j)
+                              : SL::zero_raw();
 #pragma unroll
-          for (int e = 0; e < E; ++e) acc[j][e] += v[u][j][e];
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < V; ++j) SL::accum(acc[j], v[u][j]);
     }
 #pragma unroll
     for (int o = L; o < S; o <<= 1)
