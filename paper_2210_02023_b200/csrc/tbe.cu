@@ -534,6 +534,13 @@ __device__ __forceinline__ void load_grad(const float* p, float (&v)[E]) {
     v[e] = x.x; v[e + 1] = x.y; v[e + 2] = x.z; v[e + 3] = x.w;
   }
 }
+// 8 gradient values in one 32-byte load (p 32-byte aligned)
+__device__ __forceinline__ void load_grad32(const float* p, float (&v)[8]) {
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+        "=f"(v[7])
+      : "l"(p));
+}
 
 // One round of up to P short runs [j, jend) of the tile (span s: run j+s).
 template <class G, class BagT, class T>
@@ -915,12 +922,22 @@ __device__ __forceinline__ void sgd_seg_tile(const TableMeta& m, const SgdTile& 
         Slice<T>::red_add(wbase + static_cast<int64_t>(row) * m.dim, d);
       }
     };
+    // 2-byte rows: a lane's 8 gradient columns are one 32-byte load when
+    // the table's columns and the gradient's row stride are 32-byte aligned
+    // (fp16 SGD at cfg3 1.609 -> 1.524 ms)
+    const bool g32 = E == 8 && ((m.lcol | ldg) & 7) == 0;
     for (int k = cs; k < ce; k += kSegU) {
       float v[kSegU][E];
 #pragma unroll
       for (int u = 0; u < kSegU; ++u) {
         if (k + u < ce) {
-          load_grad<E>(gcol + static_cast<int64_t>(sh.bag[k + u]) * ldg, v[u]);
+          const float* gp = gcol + static_cast<int64_t>(sh.bag[k + u]) * ldg;
+          if constexpr (E == 8) {
+            if (g32) load_grad32(gp, v[u]);
+            else load_grad<E>(gp, v[u]);
+          } else {
+            load_grad<E>(gp, v[u]);
+          }
         } else {
 #pragma unroll
           for (int e = 0; e < E; ++e) v[u][e] = 0.f;
