@@ -9,8 +9,9 @@ Workload (config.workload): BASELINE cfg3 — the 100 synthetic DLRM tables of
 paper_2210_02023_b200/data/pools.json (synth_pool, seed 2210, dims 16-128,
 rows 1e5-1e6), batch 65536, split over D = N GPUs by the DreamShard placement
 (greedy rollout of the committed checkpoint on our GPU evaluator). One step =
-K1 forward -> fwd all-to-all -> bwd all-to-all -> K4 sort + row-wise SGD over
-one synthetic batch. Inputs (tables 9.2 GiB, CSR 0.2 GB) exceed L2.
+K1 forward -> fwd all-to-all -> bwd all-to-all -> row-wise SGD over one
+synthetic batch, with the K4a sort forked onto a side stream after K1 (under
+the exchanges). Inputs (tables 9.2 GiB, CSR 0.2 GB) exceed L2.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
