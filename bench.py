@@ -149,11 +149,28 @@ def bench_ranks(config: str, D: int, device: int, placement=None):
                       "compute_sort_hidden_ms": round(f + max(0.0, b - srt), 4)})
         sh.close()
         torch.cuda.synchronize()
+    # the metric at D GPUs estimated from these measurements: each rank's
+    # measured K1 and SGD, the sort under the two exchange stages, and the
+    # stages from the NVLink model (sp_comm_model) — labelled an estimate
+    dims = np.array([t.dim for t in task.tables])
+    W_tot = int(dims.sum())
+    comm = [api.comm_model_ms(task.batch_size, int(dims[np.asarray(p) == r].sum()), W_tot, D)
+            for r in range(D)]
+    stage = max(comm)
+    bwd_eff = [x["bwd_ms"] - x["sort_ms"] + max(0.0, x["sort_ms"] - 2 * stage) for x in ranks]
+    est = max(x["fwd_ms"] for x in ranks) + 2 * stage + max(bwd_eff)
     return {"placement": "dreamshard", "ranks": ranks,
             "max_fwd_ms": max(x["fwd_ms"] for x in ranks),
             "max_bwd_ms": max(x["bwd_ms"] for x in ranks),
             "max_compute_ms": max(x["compute_ms"] for x in ranks),
             "max_compute_sort_hidden_ms": max(x["compute_sort_hidden_ms"] for x in ranks),
+            "overall_estimate": {
+                "ms": round(est, 4), "exchange_stage_ms": round(stage, 4),
+                "per_rank_stage_ms": [round(c, 4) for c in comm],
+                "note": "ESTIMATE of the metric on D GPUs: max fwd + 2 x the NVLink-model "
+                        "exchange stage (770 GB/s per direction + 10 us) + max over ranks of "
+                        "the SGD plus the part of the sort the exchanges do not hide; compute "
+                        "measured here, exchange modelled (one GPU in this pool)"},
             "note": "each rank's shard alone on this B200 (sp_run_local: K1, then the sort on "
                     "a side stream, then the SGD after it; exchange excluded). The metric's "
                     "compute part is max fwd + max bwd over ranks; with the exchange, the "

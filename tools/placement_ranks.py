@@ -1,6 +1,6 @@
 """Placement study with every rank measured alone (sp_run_local): cfg3 on 8
-GPUs, each rank's shard on this B200 in turn — its K1 with the sort
-overlapped, then its SGD — for DreamShard (the reference's oracle-trained
+GPUs, each rank's shard on this B200 in turn — its K1, the sort forked
+after it, its SGD — for DreamShard (the reference's oracle-trained
 m100_d8 checkpoint and the B200-measured one), random, and the greedy
 size / lookup experts. Prints one JSON object: per placement the max-over-
 rank forward, backward and their sum (the compute part of the metric).
@@ -42,6 +42,7 @@ def main():
         r = bench.bench_ranks(args.config, args.devices, 0, placement=p)
         out[name] = {"max_fwd_ms": r["max_fwd_ms"], "max_bwd_ms": r["max_bwd_ms"],
                      "compute_ms": round(r["max_fwd_ms"] + r["max_bwd_ms"], 4),
+                     "overall_estimate_ms": r["overall_estimate"]["ms"],
                      "rank_compute_ms": [x["compute_ms"] for x in r["ranks"]]}
         print(name, out[name], flush=True)
     print(json.dumps({"config": args.config, "devices": args.devices, "placements": out}))
