@@ -159,6 +159,11 @@ def bench_ranks(config: str, D: int, device: int, placement=None):
     stage = max(comm)
     bwd_eff = [x["bwd_ms"] - x["sort_ms"] + max(0.0, x["sort_ms"] - 2 * stage) for x in ranks]
     est = max(x["fwd_ms"] for x in ranks) + 2 * stage + max(bwd_eff)
+    # peer-memory mode: the forward exchange is K1's own remote stores (the
+    # stage is the slower of K1 and its NVLink bytes), only the backward pull
+    # is a separate stage, and the sort hides under it
+    bwd_fused = [x["bwd_ms"] - x["sort_ms"] + max(0.0, x["sort_ms"] - stage) for x in ranks]
+    est_fused = max(max(x["fwd_ms"], c) for x, c in zip(ranks, comm)) + stage + max(bwd_fused)
     return {"placement": "dreamshard", "ranks": ranks,
             "max_fwd_ms": max(x["fwd_ms"] for x in ranks),
             "max_bwd_ms": max(x["bwd_ms"] for x in ranks),
@@ -166,11 +171,13 @@ def bench_ranks(config: str, D: int, device: int, placement=None):
             "max_compute_sort_hidden_ms": max(x["compute_sort_hidden_ms"] for x in ranks),
             "overall_estimate": {
                 "ms": round(est, 4), "exchange_stage_ms": round(stage, 4),
+                "peer_fused_ms": round(est_fused, 4),
                 "per_rank_stage_ms": [round(c, 4) for c in comm],
                 "note": "ESTIMATE of the metric on D GPUs: max fwd + 2 x the NVLink-model "
                         "exchange stage (770 GB/s per direction + 10 us) + max over ranks of "
                         "the SGD plus the part of the sort the exchanges do not hide; compute "
-                        "measured here, exchange modelled (one GPU in this pool)"},
+                        "measured here, exchange modelled (one GPU in this pool). peer_fused_ms: "
+                        "the same with the forward exchange fused into K1 (peer-memory mode)"},
             "note": "each rank's shard alone on this B200 (sp_run_local: K1, then the sort on "
                     "a side stream, then the SGD after it; exchange excluded). The metric's "
                     "compute part is max fwd + max bwd over ranks; with the exchange, the "

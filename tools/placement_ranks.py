@@ -43,6 +43,7 @@ def main():
         out[name] = {"max_fwd_ms": r["max_fwd_ms"], "max_bwd_ms": r["max_bwd_ms"],
                      "compute_ms": round(r["max_fwd_ms"] + r["max_bwd_ms"], 4),
                      "overall_estimate_ms": r["overall_estimate"]["ms"],
+                     "peer_fused_estimate_ms": r["overall_estimate"]["peer_fused_ms"],
                      "rank_compute_ms": [x["compute_ms"] for x in r["ranks"]]}
         print(name, out[name], flush=True)
     print(json.dumps({"config": args.config, "devices": args.devices, "placements": out}))
