@@ -12,10 +12,13 @@ tables, batch and gradient:
         (world 8, no peers: what one process per GPU runs, sp_run_local):
         the rank's pre-exchange pooled rows for all bags, its sorted keys,
         and its heaviest and lightest tables after SGD.
-  cfg4  one rank's shard of 200 tables of 1e7 rows (~62 GB on the device,
-        28-bit sort groups): sorted keys of the whole shard, all pooled rows,
-        one whole dim-16 table after SGD and sampled rows (hot and cold) of
-        the shard's heaviest table.
+  cfg4  the fewest- and the most-lookup rank's shard of 200 tables of 1e7
+        rows (~62 GB on the device, one 28-bit key space): sorted keys of the
+        whole shard, all pooled rows, one whole dim-16 table after SGD and
+        sampled rows (hot and cold) of the shard's heaviest table.
+  cfg3  with bf16 tables (D = 1): the sorted keys, pooled rows of every bag
+        for 12 tables, and 3 whole tables after SGD within the double-rounding
+        bound.
 
 Tolerances: bit-exact sort; rtol 1e-5 pooled and tables (north star)."""
 import json
@@ -149,16 +152,18 @@ def test_cfg3_d8_rank_context(cfg3_d8, rank):
     light = min(local, key=lambda t: (dims[t], nnz[t]))
     picks = sorted({heavy, light})
     before = {t: sh.get_table(t) for t in picks}
-    sh.run_local()  # K1 (sort overlapped) then the SGD on the delivered gradient
+    sh.run_local()  # K1, the sort, then the SGD on the delivered gradient
     _check_sorted(sh, rank, task, off, idx, local)
     _check_pooled(sh.local_pooled(rank), task, off, idx, local)
     _check_sgd_tables(sh, task, off, idx, picks, before)
     sh.close()
 
 
-def test_cfg4_rank_shard():
+@pytest.mark.parametrize("which", ["fewest", "most"])
+def test_cfg4_rank_shard(which):
     """One of 8 DreamShard ranks of cfg4 (200 tables x 1e7 rows, 64 GB cap):
-    the fewest-lookup rank, ~62 GB of fp32 tables on this GPU."""
+    the fewest- and the most-lookup rank (~30 M lookups in one 28-bit key
+    space: the largest sort of any config), ~62 GB of fp32 tables each."""
     tables, B, cap = _pool("cfg4")
     task = PlacementTask(tables, 8, cap, B)
     placement = _dreamshard(task, "dreamshard_m100_d8.dshd")
@@ -166,7 +171,7 @@ def test_cfg4_rank_shard():
     nnz = np.diff(off[::B])
     dims = np.array([t.dim for t in tables])
     per_rank = [int(nnz[placement == r].sum()) for r in range(8)]
-    rank = int(np.argmin(per_rank))
+    rank = int(np.argmin(per_rank) if which == "fewest" else np.argmax(per_rank))
     local = [t for t in range(len(tables)) if placement[t] == rank]
     torch.cuda.empty_cache()
     sh = EmbeddingShard(task, placement, lr=LR, rank=rank, world_size=8, nccl_id=None)
@@ -198,4 +203,61 @@ def test_cfg4_rank_shard():
                              grad_cols(SEED, B, table_cols(list(dims), heavy)), LR)
     np.testing.assert_allclose(after, want, rtol=RTOL, atol=1e-6)
     np.testing.assert_array_equal(after[rows_sel.index(untouched)], before_heavy[untouched])
+    sh.close()
+
+
+def _to_bf16(x):
+    u = np.asarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32)
+
+
+def test_cfg3_bf16_tables():
+    """cfg3 at full size with bf16 storage (the 2-byte paths: raw 16-byte
+    slices in K1, 32-byte gradient loads in the SGD, REDG.ADD.BF16x8)."""
+    from paper_2210_02023_b200.api import table_memory_gb
+    tables, B, cap = _pool("cfg3")
+    tables = [TableDesc(t.id, t.dim, t.hash_size, t.pooling_factor,
+                        table_memory_gb(t.hash_size, t.dim, 2), t.dist) for t in tables]
+    task = PlacementTask(tables, 1, 0.0, B)
+    off, idx = orc.synth_batch([t.to_dict() for t in tables], B, SEED)
+    sh = EmbeddingShard(task, np.zeros(len(tables), dtype=np.int32), lr=LR, storage="bf16")
+    sh.init_tables(SEED)
+    sh.synth_batch(SEED)
+    _check_sorted(sh, 0, task, off, idx, list(range(len(tables))))
+    nnz = np.diff(off[::B])
+    dims = [t.dim for t in tables]
+    rows = [t.hash_size for t in tables]
+    heavy = int(np.argmax(nnz * np.array(dims)))
+    picks = sorted({heavy} | set(range(3, len(tables), 9)))
+    w = {t: sh.get_table(t) for t in picks}
+    for t in picks[:3]:  # the generator's weights, rounded to bf16
+        np.testing.assert_array_equal(w[t][:64, :4], _to_bf16(
+            np.array([[orc.lib().or_weight(SEED, t, r, c) for c in range(4)] for r in range(64)],
+                     dtype=np.float32)))
+    sh.forward()
+    sh.a2a_forward()
+    pooled = sh.pooled()
+    cols = np.concatenate([table_cols(dims, t) for t in picks])
+    wl = [w.get(t) for t in range(len(tables))]
+    for lo in range(0, B, 16384):
+        want = orc.tbe_forward(dims, rows, wl, off, idx, B, tables_list=picks,
+                               bag_lo=lo, bag_hi=lo + 16384)
+        np.testing.assert_allclose(pooled[lo:lo + 16384][:, cols], want[:, cols], rtol=1e-5,
+                                   atol=1e-5)
+    sh.synth_grad(SEED)
+    sh.backward_sgd()
+    three = [heavy] + [t for t in picks if t != heavy][:2]
+    sub_off, sub_idx = sub_batch(off, idx, B, three)
+    g = grad_cols(SEED, B, np.concatenate([table_cols(dims, t) for t in three]))
+    ref = orc.tbe_backward_sgd([dims[t] for t in three], [rows[t] for t in three],
+                               [w[t] for t in three], sub_off, sub_idx, B, g, LR, [0, 1, 2])
+
+    def ulp(x):
+        x = np.abs(x.astype(np.float32))
+        return 2.0 ** (np.floor(np.log2(np.maximum(x, 2.0 ** -126))) - 7)
+    for k, t in enumerate(three):
+        got = sh.get_table(t)
+        bound = 0.5 * ulp(ref[k]) + 0.5 * ulp(ref[k] - w[t]) + 1e-7
+        assert np.all(np.abs(got - ref[k]) <= bound), t
     sh.close()
