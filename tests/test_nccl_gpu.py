@@ -7,9 +7,11 @@ A whole on-device iteration (sp_run_iteration) per rank, checked against
 the CPU oracle: each rank's received pooled slice, its updated tables, and
 the breakdown's composition (oracle.hpp:222-227).
 
-Needs >= 2 GPUs (NCCL refuses two ranks on one device); skipped otherwise —
-the peer path alone is covered on one GPU by tests/test_peer_gpu.py and the
-exchange plan by tests/test_dist_cpu.py."""
+The iterations need >= 2 GPUs (NCCL refuses two ranks on one device) and
+skip otherwise — the peer path alone is covered on one GPU by
+tests/test_peer_gpu.py and the exchange plan by tests/test_dist_cpu.py. On
+one GPU, test_nccl_binding_reaches_comm_init still drives the NCCL binding
+up to ncclCommInitRank and checks its refusal comes back as an error."""
 import os
 import socket
 import traceback
@@ -18,9 +20,9 @@ import numpy as np
 import pytest
 import torch
 
-pytestmark = [pytest.mark.gpu,
-              pytest.mark.skipif(torch.cuda.device_count() < 2,
-                                 reason="NCCL exchange needs >= 2 GPUs")]
+pytestmark = pytest.mark.gpu
+needs_two = pytest.mark.skipif(torch.cuda.device_count() < 2,
+                               reason="NCCL exchange needs >= 2 GPUs")
 
 LR = 0.03
 
@@ -105,6 +107,7 @@ def _worker(rank, world, port, name, peer, q):
         q.put((rank, traceback.format_exc()))
 
 
+@needs_two
 @pytest.mark.parametrize("peer", [False, True], ids=["nccl", "nccl+peer"])
 @pytest.mark.parametrize("name", ["random", "cfg1"])
 def test_nccl_exchange_iteration(name, peer):
@@ -129,3 +132,52 @@ def test_nccl_exchange_iteration(name, peer):
                 p.kill()
     for r in range(world):
         assert results.get(r) == "ok", results.get(r)
+
+
+def _dup_worker(rank, port, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=2)
+        from paper_2210_02023_b200 import api
+        from paper_2210_02023_b200.api import EmbeddingShard, ShardplanError
+        task, placement, _ = _case("random", 2)
+        obj = [api.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        try:
+            EmbeddingShard(task, placement, rank=rank, world_size=2, nccl_id=obj[0], device=0)
+            q.put((rank, "created"))
+        except ShardplanError as e:
+            q.put((rank, f"{e.kind}: {e}"))
+        dist.destroy_process_group()
+    except BaseException:  # noqa: BLE001
+        q.put((rank, traceback.format_exc()))
+
+
+def test_nccl_binding_reaches_comm_init():
+    """On any box: the run-time NCCL binding (csrc/nccl_loader.h, bound to the
+    NCCL already in the process) creates a unique id and reaches
+    ncclCommInitRank; two ranks on one device are refused by NCCL
+    ("Duplicate GPU"), and the refusal comes back as a ShardplanError of
+    kind nccl, not a crash."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dup_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = {}
+    try:
+        for _ in range(2):
+            r, msg = q.get(timeout=300)
+            results[r] = msg
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    for r in range(2):
+        assert "invalid usage" in results.get(r, ""), results.get(r)
+        assert results[r].startswith("nccl"), results[r]
