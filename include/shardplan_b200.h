@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 1
+#define SP_ABI_VERSION 2
 #define SP_NUM_BINS 17      /* table.hpp:26 kNumBins */
 #define SP_NUM_FEATURES 21  /* table.hpp:28 kNumFeatures */
 #define SP_NCCL_ID_BYTES 128

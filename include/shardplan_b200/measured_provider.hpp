@@ -133,6 +133,11 @@ class Shard {
  public:
   Shard(const PlacementTask& task, const Placement& placement, const MeasureOptions& o)
       : D_(task.num_devices) {
+    if (sp_abi_version() != SP_ABI_VERSION)
+      throw Error(ErrorKind::bad_input, "libshardplan_b200 ABI " +
+                                            std::to_string(sp_abi_version()) +
+                                            " does not match this header's " +
+                                            std::to_string(SP_ABI_VERSION));
     std::vector<sp_table_spec> specs;
     for (const TableDesc& t : task.tables) specs.push_back(to_spec(t));
     std::vector<int32_t> p(placement.begin(), placement.end());

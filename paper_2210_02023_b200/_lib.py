@@ -19,6 +19,8 @@ c_f64 = ctypes.c_double
 c_vp = ctypes.c_void_p
 P = ctypes.POINTER
 
+ABI_VERSION = 2  # SP_ABI_VERSION of include/shardplan_b200.h
+
 # Every function the header declares, with (restype, argtypes).
 SIGNATURES = {
     "sp_abi_version": (c_i32, []),
@@ -173,6 +175,10 @@ def lib() -> ctypes.CDLL:
                 f"{LIB_PATH} is missing: build it with `python -m paper_2210_02023_b200.build`"
                 " (there is no CPU fallback)")
         L = ctypes.CDLL(LIB_PATH)
+        L.sp_abi_version.restype = c_i32
+        if L.sp_abi_version() != ABI_VERSION:
+            raise ImportError(f"{LIB_PATH} has ABI {L.sp_abi_version()}, this binding expects "
+                              f"{ABI_VERSION}: rebuild it (python -m paper_2210_02023_b200.build)")
         for name, (res, args) in SIGNATURES.items():
             if not hasattr(L, name):
                 continue  # tests/test_abi.py asserts every header symbol exists

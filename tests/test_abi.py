@@ -36,7 +36,7 @@ def test_library_exports_every_header_symbol():
 
 def test_abi_version_and_errors():
     L = _lib.lib()
-    assert L.sp_abi_version() == 1
+    assert L.sp_abi_version() == 2
     assert isinstance(L.sp_last_error(), bytes)
 
 
