@@ -903,6 +903,10 @@ def run_ours(args, world, rank, local):
                             "compute and its own forward/sort; validation; SGD), wall clock "
                             "per step",
                     "single_step_ms": round(e2e_single_ms, 3),
+                    "h2d_gbs": round(h2d_local / (e2e_ms * 1e6), 1),
+                    "h2d_note": "the step is bound by the PCIe H2D of the int64 LookupBatch "
+                                "(pinned-copy peak ~55 GB/s on this host); the device work "
+                                "hides under it",
                     "single_step_path": "EmbeddingShard.run_batch -> CostBreakdown "
                                         "(one step, nothing to overlap with)"},
             "gpu_launches": int(kernels_per_iter * args.steps) if kernels_per_iter
