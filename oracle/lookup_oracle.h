@@ -22,8 +22,10 @@
  *
  * Parity status: lookup fwd/bwd numerics are "parity unpinned" by the
  * reference (it has no lookup code); they are pinned by the
- * hand-computed golden cases in tests/golden/lookup_cases.json. Ingest is
- * pinned against the reference itself (oracle/_ref) and SPEC.md:51-53.
+ * hand-worked golden cases in tests/golden/lookup_cases.json and against
+ * PyTorch's embedding_bag(mode="sum") + autograd SGD
+ * (tests/test_torch_reference_cpu.py). Ingest is pinned against the
+ * reference itself (oracle/_ref) and SPEC.md:51-53.
  */
 #ifndef LOOKUP_ORACLE_H_
 #define LOOKUP_ORACLE_H_

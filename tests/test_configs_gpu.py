@@ -261,3 +261,40 @@ def test_cfg3_bf16_tables():
         bound = 0.5 * ulp(ref[k]) + 0.5 * ulp(ref[k] - w[t]) + 1e-7
         assert np.all(np.abs(got - ref[k]) <= bound), t
     sh.close()
+
+
+@pytest.mark.parametrize("cfg,D", [("cfg1", 2), ("cfg2", 4)])
+def test_against_torch_embedding_bag(cfg, D):
+    """The GPU iteration against a third-party implementation of the same
+    operator: PyTorch's embedding_bag(mode="sum") per table and the SGD
+    step from its autograd (CPU), on the generator's tables, batch and
+    gradient; every pooled value and every table after the step. Both sides
+    accumulate in fp32 in their own order (hot rows sum thousands of
+    gradient rows), so the tables get atol 5e-6 beside rtol 1e-5."""
+    tables, B, cap = _pool(cfg)
+    task = PlacementTask(tables, D, cap, B)
+    placement = _dreamshard(task, "dreamshard_m50_d4.dshd")
+    off, idx = orc.synth_batch([t.to_dict() for t in tables], B, SEED)
+    sh = EmbeddingShard(task, placement, lr=LR)
+    sh.init_tables(SEED)
+    sh.synth_batch(SEED)
+    sh.synth_grad(SEED)
+    weights = [sh.get_table(t) for t in range(len(tables))]
+    sh.run_iteration()
+    dims = [t.dim for t in tables]
+    grad = grad_cols(SEED, B, np.arange(sum(dims)))
+    pooled = sh.pooled()
+    col = 0
+    for t, tab in enumerate(tables):
+        seg = off[t * B:(t + 1) * B + 1]
+        ids = torch.from_numpy(idx[seg[0]:seg[-1]].astype(np.int64))
+        offs = torch.from_numpy((seg[:-1] - seg[0]).astype(np.int64))
+        w = torch.tensor(weights[t], requires_grad=True)
+        p = torch.nn.functional.embedding_bag(ids, w, offs, mode="sum")
+        (p * torch.from_numpy(np.ascontiguousarray(grad[:, col:col + tab.dim]))).sum().backward()
+        np.testing.assert_allclose(pooled[:, col:col + tab.dim], p.detach().numpy(),
+                                   rtol=RTOL, atol=1e-5)
+        np.testing.assert_allclose(sh.get_table(t), (w - LR * w.grad).detach().numpy(),
+                                   rtol=RTOL, atol=5e-6)
+        col += tab.dim
+    sh.close()
