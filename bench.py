@@ -730,8 +730,8 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     barrier(world)
 
-    # timed region: K eager iterations (the backward sort overlaps the
-    # forward on the context's side stream)
+    # timed region: K eager iterations (the backward sort runs on the
+    # context's side stream, forked after K1: under the exchanges at N > 1)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     launches0 = api.lib().sp_kernel_launches()
