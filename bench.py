@@ -478,12 +478,17 @@ def run_reference(args, world, rank):
 
 
 def config_dict(args, task):
-    return {"workload": f"{args.config}: {len(task.tables)} synthetic DLRM tables (dims 16-128, "
-                        f"rows 1e5-1e6, pools.json seed 2210), batch {task.batch_size}, "
-                        f"D={task.num_devices} devices, {args.placement} placement",
+    dims = sorted({t.dim for t in task.tables})
+    rows = [t.hash_size for t in task.tables]
+    gib = sum(t.hash_size * t.dim * 4 for t in task.tables) / 2 ** 30
+    return {"workload": f"{args.config}: {len(task.tables)} synthetic DLRM tables (dims "
+                        f"{dims[0]}-{dims[-1]}, rows {min(rows):.0e}-{max(rows):.0e}, pools.json "
+                        f"seed 2210), batch {task.batch_size}, D={task.num_devices} devices, "
+                        f"{args.placement} placement",
             "tables": len(task.tables), "batch": task.batch_size,
             "devices": task.num_devices, "placement": args.placement,
-            "l2": "inputs larger than L2 (tables 9.2 GiB fp32, CSR 0.2 GB, no flush)",
+            "l2": f"inputs larger than L2 (tables {gib:.1f} GiB fp32, CSR 0.2 GB, no flush)"
+                  if gib > 1 else "tables fit in L2 (small config)",
             "parallelism": f"table-wise model parallel x{task.num_devices}"}
 
 

@@ -62,3 +62,25 @@ def test_cpu_iteration_exchange_is_a_relayout():
         res.append([w.copy() for w in it.weights])
     for a, b in zip(*res):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "oracle", "_ref",
+                                                    "libshardplan_ref.so")),
+                    reason="the reference build (oracle/_ref) places the reference arm's tables")
+def test_reference_arm_two_ranks_prints_one_line():
+    """`bench.py --impl reference --gpus 2` (self-launched as two ranks, as the
+    driver's torchrun would): rank 0 alone times the full-batch CPU iteration
+    at D = 2 and prints one JSON line; the other rank exits 0 without work."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--gpus", "2", "--config", "cfg1", "--steps", "2", "--warmup", "3",
+                          "--no-cpu-single"], capture_output=True, text=True, timeout=600,
+                         env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    line = lines[0]
+    assert line["impl"] == "reference" and line["n_gpus"] == 2
+    assert line["config"]["devices"] == 2 and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0
