@@ -844,7 +844,8 @@ def run_ours(args, world, rank, local):
     # CPU baseline (rank 0, N = 1 only): the full iteration on the host cores
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(task, placement, steps=3, warmup=1, single=not args.no_cpu_single)
+        # 5 warm-up, 10 timed, median
+        cpu = cpu_baseline(task, placement, steps=10, warmup=5, single=not args.no_cpu_single)
 
     # D=8 DreamShard placement emulated on this GPU (N = 1 only)
     emulated = None
