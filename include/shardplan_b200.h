@@ -293,9 +293,9 @@ int sp_enqueue_iteration(sp_ctx* ctx);
 int sp_graph_replay(sp_ctx* ctx, int32_t iters, int32_t* kernels_per_iter);
 
 /* The backward's stable sort (K4a) reads only the batch: by default (one
- * device per context) it runs on a high-priority side stream, concurrently
- * with the forward and the exchanges. on = 0 serialises it behind K1
- * (per-kernel timing in isolation). */
+ * device per context) it runs on a high-priority side stream forked after
+ * K1, concurrently with the exchanges, and the SGD waits for it. on = 0
+ * runs it on the main stream behind K1 (per-kernel timing in isolation). */
 int sp_ctx_set_overlap(sp_ctx* ctx, int32_t on);
 
 /* The exchange of one GPU emulating D devices is a device-local copy, not

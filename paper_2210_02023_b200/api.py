@@ -610,8 +610,9 @@ class EmbeddingShard:
         check(lib().sp_ctx_set_comm_model(self._h, 1 if on else 0))
 
     def set_overlap(self, on: bool):
-        """Backward sort on the side stream concurrently with the forward
-        (default) or serialised behind it (sp_ctx_set_overlap)."""
+        """Backward sort on the side stream, forked after K1 and concurrent
+        with the exchanges (default), or on the main stream behind K1
+        (sp_ctx_set_overlap)."""
         check(lib().sp_ctx_set_overlap(self._h, 1 if on else 0))
 
     def set_sort_target(self, lookups: int):

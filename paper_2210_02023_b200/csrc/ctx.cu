@@ -172,9 +172,10 @@ struct sp_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // H2D of uploaded batches
   // The backward's sort depends only on the batch, not on the gradient: with
-  // one (virtual) device it runs on the high-priority `side` stream
-  // concurrently with the forward and the exchanges (sp_ctx_set_overlap(0)
-  // serialises it behind K1).
+  // one (virtual) device it runs on the high-priority `side` stream, forked
+  // after K1, concurrently with the exchanges (sp_ctx_set_overlap(0) runs it
+  // on the main stream; the host-buffer step sorts each uploaded chunk on
+  // the side stream while the next chunk is in flight).
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_sort[2] = {nullptr, nullptr};  // timing: the forked sort's span
@@ -371,7 +372,7 @@ struct ProfScope {
 
 // ---- stages ---------------------------------------------------------------
 
-// The sort runs on the side stream, concurrently with the forward.
+// The sort runs on the side stream (forked after K1, see fork_sort).
 bool overlap_active(const sp_ctx* c) {
   return c->overlap_sort && c->vdevs.size() == 1 && c->vdevs[0].nnz > 0;
 }
