@@ -55,6 +55,11 @@ constexpr int kMaxBuckets = 1024;          // buckets per table
 // zero / scan rounds per lookup in both passes)
 constexpr int kCap3 = 8192;
 constexpr double kBucketTarget = 4096.0;
+// P4's warp-per-bucket kernel (buckets of <= 512 lookups): digits of <= 6
+// bits whatever the table's db (which suits its average bucket), so the
+// warp's histogram is 96 words instead of 1056: sort 0.820 -> 0.800 ms at
+// cfg3 (5 and 7 bits the same within 0.3 %)
+constexpr int kSmallDigitBits = 6;
 constexpr int kMaxDigitBits = 10;          // <= 10-bit digits (sort_plan picks per table)
 constexpr int kSmallCapScan = 512;         // = kSmallCap: buckets above go to sort_big_kernel          // P4 digit (a warp's histogram: 4 KB)
 // a warp histogram of 2^db bins takes hist_words(db) words (+ one pad word
@@ -519,7 +524,9 @@ __global__ void __launch_bounds__(kThreads, 4)
   const uint32_t mofs = 4u * (hw + 1);  // cursor -> its peer mask
   const uint32_t stage = smem_addr(w + 2 * (hw + 1));
   for (int k = lane; k <= hw; k += 32) sts(h + mofs + 4u * k, 0u);
-  const int db = s.db;
+  // digits of <= kSmallDigitBits (see its definition)
+  const int passes_s = (s.lo + kSmallDigitBits - 1) / kSmallDigitBits;
+  const int db = passes_s ? (s.lo + passes_s - 1) / passes_s : 1;
   const int passes = (s.lo + db - 1) / db;
   const unsigned lt = lanemask_lt(), me = 1u << lane;
   auto valid = [&](int r) { return 32 * r + lane < n; };
@@ -750,10 +757,11 @@ void launch_sort_t(const SortPlan& pl, const SortTable* d_tabs, const int2* d_ti
   }
   const int64_t w0 = pl.wt_start[t0], w1 = pl.wt_start[t1];
   const int64_t k0 = pl.bk_start[t0], k1 = pl.bk_start[t1];
-  int nb_max = 1, db_max = 1;
+  int nb_max = 1, db_max = 1, lo_max = 1;
   for (int t = t0; t < t1; ++t) {
     nb_max = std::max(nb_max, pl.tabs[t].nb);
     db_max = std::max(db_max, pl.tabs[t].db);
+    lo_max = std::max(lo_max, pl.tabs[t].lo);
   }
   const int hw = hist_words(db_max);
   const unsigned n_tiles = static_cast<unsigned>(w1 - w0);
@@ -774,8 +782,9 @@ void launch_sort_t(const SortPlan& pl, const SortTable* d_tabs, const int2* d_ti
     SP_LAUNCHED();
   }
   if (n_bk > 0) {
-    sort_bucket_kernel<BagT, M><<<(n_bk + kWarps - 1) / kWarps, kThreads, small_smem<V>(hw), st>>>(
-        d_tabs, d_bkts + k0, n_bk, d_bstart, mid, d_keys, static_cast<BagT*>(d_bags), hw);
+    const int hws = hist_words(std::min(lo_max, kSmallDigitBits));
+    sort_bucket_kernel<BagT, M><<<(n_bk + kWarps - 1) / kWarps, kThreads, small_smem<V>(hws), st>>>(
+        d_tabs, d_bkts + k0, n_bk, d_bstart, mid, d_keys, static_cast<BagT*>(d_bags), hws);
     SP_LAUNCHED();
     const int per_sm = std::max(1, static_cast<int>(200 * 1024 / big_smem(hw)));
     const int grid = std::max(1, std::min(n_bk, per_sm * num_sms()));
