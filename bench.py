@@ -722,12 +722,17 @@ def run_ours(args, world, rank, local):
     shard.synth_batch(SEED)
     shard.synth_grad(SEED)
     stream = torch.cuda.ExternalStream(shard.stream, device=local)
-    try:  # kernel nodes of one captured iteration (the launch count claim)
-        kernels_per_iter = shard.graph_replay(0)
-    except Exception as e:  # noqa: BLE001  (e.g. a capture the NCCL build refuses)
-        print(f"bench: iteration capture failed ({e}); counting launches instead",
-              file=sys.stderr)
-        kernels_per_iter = None
+    kernels_per_iter = None
+    if world == 1:
+        # kernel nodes of one captured iteration (the launch count claim). Not
+        # at N > 1: capturing NCCL send/recv before their first eager run
+        # would set up the peer connections inside the capture; there the
+        # launches are counted instead.
+        try:
+            kernels_per_iter = shard.graph_replay(0)
+        except Exception as e:  # noqa: BLE001
+            print(f"bench: iteration capture failed ({e}); counting launches instead",
+                  file=sys.stderr)
 
     # warm-up
     for _ in range(args.warmup):
@@ -975,6 +980,7 @@ def main():
         run_ours(args, world, rank, local)
     if world > 1 and args.impl == "ours":
         import torch.distributed as dist
+        barrier(world)  # rank 0's evaluator runs after the others' last collective
         dist.destroy_process_group()
 
 
