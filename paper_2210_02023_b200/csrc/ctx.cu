@@ -172,7 +172,7 @@ struct sp_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // H2D of uploaded batches
   // The backward's sort depends only on the batch, not on the gradient: with
-  // one (virtual) device it runs on the high-priority `side` stream, forked
+  // one (virtual) device it runs on the `side` stream, forked
   // after K1, concurrently with the exchanges (sp_ctx_set_overlap(0) runs it
   // on the main stream; the host-buffer step sorts each uploaded chunk on
   // the side stream while the next chunk is in flight).
@@ -683,15 +683,21 @@ int sp_ctx_create_ex(const sp_table_spec* tables, int32_t num_tables,
     c->tables.assign(tables, tables + num_tables);
     c->placement.assign(placement, placement + num_tables);
     SP_CUDA(cudaSetDevice(cuda_device));
-    SP_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    SP_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     {
-      // high priority: the sort's blocks are dispatched as K1's retire
-      // instead of queueing behind all of K1's blocks
+      // One rank per GPU: the forked sort shares the SMs with the exchange's
+      // NCCL kernels (a few CTAs on the main stream); the main stream gets
+      // the higher priority so those CTAs take the first free SM slots
+      // instead of waiting behind every block of the sort. One process (no
+      // exchange, or emulated devices): the side stream keeps the high
+      // priority, so a sort overlapped with the host-buffer upload is
+      // dispatched as K1's blocks retire.
       int lo = 0, hi = 0;
       SP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      SP_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi));
+      const bool ranks = world_size > 1;
+      SP_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, ranks ? hi : lo));
+      SP_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, ranks ? lo : hi));
     }
+    SP_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     SP_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     SP_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     SP_CUDA(cudaEventCreate(&c->ev_sort[0]));
