@@ -703,6 +703,59 @@ def roofline_block(args, D, kernels, per_launch, alg, dominant, ab):
     return out
 
 
+def make_rank_shard(args, task, placement, world, rank, local):
+    """This rank's EmbeddingShard. N > 1: an NCCL communicator (exchanges,
+    device-side barriers, the breakdown AllGather); with --exchange peer (the
+    default) every rank also maps the others' receive / gradient buffers
+    (CUDA IPC over NVLink), so K1 stores each pooled slice straight into its
+    receiver — the forward all-to-all fused into the lookup kernel — and the
+    backward pulls its gradient slices from the peers. Every rank must end in
+    the same mode: if any rank cannot map its peers, all of them rebuild
+    their shard NCCL-only."""
+    from paper_2210_02023_b200 import api
+
+    def build():
+        nccl_id = None
+        if world > 1:
+            import torch.distributed as dist
+            obj = [api.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nccl_id = obj[0]
+        return api.EmbeddingShard(task, placement, lr=0.01, rank=rank, world_size=world,
+                                  nccl_id=nccl_id, device=local)
+
+    shard = build()
+    if world == 1:
+        return shard, "none (one device)"
+    if args.exchange == "nccl":
+        return shard, "nccl"
+    import torch.distributed as dist
+    ok = 1
+    try:
+        mine = shard.ipc_export()
+    except Exception as e:  # noqa: BLE001
+        print(f"bench rank {rank}: ipc_export failed ({e})", file=sys.stderr)
+        mine, ok = None, 0
+    handles = [None] * world
+    dist.all_gather_object(handles, mine)
+    if ok and all(h is not None for h in handles):
+        try:
+            shard.ipc_import(handles)
+        except Exception as e:  # noqa: BLE001
+            print(f"bench rank {rank}: ipc_import failed ({e})", file=sys.stderr)
+            ok = 0
+    else:
+        ok = 0
+    flags = [None] * world
+    dist.all_gather_object(flags, ok)
+    if all(flags):
+        return shard, "nccl+peer"
+    shard.close()
+    print(f"bench rank {rank}: peer mapping failed on ranks "
+          f"{[r for r, f in enumerate(flags) if not f]}; NCCL-only exchange", file=sys.stderr)
+    return build(), "nccl (peer mapping failed)"
+
+
 def run_ours(args, world, rank, local):
     import torch
     from paper_2210_02023_b200 import api
@@ -710,14 +763,7 @@ def run_ours(args, world, rank, local):
     D = world
     task = load_task(args.config, D)
     placement = make_placement(task, args.placement, local)
-    nccl_id = None
-    if world > 1:
-        import torch.distributed as dist
-        obj = [api.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
-    shard = api.EmbeddingShard(task, placement, lr=0.01, rank=rank, world_size=world,
-                               nccl_id=nccl_id, device=local)
+    shard, exchange = make_rank_shard(args, task, placement, world, rank, local)
     shard.init_tables(SEED)
     shard.synth_batch(SEED)
     shard.synth_grad(SEED)
@@ -800,6 +846,13 @@ def run_ours(args, world, rank, local):
     if world > 1:
         for name, st in (("fwd_a2a", bd.fwd_comm_stage_ms), ("bwd_a2a", bd.bwd_comm_stage_ms)):
             gbs = ab["a2a"] / (st * 1e6) if st > 0 else None
+            if name == "fwd_a2a" and exchange == "nccl+peer":
+                # the pooled slices moved inside K1 (remote stores); the
+                # stage is only the barrier that completes them
+                roofline[name] = {"bytes_sent_per_rank": ab["a2a"], "stage_ms": round(st, 4),
+                                  "fused_into": "fwd (K1 remote stores over NVLink)",
+                                  "peak": NVLINK_GBS, "unit": "GB/s"}
+                continue
             roofline[name] = {"bytes_sent_per_rank": ab["a2a"], "stage_ms": round(st, 4),
                               "achieved": round(gbs, 1) if gbs else None,
                               "peak": NVLINK_GBS, "unit": "GB/s",
@@ -895,6 +948,7 @@ def run_ours(args, world, rank, local):
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (SURVEY §8d generator, seed 2210)",
             "config": config_dict(args, task),
+            "exchange": exchange,
             "breakdown": {"fwd_ms": [round(x, 4) for x in bd.fwd_ms],
                           "bwd_ms": [round(x, 4) for x in bd.bwd_ms],
                           "fwd_comm_stage_ms": round(bd.fwd_comm_stage_ms, 4),
@@ -957,6 +1011,10 @@ def parse_args(argv=None):
     ap.add_argument("--no-fp16", action="store_true")
     ap.add_argument("--no-studies", action="store_true",
                     help="skip the placement study (cfg2/cfg3) and the cfg4 per-rank shards")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: 'peer' = K1 stores pooled rows into the receivers over "
+                         "NVLink (CUDA IPC) with NCCL barriers, backward pulls from the peers; "
+                         "'nccl' = NCCL grouped send/recv all-to-all after K1")
     ap.add_argument("--dry-dist", action="store_true",
                     help="rendezvous only (gloo), print {world, rank} per rank and exit")
     args = ap.parse_args(argv)
