@@ -84,3 +84,68 @@ def test_reference_arm_two_ranks_prints_one_line():
     assert line["impl"] == "reference" and line["n_gpus"] == 2
     assert line["config"]["devices"] == 2 and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def _mode_worker(rank, world, port, fail_rank, q):
+    """One rank of make_rank_shard with a stand-in shard (no GPU): rank
+    `fail_rank` cannot map its peers."""
+    import traceback
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2210_02023_b200 import api
+        built = []
+
+        class FakeShard:
+            def __init__(self, task, placement, **kw):
+                self.kw, self.closed, self.peer = kw, False, False
+                built.append(self)
+
+            def ipc_export(self):
+                return bytes([self.kw["rank"]]) * 4
+
+            def ipc_import(self, handles):
+                assert [h[0] for h in handles] == list(range(world))
+                if self.kw["rank"] == fail_rank:
+                    raise api.ShardplanError(4, "no peer access")
+                self.peer = True
+
+            def close(self):
+                self.closed = True
+
+        api.EmbeddingShard = FakeShard
+        api.nccl_unique_id = lambda: b"id"
+        args = bench.parse_args(["--gpus", str(world)])
+        shard, mode = bench.make_rank_shard(args, None, None, world, rank, rank)
+        q.put((rank, mode, len(built), built[0].closed, shard.peer))
+        dist.destroy_process_group()
+    except BaseException:  # noqa: BLE001
+        q.put((rank, traceback.format_exc(), 0, False, False))
+
+
+@pytest.mark.parametrize("fail_rank", [-1, 1])
+def test_exchange_mode_agreed_over_ranks(fail_rank):
+    """--exchange peer (the N > 1 default): every rank maps the others'
+    buffers; if any rank cannot, all ranks rebuild NCCL-only (mixed modes
+    would deadlock the barriers)."""
+    import multiprocessing as mp
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_mode_worker, args=(r, 2, port, fail_rank, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    for rank, mode, n_built, first_closed, peer in out:
+        if fail_rank < 0:
+            assert (mode, n_built, first_closed, peer) == ("nccl+peer", 1, False, True), out
+        else:
+            assert mode.startswith("nccl (peer mapping failed)"), out
+            assert (n_built, first_closed, peer) == (2, True, False), out
