@@ -191,6 +191,11 @@ struct sp_ctx {
   float* peer_gin[sp::kMaxPeers] = {};
   sp::RowMap* d_rowmap = nullptr;  // K1's peer row map (device), null = local
   std::vector<void*> ipc_opened;
+  // the backward pull: one stream per peer, so the world-1 peer reads run on
+  // concurrent copy engines instead of queueing behind one (ev_pull[0]:
+  // fork from the main stream; ev_pull[1 + k]: peer stream k done)
+  std::vector<cudaStream_t> pull_streams;
+  std::vector<cudaEvent_t> ev_pull;
   double* d_bd = nullptr;      // breakdown gather buffer
   int32_t* d_barrier = nullptr;
   cudaEvent_t ev_a2a[4] = {};
@@ -241,6 +246,9 @@ struct sp_ctx {
     for (void* p : sort_owned) cudaFree(p);
     for (void* p : owned) cudaFree(p);
     if (comm) sp::nccl().CommDestroy(comm);
+    for (cudaStream_t ps : pull_streams) cudaStreamSynchronize(ps);
+    for (cudaEvent_t e : ev_pull) cudaEventDestroy(e);
+    for (cudaStream_t ps : pull_streams) cudaStreamDestroy(ps);
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (copy_stream) cudaStreamSynchronize(copy_stream);
     if (side) cudaStreamSynchronize(side);
@@ -468,12 +476,30 @@ void a2a_bwd_nccl(sp_ctx* c) {
 
 // Backward exchange over peer memory: this rank's gradient slice of every
 // receiver j ([B/D, W_r] at j's slot for this rank) is pulled into grad_v.
+// Each peer's slice is one contiguous NVLink read, on its own stream (its
+// own copy engine), forked from and joined back into the main stream
+// (capture-safe); the rank's own slice is a local copy on the main stream.
 void a2a_bwd_peer(sp_ctx* c) {
   VDev& v = c->vdevs[0];
   const int64_t R = c->B / c->D;
-  for (int j = 0; j < c->D; ++j)
-    d2d(v.d_grad + j * R * v.W, c->peer_gin[j] + R * c->cumW[c->rank], R * v.W * sizeof(float),
-        c->stream);
+  const size_t bytes = R * v.W * sizeof(float);
+  if (bytes == 0) return;
+  SP_CUDA(cudaEventRecord(c->ev_pull[0], c->stream));
+  int k = 0;
+  for (int j = 0; j < c->D; ++j) {
+    float* dst = v.d_grad + j * R * v.W;
+    const float* src = c->peer_gin[j] + R * c->cumW[c->rank];
+    if (j == c->rank) {
+      d2d(dst, src, bytes, c->stream);
+      continue;
+    }
+    cudaStream_t ps = c->pull_streams[k];
+    SP_CUDA(cudaStreamWaitEvent(ps, c->ev_pull[0], 0));
+    d2d(dst, src, bytes, ps);
+    SP_CUDA(cudaEventRecord(c->ev_pull[1 + k], ps));
+    ++k;
+  }
+  for (int q = 0; q < k; ++q) SP_CUDA(cudaStreamWaitEvent(c->stream, c->ev_pull[1 + q], 0));
 }
 
 void a2a_fwd_rank(sp_ctx* c) {
@@ -933,6 +959,13 @@ int sp_ipc_import(sp_ctx* ctx, const uint8_t* all) {
     for (int j = 0; j < c->D; ++j) rm.base[j] = c->peer_recv[j] + R * c->cumW[c->rank];
     rm.rows_per_part = R;
     rm.parts = c->D;
+    for (int j = 0; j + 1 < c->world; ++j) {
+      cudaStream_t ps = nullptr;
+      SP_CUDA(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking));
+      c->pull_streams.push_back(ps);
+    }
+    c->ev_pull.resize(c->world);
+    for (auto& e : c->ev_pull) SP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c->d_rowmap = dalloc<RowMap>(1, c->owned, c->dev_bytes);
     SP_CUDA(cudaMemcpy(c->d_rowmap, &rm, sizeof(rm), cudaMemcpyHostToDevice));
     c->peer = true;
