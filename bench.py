@@ -321,13 +321,13 @@ def self_launch(args) -> int:
     return subprocess.call(cmd)
 
 
-def allreduce_max(x: float, world: int) -> float:
+def allreduce_max(x: float, world: int, op: str = "max") -> float:
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
     t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return float(t.item())
 
 
@@ -890,6 +890,7 @@ def run_ours(args, world, rank, local):
         shard.run_batch(batch)
     e2e_single_ms = (time.perf_counter() - t0) * 1e3 / 3
     e2e_ms = allreduce_max(e2e_ms, world)
+    h2d_job = int(allreduce_max(float(h2d_local), world, op="sum"))  # every rank's own tables
     del keep
 
     # (before the multi-threaded CPU baseline, whose threads would share the
@@ -966,8 +967,8 @@ def run_ours(args, world, rank, local):
                             "(under the exchanges when N > 1; straight after K1 at N = 1)",
             "roofline": roofline,
             "cpu_baseline": cpu,
-            "e2e": {"value": round(e2e_ms, 3), "unit": UNIT, "h2d_bytes_per_step": h2d_local,
-                    "d2h_bytes_per_step": d2h,
+            "e2e": {"value": round(e2e_ms, 3), "unit": UNIT, "h2d_bytes_per_step": h2d_job,
+                    "d2h_bytes_per_step": d2h * world, "h2d_bytes_per_step_rank0": h2d_local,
                     "path": "EmbeddingShard.run_batches(20 pinned int64 LookupBatches) "
                             "(sp_run_batches: each step's H2D overlaps the previous step's "
                             "compute and its own forward/sort; validation; SGD), wall clock "
