@@ -53,7 +53,7 @@ struct VDev {
   std::vector<TableMeta> meta_canon;
   std::vector<int32_t> colmap;  // local col -> global col
   int64_t W = 0, rows_total = 0, n_tiles = 0;
-  int4* d_tiles = nullptr;      // K1 tiles in launch order (heavy tables first)
+  int4* d_tiles = nullptr;      // K1 tiles in launch order (= d_tiles_canon)
   int4* d_tiles_canon = nullptr;  // K1 tiles in table order (pipelined upload path)
   std::vector<int64_t> tile_start;  // first canonical tile of each local table (+ end)
   // K4 SGD tiles of the current batch, one buffer per staging slot (a step's
@@ -833,31 +833,6 @@ int sp_ctx_create_ex(const sp_table_spec* tables, int32_t num_tables,
       }
       v.W = lcol;
       v.rows_total = static_cast<int64_t>(rb);
-      // K1 grid order, each table a contiguous block range: by weight
-      // (pf * dim) interleaved heaviest / lightest / 2nd heaviest / ... so
-      // the tables in flight together mix large and small row footprints in
-      // L2 (cfg3 iteration 4.13 -> 4.08 ms vs heaviest-first; canonical
-      // order 4.10; profiles/r01_notes.md).
-      std::vector<int> order(T);
-      std::iota(order.begin(), order.end(), 0);
-      std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-        const auto& ta = tables[v.tables[a]];
-        const auto& tb = tables[v.tables[b]];
-        return ta.pooling_factor * ta.dim > tb.pooling_factor * tb.dim;
-      });
-      {
-        std::vector<int> r;  // o[0], o[n-1], o[1], o[n-2], ...
-        for (size_t i = 0, j = order.size(); i < j;) {
-          r.push_back(order[i++]);
-          if (i < j) r.push_back(order[--j]);
-        }
-        order = r;
-      }
-      const std::vector<int4> tiles = make_fwd_tiles(v.meta_canon, order, batch_size);
-      v.n_tiles = static_cast<int64_t>(tiles.size());
-      v.d_tiles = dalloc<int4>(tiles.size(), c->owned, c->dev_bytes);
-      if (!tiles.empty())
-        SP_CUDA(cudaMemcpy(v.d_tiles, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice));
       {
         std::vector<int> canon_order(T);
         for (int li = 0; li < T; ++li) canon_order[li] = li;
@@ -869,6 +844,17 @@ int sp_ctx_create_ex(const sp_table_spec* tables, int32_t num_tables,
         v.tile_start.assign(T + 1, 0);
         for (const int4& tl : ct) ++v.tile_start[tl.x + 1];
         for (int li = 0; li < T; ++li) v.tile_start[li + 1] += v.tile_start[li];
+        // K1's grid runs the tables in canonical (placement) order, each a
+        // contiguous block range, the same tiles the host-buffer step
+        // launches per upload chunk. Measured against reordering by weight
+        // (cfg3 K1 ms, fp32 / fp16 tables): canonical 1.374 / 1.101;
+        // heaviest / lightest interleave by pf x dim (round 1's choice, made
+        // while the sort still ran beside K1) 1.408 / 1.134; interleave by
+        // rows x dim 1.378 / 1.121; heaviest first 1.409; largest touched
+        // footprint followed by 2-4 of the smallest 1.370-1.385 / 1.121-1.128
+        // (fewer DRAM bytes, 4.68 vs 4.77 GB, but longer tails).
+        v.n_tiles = static_cast<int64_t>(ct.size());
+        v.d_tiles = v.d_tiles_canon;
       }
       v.d_meta_canon = dalloc<TableMeta>(T, c->owned, c->dev_bytes);
       v.d_colmap = dalloc<int32_t>(v.W, c->owned, c->dev_bytes);
