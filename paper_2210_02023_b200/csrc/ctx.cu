@@ -53,7 +53,7 @@ struct VDev {
   std::vector<TableMeta> meta_canon;
   std::vector<int32_t> colmap;  // local col -> global col
   int64_t W = 0, rows_total = 0, n_tiles = 0;
-  int4* d_tiles = nullptr;      // K1 tiles in launch order (= d_tiles_canon)
+  int4* d_tiles = nullptr;      // K1 tiles in launch order (lightest tables last)
   int4* d_tiles_canon = nullptr;  // K1 tiles in table order (pipelined upload path)
   std::vector<int64_t> tile_start;  // first canonical tile of each local table (+ end)
   // K4 SGD tiles of the current batch, one buffer per staging slot (a step's
@@ -844,9 +844,10 @@ int sp_ctx_create_ex(const sp_table_spec* tables, int32_t num_tables,
         v.tile_start.assign(T + 1, 0);
         for (const int4& tl : ct) ++v.tile_start[tl.x + 1];
         for (int li = 0; li < T; ++li) v.tile_start[li + 1] += v.tile_start[li];
-        // K1's grid runs the tables in canonical (placement) order, each a
-        // contiguous block range, the same tiles the host-buffer step
-        // launches per upload chunk. Measured against reordering by weight
+        // (d_tiles_canon: the host-buffer step launches K1 per upload chunk
+        // of tables from it.) The iteration's K1 grid runs the tables in
+        // canonical (placement) order too, each a contiguous block range.
+        // Measured against reordering by weight
         // (cfg3 K1 ms, fp32 / fp16 tables): canonical 1.374 / 1.101;
         // heaviest / lightest interleave by pf x dim (round 1's choice, made
         // while the sort still ran beside K1) 1.408 / 1.134; interleave by
@@ -854,7 +855,32 @@ int sp_ctx_create_ex(const sp_table_spec* tables, int32_t num_tables,
         // footprint followed by 2-4 of the smallest 1.370-1.385 / 1.121-1.128
         // (fewer DRAM bytes, 4.68 vs 4.77 GB, but longer tails).
         v.n_tiles = static_cast<int64_t>(ct.size());
-        v.d_tiles = v.d_tiles_canon;
+        // ... except that the lightest tables (pf x dim) run last, lightest
+        // at the very end, so the kernel's tail is short tiles: cfg3 K1
+        // 1.374 -> 1.362 ms fp32 (1.101 -> 1.098 fp16) with 10 of them; 25
+        // the same
+        {
+          constexpr int kLightTail = 10;
+          std::vector<int> light(T);
+          std::iota(light.begin(), light.end(), 0);
+          std::stable_sort(light.begin(), light.end(), [&](int a, int b) {
+            const auto& ta = tables[v.tables[a]];
+            const auto& tb = tables[v.tables[b]];
+            return ta.pooling_factor * ta.dim < tb.pooling_factor * tb.dim;
+          });
+          const int k = std::min(T, kLightTail);
+          std::vector<char> is_tail(T, 0);
+          for (int q = 0; q < k; ++q) is_tail[light[q]] = 1;
+          std::vector<int> ord;
+          for (int li = 0; li < T; ++li)
+            if (!is_tail[li]) ord.push_back(li);
+          for (int q = k - 1; q >= 0; --q) ord.push_back(light[q]);
+          const std::vector<int4> ot = make_fwd_tiles(v.meta_canon, ord, batch_size);
+          v.d_tiles = dalloc<int4>(ot.size(), c->owned, c->dev_bytes);
+          if (!ot.empty())
+            SP_CUDA(cudaMemcpy(v.d_tiles, ot.data(), ot.size() * sizeof(int4),
+                               cudaMemcpyHostToDevice));
+        }
       }
       v.d_meta_canon = dalloc<TableMeta>(T, c->owned, c->dev_bytes);
       v.d_colmap = dalloc<int32_t>(v.W, c->owned, c->dev_bytes);
