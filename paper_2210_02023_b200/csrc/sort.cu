@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(kScanThreads)
     sort_scan_kernel(const SortTable* __restrict__ tabs, int t0, int batch,
                      const int32_t* __restrict__ off, int* __restrict__ cnt,
                      int* __restrict__ bstart, int2* __restrict__ big, int* __restrict__ n_big) {
+  pdl_wait();  // launched as a programmatic dependent (launch_sort_t)
   using BlockScan = cub::BlockScan<int, kScanThreads>;
   __shared__ typename BlockScan::TempStorage tmp;
   const int t = t0 + blockIdx.x;
@@ -267,6 +268,7 @@ __global__ void __launch_bounds__(kThreads, 4)
                         int batch, const int32_t* __restrict__ off,
                         const int32_t* __restrict__ idx, const int* __restrict__ cnt,
                         typename M::type* __restrict__ mid, int nb_max) {
+  pdl_wait();  // launched as a programmatic dependent (launch_sort_t)
   extern __shared__ __align__(16) unsigned char smem[];
   const int wstride = nb_max + 1;  // + the spare cursor of invalid lanes
   uint32_t* whist = reinterpret_cast<uint32_t*>(smem);
@@ -488,6 +490,7 @@ __global__ void __launch_bounds__(kThreads, 4)
                        int n_bk, const int* __restrict__ bstart,
                        typename M::type* __restrict__ mid, uint32_t* __restrict__ keys,
                        BagT* __restrict__ bags, int hw) {
+  pdl_wait();  // launched as a programmatic dependent (launch_sort_t)
   using V = typename M::type;
   extern __shared__ __align__(16) uint32_t smem_u[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -584,6 +587,7 @@ __global__ void __launch_bounds__(kThreads)
                     const int* __restrict__ n_big, const int* __restrict__ bstart,
                     typename M::type* __restrict__ mid, typename M::type* __restrict__ scratch,
                     uint32_t* __restrict__ keys, BagT* __restrict__ bags, int hw) {
+  pdl_wait();  // launched as a programmatic dependent (launch_sort_t)
   using V = typename M::type;
   using BlockScan = cub::BlockScan<uint32_t, kThreads>;
   __shared__ typename BlockScan::TempStorage scan_tmp;
@@ -766,31 +770,33 @@ void launch_sort_t(const SortPlan& pl, const SortTable* d_tabs, const int2* d_ti
   const int hw = hist_words(db_max);
   const unsigned n_tiles = static_cast<unsigned>(w1 - w0);
   const int n_bk = static_cast<int>(k1 - k0);
+  // P2..P4 are launched as programmatic dependents of their predecessor
+  // (each waits for it on entry), so a pass's blocks are scheduled during
+  // the previous pass's tail; the n_big reset goes first so P1 -> P2 is a
+  // kernel-to-kernel edge
+  SP_CUDA(cudaMemsetAsync(d_nbig, 0, sizeof(int), st));
   if (n_tiles > 0) {
     sort_count_kernel<<<n_tiles, kThreads, 0, st>>>(d_tabs, d_tiles + w0, batch, d_off, d_idx,
                                                     d_cnt);
     SP_LAUNCHED();
   }
-  SP_CUDA(cudaMemsetAsync(d_nbig, 0, sizeof(int), st));
-  sort_scan_kernel<<<t1 - t0, kScanThreads, 0, st>>>(d_tabs, t0, batch, d_off, d_cnt, d_bstart,
-                                                     d_big, d_nbig);
-  SP_LAUNCHED();
+  launch_pdl(sort_scan_kernel, dim3(t1 - t0), dim3(kScanThreads), 0, st, d_tabs, t0, batch,
+             d_off, d_cnt, d_bstart, d_big, d_nbig);
   V* mid = static_cast<V*>(d_mid);
-  if (n_tiles > 0) {
-    sort_scatter_kernel<BagT, M><<<n_tiles, kThreads, scatter_smem<BagT>(nb_max), st>>>(
-        d_tabs, d_tiles + w0, batch, d_off, d_idx, d_cnt, mid, nb_max);
-    SP_LAUNCHED();
-  }
+  if (n_tiles > 0)
+    launch_pdl(sort_scatter_kernel<BagT, M>, dim3(n_tiles), dim3(kThreads),
+               scatter_smem<BagT>(nb_max), st, d_tabs, d_tiles + w0, batch, d_off, d_idx,
+               d_cnt, mid, nb_max);
   if (n_bk > 0) {
     const int hws = hist_words(std::min(lo_max, kSmallDigitBits));
-    sort_bucket_kernel<BagT, M><<<(n_bk + kWarps - 1) / kWarps, kThreads, small_smem<V>(hws), st>>>(
-        d_tabs, d_bkts + k0, n_bk, d_bstart, mid, d_keys, static_cast<BagT*>(d_bags), hws);
-    SP_LAUNCHED();
+    launch_pdl(sort_bucket_kernel<BagT, M>, dim3((n_bk + kWarps - 1) / kWarps), dim3(kThreads),
+               small_smem<V>(hws), st, d_tabs, d_bkts + k0, n_bk, d_bstart, mid, d_keys,
+               static_cast<BagT*>(d_bags), hws);
     const int per_sm = std::max(1, static_cast<int>(200 * 1024 / big_smem(hw)));
     const int grid = std::max(1, std::min(n_bk, per_sm * num_sms()));
-    sort_big_kernel<BagT, M><<<grid, kThreads, big_smem(hw), st>>>(
-        d_tabs, d_big, d_nbig, d_bstart, mid, mid + mid_cap, d_keys, static_cast<BagT*>(d_bags), hw);
-    SP_LAUNCHED();
+    launch_pdl(sort_big_kernel<BagT, M>, dim3(grid), dim3(kThreads), big_smem(hw), st, d_tabs,
+               d_big, d_nbig, d_bstart, mid, mid + mid_cap, d_keys, static_cast<BagT*>(d_bags),
+               hw);
   }
 }
 

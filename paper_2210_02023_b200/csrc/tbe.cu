@@ -1104,6 +1104,7 @@ __global__ void sgd_carry_kernel(const TableMeta* __restrict__ meta,
                                  T* __restrict__ w, const float* __restrict__ carry_f,
                                  const int32_t* __restrict__ carry_i,
                                  const int32_t* __restrict__ abort_flag) {
+  pdl_wait();  // a programmatic dependent of sgd_seg_kernel (launch_sgd)
   if (abort_flag != nullptr && *abort_flag != 0) return;
   const int i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -1337,10 +1338,9 @@ void launch_sgd(const TableMeta* d_meta_canon, const int* d_tiles, const int64_t
           d_meta_canon, tiles + counts[0], d_keys, bags, d_grad, ldg, lr, w, d_carry_f,
           d_carry_i, d_abort);
       SP_LAUNCHED();
-      sgd_carry_kernel<T><<<static_cast<unsigned>((counts[1] + 7) / 8), 256, 0, st>>>(
-          d_meta_canon, tiles + counts[0], static_cast<int>(counts[1]), lr, w, d_carry_f,
-          d_carry_i, d_abort);
-      SP_LAUNCHED();
+      launch_pdl(sgd_carry_kernel<T>, dim3(static_cast<unsigned>((counts[1] + 7) / 8)),
+                 dim3(256), 0, st, d_meta_canon, tiles + counts[0],
+                 static_cast<int>(counts[1]), lr, w, d_carry_f, d_carry_i, d_abort);
     }
     if (counts[0] > 0) {
       sgd_kernel<BagT, T><<<static_cast<unsigned>(counts[0]), kBlockThreads, 0, st>>>(
